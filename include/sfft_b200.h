@@ -1,0 +1,246 @@
+/*
+ * libsfftb200 -- C ABI of the B200-native multiple-rank-1-lattice sparse FFT
+ * hot path (arXiv 2006.13053, reference package latfft 0.1.0).
+ *
+ * Two layers:
+ *
+ *  1. The drop-in plugin API.  These four functions are exactly what the
+ *     reference's kernel dispatch module binds (latfft/_kernels/__init__.py,
+ *     reference file:line cited per function).  Host buffers in, host buffers
+ *     out; the host<->device copies happen inside.  INTEGRATION.md shows the
+ *     ctypes stub a maintainer adds to latfft/_kernels/__init__.py.
+ *
+ *  2. Device-resident entry points used by the Python drivers
+ *     (paper_2006_13053_b200.detect / .dimincr).  Device pointers, sizes and
+ *     an explicit cudaStream_t (passed as void*); stream-ordered and
+ *     reentrant.  Buffers are owned by the caller; functions that need
+ *     scratch take a caller-provided workspace whose size a *_workspace_bytes
+ *     query returns.  The only library-owned device state is the Bluestein
+ *     plan cache (chirps / filter spectra keyed by device and M, guarded by
+ *     a mutex), released by sfftb_plan_cache_clear().
+ *
+ * Complex numbers are interleaved (re, im) doubles: numpy complex128 layout.
+ * Every function returns a status code; sfftb_last_error() describes the
+ * last failure on the calling thread.
+ */
+#ifndef SFFT_B200_H
+#define SFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFFTB_OK 0
+#define SFFTB_EINVAL 1 /* -> ParameterError / ValueError */
+#define SFFTB_ENOMEM 2 /* -> MemoryError (the reference's _core.pyx:89-90) */
+#define SFFTB_ECUDA 3  /* -> RuntimeError */
+
+const char *sfftb_version(void);
+const char *sfftb_last_error(void);
+/* Release the cached Bluestein plans of every device. */
+int sfftb_plan_cache_clear(void);
+
+/* ------------------------------------------------------------------ */
+/* 1. plugin API (host buffers)                                        */
+/* ------------------------------------------------------------------ */
+
+/*
+ * Per-candidate hit counts and odd-L coefficient medians.
+ * Replaces latfft._kernels.detect_gather (_kernels/__init__.py:54-70), i.e.
+ * _core.detect_gather (_core.pyx:164-202) / fallback.detect_gather
+ * (fallback.py:106-131).  elems (n, d) int64 must already be reduced mod M
+ * (the reference's precondition, fallback.py:109-110); zmat (L, d) int64;
+ * ghat (L, M) complex128.  hits[i] = #{l : |ghat[l, r_l(i)]| > theta},
+ * r_l(i) = elems[i] . zmat[l] mod M; medians[i] = median_l Re + i median_l Im
+ * when want_medians and hits[i] >= hit_threshold, else 0.  Medians need odd L
+ * (SFFTB_EINVAL otherwise, the reference's ValueError, __init__.py:60-61).
+ */
+int sfftb_detect_gather(const int64_t *elems, int64_t n, int64_t d,
+                        const int64_t *zmat, int64_t L, int64_t M,
+                        const double *ghat, double theta, double hit_threshold,
+                        int want_medians, int64_t *hits, double *medians);
+
+/*
+ * *injective = 1 iff the rows of elems (n, d), reduced componentwise mod p,
+ * are pairwise distinct.  Replaces latfft._kernels.rows_injective_mod
+ * (_kernels/__init__.py:45-51; _core.pyx:103-144 / fallback.py:78-103) with
+ * no 62-bit packing limit (the compiled core's -1 case is handled here).
+ */
+int sfftb_rows_injective_mod(const int64_t *elems, int64_t n, int64_t d,
+                             int64_t p, int *injective);
+
+/*
+ * |{k in Z^d : prod_t max(1, w_t |k_t|) <= bound}| and its lexicographic
+ * enumeration.  Replaces latfft._kernels.hc_count / hc_enumerate
+ * (_kernels/__init__.py:29-42; _core.pyx:24-96).  Host C++ (the recursion
+ * is not data-parallel work).  hc_enumerate writes count*d int64 into out,
+ * which must hold `capacity` rows.
+ */
+int sfftb_hc_count(int d, double bound, const double *weights, int64_t *count);
+int sfftb_hc_enumerate(int d, double bound, const double *weights, int64_t *out,
+                       int64_t capacity);
+
+/* ------------------------------------------------------------------ */
+/* 2. device-resident entry points                                     */
+/* ------------------------------------------------------------------ */
+
+/*
+ * Batched prime-length (any length) DFT by Bluestein chirp-z onto
+ * power-of-two FFTs in FP64 complex.  Row b of x (stride x_stride complex
+ * elements) maps to row b of y:
+ *   y[h] = scale * sum_j x[j] exp(-+2 pi i j h / M)   (sign - forward, + inverse)
+ * dft_forward_normalized (dft.py:18-27) is inverse=0, scale=1/M; the
+ * lattice sampler's M*ifft (polyeval.py:87) is inverse=1, scale=1.
+ * ws: sfftb_dft_workspace_bytes(batch, M) bytes of device memory.
+ */
+int64_t sfftb_dft_workspace_bytes(int64_t batch, int64_t M);
+int sfftb_dft(const double *x, int64_t x_stride, double *y, int64_t y_stride,
+              int64_t batch, int64_t M, int inverse, double scale, void *ws,
+              void *stream);
+
+/* out[b] = sum_j |x[b, j]|^2 (for default_zero_test, detect.py:42-53). */
+int sfftb_sumsq(const double *x, int64_t stride, int64_t batch, int64_t M,
+                double *out, void *stream);
+
+/*
+ * theta[g] = max(1e-12, 1e-10 * median_l sqrt(sumsq[g*L + l] / M)) for each of
+ * G groups of L lattices (default_zero_test, detect.py:42-53; even-L median
+ * averages the middle pair).
+ */
+int sfftb_zero_thresholds(const double *sumsq, int64_t G, int64_t L, int64_t M,
+                          double *theta, void *stream);
+
+/* Words per lattice bitmap: ceil(M/32) rounded up to a multiple of 4. */
+int64_t sfftb_bitmap_words(int64_t M);
+
+/*
+ * bits[(g*L + l)*W + w] bit b = |ghat[g*L + l, 32w + b]| > theta[g] (device
+ * theta, one per group), W = sfftb_bitmap_words(M).  The predicate is
+ * _core.pyx:195's.
+ */
+int sfftb_nonzero_bitmap(const double *ghat, int64_t G, int64_t L, int64_t M,
+                         const double *theta, uint32_t *bits, void *stream);
+
+/*
+ * Candidate hashing + hit counting for G groups of L lattices (shared M):
+ *   hits[g*n + i] = sum_l bit(g, l, elems[i] . zmat[g*L + l] mod M)
+ * elems (n, d) int64 with ARBITRARY signs/magnitudes (the % M of detect.py:132
+ * is fused).  kbound = sum_j max_i |elems[i, j]| when known (enables the
+ * 32-bit residue path), else -1.  hits64 (G*n int64) may be NULL;
+ * detmask[g*ceil(n/32) + w] bit b is set when hits of row 32w+b >= min_hits.
+ */
+int sfftb_hash_hits(const int64_t *elems, int64_t n, int64_t d,
+                    const int64_t *zmat, int64_t G, int64_t L, int64_t M,
+                    const uint32_t *bits, int64_t kbound, int64_t min_hits,
+                    int64_t *hits64, uint32_t *detmask, void *stream);
+
+/*
+ * Ascending indices of set bits per group: idx[g*n + k], counts[g].
+ * ws: sfftb_compact_workspace_bytes(G, n).
+ */
+int64_t sfftb_compact_workspace_bytes(int64_t G, int64_t n);
+int sfftb_compact_mask(const uint32_t *mask, int64_t G, int64_t n, int64_t *idx,
+                       int64_t *counts, void *ws, void *stream);
+
+/*
+ * Odd-L componentwise medians of the L per-lattice values of the compacted
+ * rows: coeffs[g*cap + k] for row idx[g*cap + k], k < counts[g] (device).
+ * The middle element of a stable sort, i.e. the reference's insertion-sort
+ * median (_core.pyx:151-161, :198-200) bit for bit.
+ */
+int sfftb_medians(const int64_t *elems, int64_t d, const int64_t *zmat,
+                  int64_t G, int64_t L, int64_t M, const double *ghat,
+                  const int64_t *idx, const int64_t *counts, int64_t cap,
+                  double *coeffs, void *stream);
+
+/*
+ * Gather the per-lattice values ghat[l, r_l(row)] for listed rows:
+ * out[k*L + l] (per_lattice_coefficients, detect.py:112-119).
+ */
+int sfftb_lattice_values(const int64_t *elems, int64_t d, const int64_t *zmat,
+                         int64_t L, int64_t M, const double *ghat,
+                         const int64_t *rows, int64_t nrows, double *out,
+                         void *stream);
+
+/*
+ * Threshold + top-s selection (detect_topk, detect.py:184-193), per group:
+ * keep |c| >= theta; if more than s_tilde remain keep the s_tilde largest by
+ * (|c| descending, candidate index ascending); output in ascending candidate
+ * order.  In: idx/coeffs[g*cap + k], k < counts[g].  Out: kidx/kcoeffs[g*cap
+ * + k], k < kcounts[g].  ws: sfftb_topk_workspace_bytes(G, cap).
+ */
+int64_t sfftb_topk_workspace_bytes(int64_t G, int64_t cap);
+int sfftb_topk(const int64_t *idx, const double *coeffs, const int64_t *counts,
+               int64_t G, int64_t cap, double theta, int64_t s_tilde,
+               int64_t *kidx, double *kcoeffs, int64_t *kcounts, void *ws,
+               void *stream);
+
+/* Set mask bit i for every listed index (group union, dimincr.py:239-240). */
+int sfftb_mark_indices(const int64_t *idx, const int64_t *counts, int64_t G,
+                       int64_t cap, uint32_t *mask, int64_t n, void *stream);
+
+/* dst[k] = src[rows[k]] for k < *count (device count), rows of d int64. */
+int sfftb_gather_rows(const int64_t *src, int64_t d, const int64_t *rows,
+                      const int64_t *count, int64_t cap, int64_t *dst,
+                      void *stream);
+
+/*
+ * Cartesian candidate builder J = I_prev x I_t in lexicographic order
+ * (pair_candidates, dimincr.py:155-175): out[i*n2 + j] = (prev[i], vals[j]).
+ */
+int sfftb_pair_product(const int64_t *prev, int64_t n1, int64_t t,
+                       const int64_t *vals, int64_t n2, int64_t *out,
+                       void *stream);
+
+/* Per-coordinate (min, max) of n rows: out[2j] = min, out[2j+1] = max. */
+int sfftb_row_bounds(const int64_t *elems, int64_t n, int64_t d, int64_t *out,
+                     void *stream);
+
+/*
+ * Lattice sampler, step 1: anchored coefficients for G fixed tails
+ *   out[g*s + k] = c_k * exp(2 pi i sum_{j >= t_dim} support[k, j] tail[g, j - t_dim])
+ * (the non-lattice coordinates of dimincr.py:188-190 folded into a phase).
+ */
+int sfftb_anchor_coeffs(const int64_t *support, int64_t s, int64_t d,
+                        int64_t t_dim, const double *coeffs, const double *tails,
+                        int64_t G, double *out, void *stream);
+
+/*
+ * Lattice sampler, step 2: residue bins for G*L lattices,
+ *   bins[(g*L + l)*M + h] = sum_{k : support[k, :t_dim] . z[g*L + l] = h mod M} anchored[g*s + k]
+ * summed in ascending k order (deterministic; np.bincount's order,
+ * polyeval.py:85-86).  ws: sfftb_scatter_workspace_bytes(G*L, s).
+ */
+int64_t sfftb_scatter_workspace_bytes(int64_t lattices, int64_t s);
+int sfftb_scatter_bins(const int64_t *support, int64_t s, int64_t d,
+                       int64_t t_dim, const double *anchored,
+                       const int64_t *zmat, int64_t G, int64_t L, int64_t M,
+                       double *bins, void *ws, void *stream);
+
+/*
+ * Dense evaluation p(x) = sum_k c_k exp(2 pi i k . x) at m points X (m, d)
+ * (evaluate_many, polyeval.py:66-75).
+ */
+int sfftb_eval_dense(const int64_t *support, int64_t s, int64_t d,
+                     const double *coeffs, const double *X, int64_t m,
+                     double *out, void *stream);
+
+/*
+ * Harness noise: rows r of x (length M each) get sigma*(N(0,1) + i N(0,1))
+ * from Philox4x32-10 keyed by seed with counter (m, call0 + r)  (the config-5
+ * noise stream; restated in oracle/port.py:noise_for_call).
+ */
+int sfftb_add_noise(double *x, int64_t rows, int64_t M, uint64_t seed,
+                    int64_t call0, double sigma, void *stream);
+
+/* Device injectivity test of n rows mod p; result written to *injective. */
+int sfftb_injective_mod_dev(const int64_t *elems, int64_t n, int64_t d,
+                            int64_t p, int *injective, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFFT_B200_H */

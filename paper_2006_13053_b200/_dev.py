@@ -1,0 +1,79 @@
+"""Device-buffer plumbing: PyTorch is used only for CUDA memory and streams.
+
+All kernels are launched by libsfftb200 on the caller's current torch stream;
+tensors handed to the C ABI are contiguous and their lifetimes are owned by
+the Python side.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+
+_CHECKED = False
+
+
+def device():
+    """The CUDA device; raises if there is none (no CPU fallback exists)."""
+    global _CHECKED
+    if not _CHECKED:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_2006_13053_b200 needs a CUDA device (sm_100a); "
+                "there is no CPU fallback")
+        _native.lib()
+        _CHECKED = True
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    """cudaStream_t of the current torch stream, as an int for ctypes."""
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def upload(arr, dtype=None):
+    """numpy -> contiguous CUDA tensor (int64 / float64 / complex128)."""
+    a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
+    t = torch.from_numpy(a)
+    if t.numel() >= (1 << 20):
+        t = t.pin_memory()
+        return t.to(device(), non_blocking=True)
+    return t.to(device())
+
+
+def download(t):
+    return t.detach().cpu().numpy()
+
+
+def empty(shape, dtype):
+    return torch.empty(shape, dtype=dtype, device=device())
+
+
+def zeros(shape, dtype):
+    return torch.zeros(shape, dtype=dtype, device=device())
+
+
+def workspace(nbytes):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device())
+
+
+def as_i64(t):
+    if isinstance(t, torch.Tensor):
+        if t.device.type != "cuda":
+            t = t.to(device())
+        return t.to(torch.int64).contiguous()
+    return upload(np.asarray(t, dtype=np.int64))
+
+
+def as_c128(t):
+    if isinstance(t, torch.Tensor):
+        if t.device.type != "cuda":
+            t = t.to(device())
+        return t.to(torch.complex128).contiguous()
+    return upload(np.asarray(t, dtype=np.complex128))

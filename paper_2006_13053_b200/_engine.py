@@ -1,0 +1,146 @@
+"""Device pipeline of one detection batch (G groups x L lattices, shared M).
+
+The chain that replaces detect._gather + the compiled gather
+(detect.py:122-169, _core.pyx:164-202) when the samples, generators and
+candidate rows are already in HBM:
+
+  samples (G*L, M)  --sumsq/zero test-->  theta0 (G)          [detect.py:42-53]
+                    --Bluestein DFT----->  ghat (G*L, M)       [detect.py:98-109]
+  ghat, theta0      --bitmap------------>  bits (G*L, W)       [_core.pyx:195]
+  rows J, z, bits   --hash + hits------->  hits, detmask       [_core.pyx:185-197]
+  detmask           --compaction-------->  idx (ascending)     [detect.py:167]
+  idx, ghat         --medians----------->  coeffs              [_core.pyx:198-200]
+  idx, coeffs       --top-s (optional)-->  kept idx, coeffs    [detect.py:184-193]
+
+Nothing here synchronises with the host; callers read counts when they need
+them (one sync per driver stage).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _dev, _native
+from .dft import dft_batch
+
+
+@dataclass
+class Batch:
+    G: int
+    L: int
+    M: int
+    n: int
+    ghat: torch.Tensor
+    theta0: torch.Tensor
+    hits: torch.Tensor | None
+    idx: torch.Tensor | None
+    counts: torch.Tensor | None
+    coeffs: torch.Tensor | None
+
+
+def zero_thresholds(samples, G, L, M):
+    """theta0 per group from the sample RMS (detect.py:42-53) -> (G,) f64."""
+    sumsq = _dev.empty((G * L,), torch.float64)
+    _native.call("sfftb_sumsq", _dev.ptr(samples), M, G * L, M, _dev.ptr(sumsq), _dev.stream())
+    theta = _dev.empty((G,), torch.float64)
+    _native.call("sfftb_zero_thresholds", _dev.ptr(sumsq), G, L, M, _dev.ptr(theta),
+                 _dev.stream())
+    return theta
+
+
+def min_hits_for(nu, L):
+    """detected iff hits >= nu*L (a float) <=> hits >= ceil(nu*L)."""
+    return int(math.ceil(nu * L))
+
+
+def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
+                 want_medians=True, want_hits=False):
+    """Run the full detection chain on device tensors.
+
+    samples (G*L, M) c128; zmat (G*L, d) i64; rows (n, d) i64 (any signs);
+    theta0: (G,) f64 tensor or None (default zero test per group).
+    """
+    n, d = int(rows.shape[0]), int(rows.shape[1])
+    st = _dev.stream()
+    if theta0 is None:
+        theta0 = zero_thresholds(samples, G, L, M)
+    ghat = dft_batch(samples, M)
+    W = int(_native.lib().sfftb_bitmap_words(M))
+    bits = _dev.empty((G * L * W,), torch.int32)
+    _native.call("sfftb_nonzero_bitmap", _dev.ptr(ghat), G, L, M, _dev.ptr(theta0),
+                 _dev.ptr(bits), st)
+    nwords = (n + 31) // 32
+    detmask = _dev.empty((G * max(nwords, 1),), torch.int32)
+    hits = _dev.empty((G * n,), torch.int64) if want_hits else None
+    min_hits = min_hits_for(nu, L)
+    if n:
+        _native.call("sfftb_hash_hits", _dev.ptr(rows), n, d, _dev.ptr(zmat), G, L, M,
+                     _dev.ptr(bits), int(kbound), min_hits, _dev.ptr(hits), _dev.ptr(detmask),
+                     st)
+    idx = _dev.empty((G * max(n, 1),), torch.int64)
+    counts = _dev.zeros((G,), torch.int64)
+    if n:
+        ws = _dev.workspace(_native.lib().sfftb_compact_workspace_bytes(G, n))
+        _native.call("sfftb_compact_mask", _dev.ptr(detmask), G, n, _dev.ptr(idx),
+                     _dev.ptr(counts), _dev.ptr(ws), st)
+    coeffs = None
+    if want_medians:
+        coeffs = _dev.empty((G * max(n, 1),), torch.complex128)
+        if n:
+            _native.call("sfftb_medians", _dev.ptr(rows), d, _dev.ptr(zmat), G, L, M,
+                         _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(counts), n, _dev.ptr(coeffs),
+                         st)
+    return Batch(G, L, M, n, ghat, theta0, hits, idx, counts, coeffs)
+
+
+def topk(idx, coeffs, counts, G, cap, theta, s_tilde):
+    """Threshold + top-s per group (detect.py:184-193) on device."""
+    cap = max(int(cap), 1)
+    kidx = _dev.empty((G * cap,), torch.int64)
+    kco = _dev.empty((G * cap,), torch.complex128)
+    kcounts = _dev.empty((G,), torch.int64)
+    ws = _dev.workspace(_native.lib().sfftb_topk_workspace_bytes(G, cap))
+    _native.call("sfftb_topk", _dev.ptr(idx), _dev.ptr(coeffs), _dev.ptr(counts), G, cap,
+                 float(theta), int(s_tilde), _dev.ptr(kidx), _dev.ptr(kco), _dev.ptr(kcounts),
+                 _dev.ptr(ws), _dev.stream())
+    return kidx, kco, kcounts
+
+
+def union_indices(kidx, kcounts, G, cap, n):
+    """Ascending union of the kept indices of all groups (dimincr.py:239-240).
+
+    Returns (idx (n,) i64 tensor, count (1,) i64 tensor)."""
+    nwords = max((n + 31) // 32, 1)
+    mask = _dev.zeros((nwords,), torch.int32)
+    _native.call("sfftb_mark_indices", _dev.ptr(kidx), _dev.ptr(kcounts), G, max(cap, 1),
+                 _dev.ptr(mask), n, _dev.stream())
+    idx = _dev.empty((max(n, 1),), torch.int64)
+    count = _dev.zeros((1,), torch.int64)
+    if n:
+        ws = _dev.workspace(_native.lib().sfftb_compact_workspace_bytes(1, n))
+        _native.call("sfftb_compact_mask", _dev.ptr(mask), 1, n, _dev.ptr(idx), _dev.ptr(count),
+                     _dev.ptr(ws), _dev.stream())
+    return idx, count
+
+
+def gather_rows(src, rows_idx, count_dev, cap):
+    """dst[k] = src[rows_idx[k]] for k < count (device count)."""
+    d = int(src.shape[1])
+    dst = _dev.empty((max(int(cap), 1), d), torch.int64)
+    _native.call("sfftb_gather_rows", _dev.ptr(src), d, _dev.ptr(rows_idx), _dev.ptr(count_dev),
+                 int(cap), _dev.ptr(dst), _dev.stream())
+    return dst
+
+
+def pair_product(prev, vals):
+    """J = prev x vals in lexicographic order (dimincr.py:155-175)."""
+    n1, t = int(prev.shape[0]), int(prev.shape[1])
+    n2 = int(vals.shape[0])
+    out = _dev.empty((n1 * n2, t + 1), torch.int64)
+    if n1 * n2:
+        _native.call("sfftb_pair_product", _dev.ptr(prev), n1, t, _dev.ptr(vals), n2,
+                     _dev.ptr(out), _dev.stream())
+    return out

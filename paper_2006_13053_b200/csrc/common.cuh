@@ -1,0 +1,83 @@
+// Shared helpers for the sm_100a kernels of libsfftb200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/sfft_b200.h"
+
+namespace sfftb {
+
+// Thread-local error message behind sfftb_last_error().
+void set_error(const std::string& msg);
+
+#define SFFTB_CUDA(call)                                                    \
+    do {                                                                    \
+        cudaError_t err__ = (call);                                         \
+        if (err__ != cudaSuccess) {                                         \
+            ::sfftb::set_error(std::string(#call ": ") +                    \
+                               cudaGetErrorString(err__));                  \
+            return err__ == cudaErrorMemoryAllocation ? SFFTB_ENOMEM        \
+                                                      : SFFTB_ECUDA;        \
+        }                                                                   \
+    } while (0)
+
+#define SFFTB_CHECK_LAUNCH() SFFTB_CUDA(cudaGetLastError())
+
+#define SFFTB_REQUIRE(cond, msg)                                            \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            ::sfftb::set_error(msg);                                        \
+            return SFFTB_EINVAL;                                            \
+        }                                                                   \
+    } while (0)
+
+inline int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// complex double helpers (interleaved re, im == numpy complex128 layout)
+struct cplx {
+    double x, y;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+    return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+    return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+    return make_double2(a.x * s, a.y * s);
+}
+
+// |v| > theta evaluated exactly as the reference's compiled gather does
+// (_core.pyx:195): separately rounded products, one add, IEEE sqrt.
+__device__ __forceinline__ bool nonzero_test(double re, double im, double theta) {
+    double a = __dmul_rn(re, re);
+    double b = __dmul_rn(im, im);
+    return __dsqrt_rn(__dadd_rn(a, b)) > theta;
+}
+
+// Floor-mod of a signed 64-bit integer by M > 0 (result in [0, M)).
+__device__ __forceinline__ int64_t mod_floor(int64_t a, int64_t M) {
+    int64_t r = a % M;
+    return r < 0 ? r + M : r;
+}
+
+}  // namespace sfftb

@@ -1,0 +1,458 @@
+// Batched prime-length DFT in FP64: Bluestein chirp-z onto power-of-two FFTs.
+//
+// Replaces numpy/pocketfft behind dft_forward_normalized (dft.py:18-27) and
+// the inverse transform of the lattice sampler (polyeval.py:87).
+//
+//   X_h = w_h * sum_j (x_j w_j) conj(w_{h-j}),   w_n = exp(-i pi n^2 / M)
+//
+// The linear convolution runs as FFT_N -> * B^ -> IFFT_N with N >= 2M-1 a
+// power of two and B^ = FFT_N(b)/N (b_n = conj(w_|n|), wrapped) precomputed
+// once per M on the host in long double.
+//
+//  * N <= 8192: one CTA per transform, the whole chain in shared memory
+//    (bluestein_small).
+//  * N >= 16384: four-step N = N1*N2 in three kernels over a device workspace:
+//      colA : chirp + length-N2 FFTs down the N1 columns + twiddle
+//      rowB : length-N1 FFT of each row, * B^ (stored row-permuted),
+//             length-N1 IFFT, conjugate twiddle  (forward pass 2, pointwise
+//             product and inverse pass 1 fused in shared memory)
+//      colC : length-N2 IFFTs down the columns + chirp + scale -> output
+//    Each kernel moves its CTA's tile once in and once out, coalesced in
+//    runs of F consecutive complex numbers.
+#include <math.h>
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "fft_core.cuh"
+
+namespace sfftb {
+
+struct BluesteinPlan {
+    int64_t M = 0;
+    int N = 0, N1 = 0, N2 = 0, logN = 0;
+    double2* chirp = nullptr;  // M
+    double2* bhat = nullptr;   // N (natural if N <= 8192, else [k2][k1] = B^[k2 + N2 k1])
+    double2* tw_hi = nullptr;  // N/64 : e^{-2 pi i 64k/N}
+    double2* tw_lo = nullptr;  // 64   : e^{-2 pi i k/N}
+};
+
+static std::mutex g_plan_mu;
+static std::map<std::pair<int, int64_t>, BluesteinPlan*> g_plans;
+
+static constexpr int kSmallMaxLog = 13;  // single-CTA Bluestein up to N = 8192
+static constexpr int kMinLog = 8;        // N >= 256
+static constexpr int kMaxLog = 20;
+
+static int bluestein_log(int64_t M) {
+    int lg = kMinLog;
+    while ((int64_t(1) << lg) < 2 * M - 1) ++lg;
+    return lg;
+}
+
+// iterative radix-2 FFT in long double (plan construction only)
+static void host_fft_ld(std::vector<long double>& re, std::vector<long double>& im) {
+    const size_t n = re.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) {
+            std::swap(re[i], re[j]);
+            std::swap(im[i], im[j]);
+        }
+    }
+    const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<long double> wr(n / 2), wi(n / 2);
+    for (size_t k = 0; k < n / 2; ++k) {
+        long double a = -2.0L * PI * (long double)k / (long double)n;
+        wr[k] = cosl(a);
+        wi[k] = sinl(a);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const size_t half = len >> 1, step = n / len;
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < half; ++k) {
+                long double xr = re[i + k + half], xi = im[i + k + half];
+                long double tr = xr * wr[k * step] - xi * wi[k * step];
+                long double ti = xr * wi[k * step] + xi * wr[k * step];
+                re[i + k + half] = re[i + k] - tr;
+                im[i + k + half] = im[i + k] - ti;
+                re[i + k] += tr;
+                im[i + k] += ti;
+            }
+    }
+}
+
+static int build_plan(int64_t M, BluesteinPlan** out) {
+    SFFTB_REQUIRE(M >= 1, "DFT length must be >= 1");
+    const int lg = bluestein_log(M);
+    SFFTB_REQUIRE(lg <= kMaxLog, "DFT length too large for the Bluestein plan (M <= 524288)");
+    BluesteinPlan* p = new BluesteinPlan();
+    p->M = M;
+    p->logN = lg;
+    p->N = 1 << lg;
+    if (lg > kSmallMaxLog) {
+        p->N1 = 1 << (lg / 2);
+        p->N2 = 1 << (lg - lg / 2);
+    }
+    const int N = p->N;
+    const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<double2> chirp(M), thi(N / 64), tlo(64), bh(N);
+    std::vector<long double> br(N, 0.0L), bi(N, 0.0L);
+    for (int64_t j = 0; j < M; ++j) {
+        const int64_t q = (int64_t)((__int128)j * j % (2 * M));  // exact j^2 mod 2M
+        long double a = -PI * (long double)q / (long double)M;
+        long double c = cosl(a), s = sinl(a);
+        chirp[j] = make_double2((double)c, (double)s);
+        br[j] = c;
+        bi[j] = -s;  // conj
+        if (j > 0) {
+            br[N - j] = c;
+            bi[N - j] = -s;
+        }
+    }
+    for (int k = 0; k < 64; ++k) {
+        long double a = -2.0L * PI * k / N;
+        tlo[k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    for (int k = 0; k < N / 64; ++k) {
+        long double a = -2.0L * PI * (64.0L * k) / N;
+        thi[k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    host_fft_ld(br, bi);
+    for (int k = 0; k < N; ++k) {
+        int dst = k;
+        if (p->N1) {  // B^[k2 + N2 k1] stored at [k2][k1]
+            const int k2 = k % p->N2, k1 = k / p->N2;
+            dst = k2 * p->N1 + k1;
+        }
+        bh[dst] = make_double2((double)(br[k] / N), (double)(bi[k] / N));
+    }
+    auto up = [](double2** d, const std::vector<double2>& h) -> cudaError_t {
+        cudaError_t e = cudaMalloc(d, h.size() * sizeof(double2));
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(*d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    };
+    cudaError_t e;
+    if ((e = up(&p->chirp, chirp)) != cudaSuccess || (e = up(&p->bhat, bh)) != cudaSuccess ||
+        (e = up(&p->tw_hi, thi)) != cudaSuccess || (e = up(&p->tw_lo, tlo)) != cudaSuccess) {
+        cudaFree(p->chirp);
+        cudaFree(p->bhat);
+        cudaFree(p->tw_hi);
+        cudaFree(p->tw_lo);
+        delete p;
+        set_error(std::string("Bluestein plan upload: ") + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SFFTB_ENOMEM : SFFTB_ECUDA;
+    }
+    *out = p;
+    return SFFTB_OK;
+}
+
+static int get_plan(int64_t M, BluesteinPlan** out) {
+    int dev = 0;
+    SFFTB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto key = std::make_pair(dev, M);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {
+        *out = it->second;
+        return SFFTB_OK;
+    }
+    BluesteinPlan* p = nullptr;
+    int rc = build_plan(M, &p);
+    if (rc != SFFTB_OK) return rc;
+    g_plans[key] = p;
+    *out = p;
+    return SFFTB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+struct DftArgs {
+    const double2* x;
+    int64_t xs;
+    double2* y;
+    int64_t ys;
+    int64_t M;
+    double scale;
+    const double2* chirp;
+    const double2* bhat;
+    const double2* tw_hi;
+    const double2* tw_lo;
+    double2* work;  // four-step workspace, batch * N
+};
+
+template <bool C>
+__device__ __forceinline__ double2 conj_if(double2 v) {
+    return C ? make_double2(v.x, -v.y) : v;
+}
+
+// One CTA per transform; N/16 threads.
+template <int N, bool INV>
+__global__ void __launch_bounds__(N / 16) bluestein_small(DftArgs a) {
+    extern __shared__ double2 smem[];
+    const int tid = threadIdx.x;
+    constexpr int T = N / 16;
+    const int64_t b = blockIdx.x;
+    const double2* x = a.x + b * a.xs;
+    for (int i = tid; i < N; i += T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (i < a.M) v = cmul(conj_if<INV>(x[i]), a.chirp[i]);
+        smem[pad16(i)] = v;
+    }
+    __syncthreads();
+    fft_smem<N, false>(smem, tid, a.tw_hi, a.tw_lo, 1);
+    for (int i = tid; i < N; i += T) smem[pad16(i)] = cmul(smem[pad16(i)], a.bhat[i]);
+    __syncthreads();
+    fft_smem<N, true>(smem, tid, a.tw_hi, a.tw_lo, 1);
+    double2* y = a.y + b * a.ys;
+    for (int h = tid; h < a.M; h += T) {
+        double2 v = cmul(a.chirp[h], smem[pad16(h)]);
+        y[h] = cscale(conj_if<INV>(v), a.scale);
+    }
+}
+
+// colA: CTA = F columns n1 of the N1 x N2 view, length-N2 forward FFTs.
+template <int N2, bool INV>
+__global__ void __launch_bounds__(256) fs_colA(DftArgs a, int N1) {
+    constexpr int TPF = N2 / 16, F = 256 / TPF, SLOT = N2 + N2 / 16;
+    extern __shared__ double2 smem[];
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const int n1_0 = blockIdx.x * F;
+    const int N = N1 * N2;
+    const double2* x = a.x + b * a.xs;
+    for (int e = tid; e < F * N2; e += 256) {
+        const int f = e % F, n2 = e / F;
+        const int64_t j = n1_0 + f + (int64_t)N1 * n2;
+        double2 v = make_double2(0.0, 0.0);
+        if (j < a.M) v = cmul(conj_if<INV>(x[j]), a.chirp[j]);
+        smem[f * SLOT + pad16(n2)] = v;
+    }
+    __syncthreads();
+    const int f_me = tid / TPF;
+    fft_smem<N2, false>(smem + f_me * SLOT, tid % TPF, a.tw_hi, a.tw_lo, N1);
+    double2* T = a.work + b * (int64_t)N;
+    for (int e = tid; e < F * N2; e += 256) {
+        const int f = e % F, k2 = e / F;
+        const int n1 = n1_0 + f;
+        double2 v = smem[f * SLOT + pad16(k2)];
+        const int ex = n1 * k2;  // < N
+        if (ex) v = cmul(v, twiddle2<false>(a.tw_hi, a.tw_lo, ex));
+        T[(int64_t)k2 * N1 + n1] = v;
+    }
+}
+
+// rowB: CTA = F rows k2, forward FFT_N1 -> * B^ -> inverse FFT_N1 -> conj twiddle.
+template <int N1>
+__global__ void __launch_bounds__(256) fs_rowB(DftArgs a, int N2) {
+    constexpr int TPF = N1 / 16, F = 256 / TPF, SLOT = N1 + N1 / 16;
+    extern __shared__ double2 smem[];
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const int k2_0 = blockIdx.x * F;
+    const int N = N1 * N2;
+    double2* T = a.work + b * (int64_t)N;
+    for (int e = tid; e < F * N1; e += 256) {
+        const int f = e / N1, n1 = e % N1;
+        smem[f * SLOT + pad16(n1)] = T[(int64_t)(k2_0 + f) * N1 + n1];
+    }
+    __syncthreads();
+    const int f_me = tid / TPF;
+    double2* mine = smem + f_me * SLOT;
+    fft_smem<N1, false>(mine, tid % TPF, a.tw_hi, a.tw_lo, N2);
+    for (int e = tid; e < F * N1; e += 256) {
+        const int f = e / N1, k1 = e % N1;
+        smem[f * SLOT + pad16(k1)] =
+            cmul(smem[f * SLOT + pad16(k1)], a.bhat[(int64_t)(k2_0 + f) * N1 + k1]);
+    }
+    __syncthreads();
+    fft_smem<N1, true>(mine, tid % TPF, a.tw_hi, a.tw_lo, N2);
+    for (int e = tid; e < F * N1; e += 256) {
+        const int f = e / N1, m1 = e % N1;
+        const int k2 = k2_0 + f;
+        double2 v = smem[f * SLOT + pad16(m1)];
+        const int ex = m1 * k2;
+        if (ex) v = cmul(v, twiddle2<true>(a.tw_hi, a.tw_lo, ex));
+        T[(int64_t)k2 * N1 + m1] = v;
+    }
+}
+
+// colC: CTA = F columns m1, inverse length-N2 FFTs, chirp, scale, output.
+template <int N2, bool INV>
+__global__ void __launch_bounds__(256) fs_colC(DftArgs a, int N1) {
+    constexpr int TPF = N2 / 16, F = 256 / TPF, SLOT = N2 + N2 / 16;
+    extern __shared__ double2 smem[];
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const int m1_0 = blockIdx.x * F;
+    const int N = N1 * N2;
+    const double2* T = a.work + b * (int64_t)N;
+    for (int e = tid; e < F * N2; e += 256) {
+        const int f = e % F, k2 = e / F;
+        smem[f * SLOT + pad16(k2)] = T[(int64_t)k2 * N1 + m1_0 + f];
+    }
+    __syncthreads();
+    const int f_me = tid / TPF;
+    fft_smem<N2, true>(smem + f_me * SLOT, tid % TPF, a.tw_hi, a.tw_lo, N1);
+    double2* y = a.y + b * a.ys;
+    for (int e = tid; e < F * N2; e += 256) {
+        const int f = e % F, m2 = e / F;
+        const int64_t h = m1_0 + f + (int64_t)N1 * m2;
+        if (h < a.M) {
+            double2 v = cmul(a.chirp[h], smem[f * SLOT + pad16(m2)]);
+            y[h] = cscale(conj_if<INV>(v), a.scale);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+
+template <typename K>
+static cudaError_t allow_smem(K kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int N, bool INV>
+static int launch_small(const DftArgs& a, int64_t batch, cudaStream_t st) {
+    const size_t sm = sizeof(double2) * (N + N / 16);
+    SFFTB_CUDA(allow_smem(bluestein_small<N, INV>, sm));
+    bluestein_small<N, INV><<<(unsigned)batch, N / 16, sm, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <bool INV>
+static int small_dispatch(int lg, const DftArgs& a, int64_t batch, cudaStream_t st) {
+    switch (lg) {
+        case 8: return launch_small<256, INV>(a, batch, st);
+        case 9: return launch_small<512, INV>(a, batch, st);
+        case 10: return launch_small<1024, INV>(a, batch, st);
+        case 11: return launch_small<2048, INV>(a, batch, st);
+        case 12: return launch_small<4096, INV>(a, batch, st);
+        case 13: return launch_small<8192, INV>(a, batch, st);
+    }
+    set_error("internal: bad small Bluestein size");
+    return SFFTB_EINVAL;
+}
+
+template <int N2, bool INV>
+static int launch_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bool first) {
+    constexpr int F = 256 / (N2 / 16);
+    const size_t sm = sizeof(double2) * F * (N2 + N2 / 16);
+    dim3 grid(N1 / F, (unsigned)batch);
+    if (first) {
+        SFFTB_CUDA(allow_smem(fs_colA<N2, INV>, sm));
+        fs_colA<N2, INV><<<grid, 256, sm, st>>>(a, N1);
+    } else {
+        SFFTB_CUDA(allow_smem(fs_colC<N2, INV>, sm));
+        fs_colC<N2, INV><<<grid, 256, sm, st>>>(a, N1);
+    }
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <int N1>
+static int launch_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
+    constexpr int F = 256 / (N1 / 16);
+    const size_t sm = sizeof(double2) * F * (N1 + N1 / 16);
+    SFFTB_CUDA(allow_smem(fs_rowB<N1>, sm));
+    fs_rowB<N1><<<dim3(N2 / F, (unsigned)batch), 256, sm, st>>>(a, N2);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <bool INV>
+static int cols_dispatch(int N2, const DftArgs& a, int64_t batch, int N1, cudaStream_t st,
+                         bool first) {
+    switch (N2) {
+        case 128: return launch_cols<128, INV>(a, batch, N1, st, first);
+        case 256: return launch_cols<256, INV>(a, batch, N1, st, first);
+        case 512: return launch_cols<512, INV>(a, batch, N1, st, first);
+        case 1024: return launch_cols<1024, INV>(a, batch, N1, st, first);
+    }
+    set_error("internal: bad four-step column size");
+    return SFFTB_EINVAL;
+}
+
+static int rows_dispatch(int N1, const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
+    switch (N1) {
+        case 128: return launch_rows<128>(a, batch, N2, st);
+        case 256: return launch_rows<256>(a, batch, N2, st);
+        case 512: return launch_rows<512>(a, batch, N2, st);
+        case 1024: return launch_rows<1024>(a, batch, N2, st);
+    }
+    set_error("internal: bad four-step row size");
+    return SFFTB_EINVAL;
+}
+
+}  // namespace sfftb
+
+using namespace sfftb;
+
+extern "C" int64_t sfftb_dft_workspace_bytes(int64_t batch, int64_t M) {
+    if (batch <= 0 || M <= 0) return 0;
+    const int lg = bluestein_log(M);
+    if (lg <= kSmallMaxLog) return 0;
+    return batch * (int64_t(1) << lg) * (int64_t)sizeof(double2);
+}
+
+extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y_stride,
+                         int64_t batch, int64_t M, int inverse, double scale, void* ws,
+                         void* stream) {
+    SFFTB_REQUIRE(batch >= 0 && M >= 1, "dft: bad sizes");
+    if (batch == 0) return SFFTB_OK;
+    SFFTB_REQUIRE(batch <= 65535 || bluestein_log(M) <= kSmallMaxLog,
+                  "dft: batch too large for one launch");
+    BluesteinPlan* p = nullptr;
+    int rc = get_plan(M, &p);
+    if (rc != SFFTB_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    DftArgs a;
+    a.x = (const double2*)x;
+    a.xs = x_stride;
+    a.y = (double2*)y;
+    a.ys = y_stride;
+    a.M = M;
+    a.scale = scale;
+    a.chirp = p->chirp;
+    a.bhat = p->bhat;
+    a.tw_hi = p->tw_hi;
+    a.tw_lo = p->tw_lo;
+    a.work = (double2*)ws;
+    if (p->logN <= kSmallMaxLog)
+        return inverse ? small_dispatch<true>(p->logN, a, batch, st)
+                       : small_dispatch<false>(p->logN, a, batch, st);
+    SFFTB_REQUIRE(ws != nullptr, "dft: workspace required");
+    rc = inverse ? cols_dispatch<true>(p->N2, a, batch, p->N1, st, true)
+                 : cols_dispatch<false>(p->N2, a, batch, p->N1, st, true);
+    if (rc != SFFTB_OK) return rc;
+    rc = rows_dispatch(p->N1, a, batch, p->N2, st);
+    if (rc != SFFTB_OK) return rc;
+    return inverse ? cols_dispatch<true>(p->N2, a, batch, p->N1, st, false)
+                   : cols_dispatch<false>(p->N2, a, batch, p->N1, st, false);
+}
+
+extern "C" int sfftb_plan_cache_clear(void) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (auto& kv : g_plans) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second->chirp);
+        cudaFree(kv.second->bhat);
+        cudaFree(kv.second->tw_hi);
+        cudaFree(kv.second->tw_lo);
+        cudaSetDevice(cur);
+        delete kv.second;
+    }
+    g_plans.clear();
+    return SFFTB_OK;
+}

@@ -1,0 +1,166 @@
+// Power-of-two FP64 complex FFTs held in shared memory (Stockham autosort,
+// radix 16/8/4/2 butterflies in registers).  Building block of the Bluestein
+// prime-length DFT in fft.cu.
+//
+// Layout: one FFT of length n occupies n*17/16 double2 slots (one pad slot
+// per 16 elements, pad(i) = i + i/16) so that the stride-R stores of the
+// first Stockham pass do not serialise on shared-memory banks.
+#pragma once
+
+#include "common.cuh"
+
+namespace sfftb {
+
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
+
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+// e^{-2 pi i k / 16}, k < 16, correctly rounded literals.
+__device__ __forceinline__ double2 w16(int k) {
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+    constexpr double c2 = 0.70710678118654752440;
+    switch (k & 15) {
+        case 0: return make_double2(1.0, 0.0);
+        case 1: return make_double2(c1, -s1);
+        case 2: return make_double2(c2, -c2);
+        case 3: return make_double2(s1, -c1);
+        case 4: return make_double2(0.0, -1.0);
+        case 5: return make_double2(-s1, -c1);
+        case 6: return make_double2(-c2, -c2);
+        case 7: return make_double2(-c1, -s1);
+        case 8: return make_double2(-1.0, 0.0);
+        case 9: return make_double2(-c1, s1);
+        case 10: return make_double2(-c2, c2);
+        case 11: return make_double2(-s1, c1);
+        case 12: return make_double2(0.0, 1.0);
+        case 13: return make_double2(s1, c1);
+        case 14: return make_double2(c2, c2);
+        default: return make_double2(c1, s1);
+    }
+}
+
+// multiply by e^{-+2 pi i k/16} with the trivial factors special-cased
+template <bool INV>
+__device__ __forceinline__ double2 mul_w16(double2 v, int k) {
+    k &= 15;
+    if (k == 0) return v;
+    if (k == 4) return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+    if (k == 8) return make_double2(-v.x, -v.y);
+    if (k == 12) return INV ? make_double2(v.y, -v.x) : make_double2(-v.y, v.x);
+    double2 w = w16(k);
+    if (INV) w.y = -w.y;
+    return cmul(v, w);
+}
+
+// In-register radix-R DFT (R in {2,4,8,16}), natural order in and out,
+// iterative radix-2 DIT on bit-reversed inputs; all indices compile-time.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(double2 (&v)[R]) {
+    constexpr int LR = ilog2c(R);
+    double2 t[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        int rev = 0;
+#pragma unroll
+        for (int b = 0; b < LR; ++b) rev |= ((i >> b) & 1) << (LR - 1 - b);
+        t[rev] = v[i];
+    }
+#pragma unroll
+    for (int s = 1; s <= LR; ++s) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int m = 1 << s, h = m >> 1;
+#pragma unroll
+        for (int k = 0; k < R; k += m) {
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                // twiddle e^{-2 pi i j/m} = w16(j * 16/m)
+                double2 u = t[k + j];
+                double2 x = mul_w16<INV>(t[k + j + h], j * (16 / m));
+                t[k + j] = cadd(u, x);
+                t[k + j + h] = csub(u, x);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+// Twiddle e^{-+2 pi i e / NT} from a two-level table:
+// tw_hi[e >> 6] * tw_lo[e & 63] (both tables hold e^{-2 pi i (.)/NT}).
+template <bool INV>
+__device__ __forceinline__ double2 twiddle2(const double2* __restrict__ tw_hi,
+                                            const double2* __restrict__ tw_lo, int e) {
+    double2 a = tw_hi[e >> 6];
+    double2 w = (e & 63) ? cmul(a, tw_lo[e & 63]) : a;
+    if (INV) w.y = -w.y;
+    return w;
+}
+
+// Largest radix (<= 16) for the next Stockham pass given remaining log2 size.
+__host__ __device__ constexpr int pass_radix(int rem_log) {
+    return rem_log >= 4 ? 16 : (1 << rem_log);
+}
+
+// One Stockham pass of radix R over FPC FFTs of length N (threads per FFT
+// TPF = N/16, each thread owns 16 elements = 16/R butterflies).
+// Twiddle exponent for butterfly j, output r: (j mod Ns) * r * (N/(Ns R)) in
+// units of e^{-2 pi i / N}; global exponent scale `tscale` maps it into the
+// table's NT (NT = N * tscale).
+template <int N, int R, bool INV>
+__device__ __forceinline__ void stockham_pass(double2* __restrict__ buf, int tpf_id, int Ns,
+                                              const double2* __restrict__ tw_hi,
+                                              const double2* __restrict__ tw_lo,
+                                              int tscale) {
+    constexpr int TPF = N / 16;
+    constexpr int BPT = 16 / R;  // butterflies per thread
+    double2 v[BPT][R];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int j = tpf_id + q * TPF;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = buf[pad16(j + r * (N / R))];
+        if (Ns > 1) {
+            const int jm = j % Ns;
+            const int step = jm * (N / (Ns * R));
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const int e = (step * r) % N;
+                if (e) v[q][r] = cmul(v[q][r], twiddle2<INV>(tw_hi, tw_lo, e * tscale));
+            }
+        }
+        dft_reg<R, INV>(v[q]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int j = tpf_id + q * TPF;
+        const int base = (j / Ns) * Ns * R + (j % Ns);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad16(base + r * Ns)] = v[q][r];
+    }
+    __syncthreads();
+}
+
+template <int N, int NS, int REM, bool INV>
+struct StockhamRun {
+    __device__ __forceinline__ static void run(double2* buf, int tpf_id, const double2* tw_hi,
+                                               const double2* tw_lo, int tscale) {
+        constexpr int R = pass_radix(REM);
+        stockham_pass<N, R, INV>(buf, tpf_id, NS, tw_hi, tw_lo, tscale);
+        StockhamRun<N, NS * R, REM - ilog2c(R), INV>::run(buf, tpf_id, tw_hi, tw_lo, tscale);
+    }
+};
+template <int N, int NS, bool INV>
+struct StockhamRun<N, NS, 0, INV> {
+    __device__ __forceinline__ static void run(double2*, int, const double2*, const double2*, int) {}
+};
+
+// Full length-N FFT on buf (caller syncs before; ends synced).  N >= 16.
+template <int N, bool INV>
+__device__ __forceinline__ void fft_smem(double2* buf, int tpf_id, const double2* tw_hi,
+                                         const double2* tw_lo, int tscale) {
+    StockhamRun<N, 1, ilog2c(N), INV>::run(buf, tpf_id, tw_hi, tw_lo, tscale);
+}
+
+}  // namespace sfftb

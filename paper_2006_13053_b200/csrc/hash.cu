@@ -1,0 +1,763 @@
+// Candidate hashing, hit counting, detected-row compaction and medians.
+//
+// Replaces the reference's per-candidate gather (latfft/_kernels/_core.pyx:
+// 164-202; semantics of fallback.py:106-131) and the index bookkeeping of
+// detect.py:122-169.
+//
+// Design:
+//  * the L*M per-lattice values are reduced once to nonzero BITMAPS
+//    (bit = |ghat| > theta, the exact predicate of _core.pyx:195) which live
+//    in shared memory, W = ceil(M/32) words per lattice;
+//  * each thread keeps R candidate rows in registers and walks the lattices:
+//    residue by 32-bit IMAD chain (exact when sum_j max|k_j| * M/2 fits, the
+//    common case, checked on the host) or a 64-bit chain otherwise, then a
+//    multiply-high modular reduction and one bitmap probe per (row, lattice);
+//  * when the bitmaps of all L lattices exceed the shared-memory budget they
+//    are streamed through shared memory in lattice chunks per row tile;
+//  * detected rows (hits >= nu*L) leave a warp-ballot bitmask that
+//    sfftb_compact_mask turns into ascending indices; medians are computed
+//    only for those rows, one warp per row.
+#include "common.cuh"
+
+namespace sfftb {
+
+static constexpr int kHashThreads = 256;
+static constexpr size_t kBitmapSmemBudget = 192 * 1024;
+
+struct HashArgs {
+    const int64_t* elems;
+    int64_t n;
+    int d;
+    const int64_t* zmat;  // G*L*d
+    int G, L;
+    int64_t M;
+    const uint32_t* bits;  // G*L*W
+    int64_t W;
+    int Lc;              // lattices per shared-memory chunk
+    uint32_t offset;     // multiple of M >= |residue sum| (32-bit path)
+    uint32_t magic;      // floor((2^32-1)/M)
+    int64_t min_hits;
+    int64_t* hits64;     // may be null
+    uint32_t* detmask;   // G * ceil(n/32)
+    int64_t nwords;
+};
+
+__device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t M, uint32_t magic) {
+    uint32_t q = __umulhi(u, magic);  // q in {floor(u/M)-1, floor(u/M)}
+    uint32_t r = u - q * M;           // r in [0, 2M)
+    return min(r, r - M);
+}
+
+__device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t M, double invM) {
+    // u < 2^62: the double estimate is off by at most a few units
+    int64_t q = (int64_t)((double)u * invM);
+    int64_t r = (int64_t)u - q * (int64_t)M;
+    while (r < 0) r += M;
+    while (r >= (int64_t)M) r -= M;
+    return (uint64_t)r;
+}
+
+// Load the bitmaps of lattices [l0, l0+cnt) of group g into shared memory.
+__device__ __forceinline__ void load_bits(uint32_t* dst, const HashArgs& a, int g, int l0,
+                                          int cnt) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.bits + ((int64_t)g * a.L + l0) * a.W);
+    const int64_t words = (int64_t)cnt * a.W;
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    // a.W is padded to a multiple of 4 words by the host
+    for (int64_t i = threadIdx.x; i < words / 4; i += blockDim.x) d4[i] = __ldg(src + i);
+}
+
+// WIDE = false: 32-bit residue path (values truncated to int32, exact by the
+// host's bound check); WIDE = true: exact 64-bit path for any int64 input.
+template <int D, int R, bool WIDE>
+__global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
+    extern __shared__ uint32_t smem_u32[];
+    const int g = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int WARPS = kHashThreads / 32;
+    constexpr int TILE = WARPS * 32 * R;
+    const uint32_t M32 = (uint32_t)a.M;
+
+    // generators of this group, centered (32-bit path) or as-is (64-bit path)
+    int32_t* zc = reinterpret_cast<int32_t*>(smem_u32);
+    const int zwords = ((a.L * D + 3) & ~3);
+    uint32_t* bm = smem_u32 + zwords;
+    for (int i = threadIdx.x; i < a.L * D; i += blockDim.x) {
+        int64_t z = a.zmat[(int64_t)g * a.L * D + i] % a.M;
+        if (z < 0) z += a.M;
+        if (!WIDE && z > a.M / 2) z -= a.M;
+        zc[i] = (int32_t)z;
+    }
+    const int nchunks = (a.L + a.Lc - 1) / a.Lc;
+    if (nchunks == 1) load_bits(bm, a, g, 0, a.L);
+    __syncthreads();
+
+    const double invM = 1.0 / (double)a.M;
+    const int64_t ntiles = (a.n + TILE - 1) / TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * TILE + (int64_t)warp * 32 * R;
+        // rows in registers: row base + q*32 + lane
+        int32_t k[R][D];
+        uint32_t ku[WIDE ? R : 1][WIDE ? D : 1];
+        bool valid[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int64_t i = base + q * 32 + lane;
+            valid[q] = i < a.n;
+            const int64_t* row = a.elems + (valid[q] ? i : 0) * D;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                int64_t v = valid[q] ? __ldg(row + j) : 0;
+                if (WIDE) {
+                    int64_t m = v % a.M;
+                    if (m < 0) m += a.M;
+                    ku[WIDE ? q : 0][WIDE ? j : 0] = (uint32_t)m;
+                    k[q][j] = 0;
+                } else {
+                    k[q][j] = (int32_t)v;
+                }
+            }
+        }
+        int hits[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) hits[q] = 0;
+
+        for (int c = 0; c < nchunks; ++c) {
+            const int l0 = c * a.Lc;
+            const int lend = min(a.L, l0 + a.Lc);
+            if (nchunks > 1) {
+                __syncthreads();
+                load_bits(bm, a, g, l0, lend - l0);
+                __syncthreads();
+            }
+            for (int l = l0; l < lend; ++l) {
+                const int32_t* z = zc + l * D;
+                int32_t zr[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) zr[j] = z[j];
+                const uint32_t* bl = bm + (int64_t)(l - l0) * a.W;
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    uint32_t r;
+                    if (!WIDE) {
+                        uint32_t u = a.offset;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) u += (uint32_t)k[q][j] * (uint32_t)zr[j];
+                        r = mod_u32(u, M32, a.magic);
+                    } else {
+                        uint64_t acc = 0;
+#pragma unroll
+                        for (int j = 0; j < D; ++j)
+                            acc += (uint64_t)ku[WIDE ? q : 0][WIDE ? j : 0] * (uint32_t)zr[j];
+                        r = (uint32_t)mod_u64(acc, (uint64_t)a.M, invM);
+                    }
+                    const uint32_t w = bl[r >> 5];
+                    hits[q] += (w >> (r & 31)) & 1u;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int64_t i = base + q * 32 + lane;
+            const unsigned det = __ballot_sync(0xffffffffu, valid[q] && hits[q] >= a.min_hits);
+            if (valid[q] && a.hits64) a.hits64[(int64_t)g * a.n + i] = hits[q];
+            if (lane == 0 && (base + q * 32) < a.n)
+                a.detmask[(int64_t)g * a.nwords + ((base + q * 32) >> 5)] = det;
+        }
+    }
+}
+
+// Generic fallback: any d (runtime), one row per thread, exact 64-bit.
+__global__ void __launch_bounds__(kHashThreads) hash_rows_generic(HashArgs a) {
+    extern __shared__ uint32_t smem_u32[];
+    const int g = blockIdx.y;
+    uint32_t* bm = smem_u32;
+    const int nchunks = (a.L + a.Lc - 1) / a.Lc;
+    if (nchunks == 1) load_bits(bm, a, g, 0, a.L);
+    __syncthreads();
+    const int64_t ntiles = (a.n + kHashThreads - 1) / kHashThreads;
+    const int lane = threadIdx.x & 31;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * kHashThreads + threadIdx.x;
+        const bool valid = i < a.n;
+        int hits = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int l0 = c * a.Lc;
+            const int lend = min(a.L, l0 + a.Lc);
+            if (nchunks > 1) {
+                __syncthreads();
+                load_bits(bm, a, g, l0, lend - l0);
+                __syncthreads();
+            }
+            if (!valid) continue;
+            for (int l = l0; l < lend; ++l) {
+                const int64_t* z = a.zmat + ((int64_t)g * a.L + l) * a.d;
+                unsigned __int128 acc = 0;
+                for (int j = 0; j < a.d; ++j) {
+                    int64_t e = a.elems[i * a.d + j] % a.M;
+                    if (e < 0) e += a.M;
+                    int64_t zz = z[j] % a.M;
+                    if (zz < 0) zz += a.M;
+                    acc += (unsigned __int128)((uint64_t)e * (uint64_t)zz);
+                }
+                const uint32_t r = (uint32_t)(acc % (unsigned __int128)a.M);
+                const uint32_t w = bm[(int64_t)(l - l0) * a.W + (r >> 5)];
+                hits += (w >> (r & 31)) & 1u;
+            }
+        }
+        const unsigned det = __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
+        if (valid && a.hits64) a.hits64[(int64_t)g * a.n + i] = hits;
+        if (lane == 0 && (tile * kHashThreads + (threadIdx.x & ~31)) < a.n)
+            a.detmask[(int64_t)g * a.nwords + ((tile * kHashThreads + (threadIdx.x & ~31)) >> 5)] =
+                det;
+    }
+}
+
+// ---------------------------------------------------------------------------
+
+__global__ void nonzero_bitmap_kernel(const double2* __restrict__ ghat, int64_t rows, int L,
+                                      int64_t M, int64_t W, const double* __restrict__ theta,
+                                      uint32_t* __restrict__ bits) {
+    const int64_t total = rows * W;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / W, w = e % W;
+        const double th = theta[row / L];
+        uint32_t word = 0;
+        const int64_t h0 = w * 32;
+        const double2* src = ghat + row * M;
+#pragma unroll 4
+        for (int b = 0; b < 32; ++b) {
+            const int64_t h = h0 + b;
+            if (h < M) {
+                const double2 v = src[h];
+                word |= (uint32_t)nonzero_test(v.x, v.y, th) << b;
+            }
+        }
+        bits[e] = word;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// compaction of a per-row bitmask into ascending indices
+// ---------------------------------------------------------------------------
+
+static constexpr int kCompactWordsPerBlock = 4096;
+static constexpr int kCompactThreads = 256;
+
+__global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
+                              int64_t nblk, int64_t* __restrict__ blocksum) {
+    const int g = blockIdx.y;
+    const int64_t w0 = blockIdx.x * (int64_t)kCompactWordsPerBlock;
+    int64_t s = 0;
+    for (int64_t w = w0 + threadIdx.x; w < min(nwords, w0 + kCompactWordsPerBlock);
+         w += blockDim.x)
+        s += __popc(mask[(int64_t)g * nwords + w]);
+    __shared__ int64_t red[kCompactThreads];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) blocksum[(int64_t)g * nblk + blockIdx.x] = red[0];
+}
+
+__global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts) {
+    const int g = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    int64_t run = 0;
+    for (int64_t b = 0; b < nblk; ++b) {
+        const int64_t v = blocksum[(int64_t)g * nblk + b];
+        blocksum[(int64_t)g * nblk + b] = run;
+        run += v;
+    }
+    counts[g] = run;
+}
+
+__global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords, int64_t n,
+                              int64_t nblk, const int64_t* __restrict__ blocksum,
+                              int64_t* __restrict__ idx) {
+    const int g = blockIdx.y;
+    const int64_t w0 = blockIdx.x * (int64_t)kCompactWordsPerBlock;
+    __shared__ int64_t warp_tot[kCompactThreads / 32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = blocksum[(int64_t)g * nblk + blockIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t c0 = w0; c0 < min(nwords, w0 + kCompactWordsPerBlock); c0 += blockDim.x) {
+        const int64_t w = c0 + threadIdx.x;
+        const uint32_t bitsw = (w < nwords && w < w0 + kCompactWordsPerBlock)
+                                   ? mask[(int64_t)g * nwords + w]
+                                   : 0u;
+        int cnt = __popc(bitsw);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        int64_t before = carry;
+        for (int k = 0; k < warp; ++k) before += warp_tot[k];
+        int64_t pos = before + incl - cnt;
+        uint32_t b = bitsw;
+        while (b) {
+            const int bit = __ffs(b) - 1;
+            b &= b - 1;
+            const int64_t row = w * 32 + bit;
+            if (row < n) idx[(int64_t)g * n + pos++] = row;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t t = 0;
+            for (int k = 0; k < kCompactThreads / 32; ++k) t += warp_tot[k];
+            carry += t;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// medians (one warp per detected row, L <= 128)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t residue_exact(const int64_t* row, const int64_t* z, int d,
+                                                 int64_t M) {
+    uint64_t acc = 0;
+    for (int j = 0; j < d; ++j) {
+        int64_t e = row[j] % M;
+        if (e < 0) e += M;
+        int64_t zz = z[j] % M;
+        if (zz < 0) zz += M;
+        acc = (acc + (uint64_t)(((unsigned __int128)e * (uint64_t)zz) % (uint64_t)M)) %
+              (uint64_t)M;
+    }
+    return (int64_t)acc;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict__ elems, int d,
+                                                      const int64_t* __restrict__ zmat, int G,
+                                                      int L, int64_t M,
+                                                      const double2* __restrict__ ghat,
+                                                      const int64_t* __restrict__ idx,
+                                                      const int64_t* __restrict__ counts,
+                                                      int64_t cap, double2* __restrict__ coeffs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int target = L >> 1;
+    for (int g = 0; g < G; ++g) {
+        const int64_t cnt = counts[g];
+        for (int64_t k = gwarp; k < cnt; k += nwarps) {
+            const int64_t row = idx[(int64_t)g * cap + k];
+            double re[S], im[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int l = lane + 32 * s;
+                re[s] = 0.0;
+                im[s] = 0.0;
+                if (l < L) {
+                    const int64_t r = residue_exact(elems + row * d,
+                                                    zmat + ((int64_t)g * L + l) * d, d, M);
+                    const double2 v = ghat[((int64_t)g * L + l) * M + r];
+                    re[s] = v.x;
+                    im[s] = v.y;
+                }
+            }
+            // stable rank of each owned value: #{j: v_j < v_i} + #{j < i: v_j == v_i}
+            int rk_re[S], rk_im[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) rk_re[s] = rk_im[s] = 0;
+#pragma unroll
+            for (int so = 0; so < S; ++so) {
+                for (int src = 0; src < 32; ++src) {
+                    const int j = src + 32 * so;
+                    const double ore = __shfl_sync(0xffffffffu, re[so], src);
+                    const double oim = __shfl_sync(0xffffffffu, im[so], src);
+                    if (j >= L) continue;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const int i = lane + 32 * s;
+                        rk_re[s] += (ore < re[s]) || (ore == re[s] && j < i);
+                        rk_im[s] += (oim < im[s]) || (oim == im[s] && j < i);
+                    }
+                }
+            }
+            double2* out = coeffs + (int64_t)g * cap + k;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int i = lane + 32 * s;
+                if (i < L && rk_re[s] == target) out->x = re[s];
+                if (i < L && rk_im[s] == target) out->y = im[s];
+            }
+        }
+    }
+}
+
+__global__ void lattice_values_kernel(const int64_t* __restrict__ elems, int d,
+                                      const int64_t* __restrict__ zmat, int L, int64_t M,
+                                      const double2* __restrict__ ghat,
+                                      const int64_t* __restrict__ rows, int64_t nrows,
+                                      double2* __restrict__ out) {
+    const int64_t total = nrows * L;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / L;
+        const int l = (int)(e % L);
+        const int64_t row = rows ? rows[k] : k;
+        const int64_t r = residue_exact(elems + row * d, zmat + (int64_t)l * d, d, M);
+        out[e] = ghat[(int64_t)l * M + r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+
+__global__ void sumsq_kernel(const double2* __restrict__ x, int64_t stride, int64_t M,
+                             double* __restrict__ out) {
+    const int64_t b = blockIdx.x;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < M; j += blockDim.x) {
+        const double2 v = x[b * stride + j];
+        s = fma(v.x, v.x, fma(v.y, v.y, s));
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b] = red[0];
+}
+
+__global__ void zero_threshold_kernel(const double* __restrict__ sumsq, int G, int L, int64_t M,
+                                      double* __restrict__ theta) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    double v[256];
+    int n = 0;
+    for (int l = 0; l < L && l < 256; ++l) {
+        const double r = sqrt(sumsq[(int64_t)g * L + l] / (double)M);
+        int j = n++;
+        while (j > 0 && v[j - 1] > r) {
+            v[j] = v[j - 1];
+            --j;
+        }
+        v[j] = r;
+    }
+    const double mid = (n % 2 == 1) ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+    theta[g] = fmax(1e-12, 1e-10 * mid);
+}
+
+__global__ void mark_kernel(const int64_t* __restrict__ idx, const int64_t* __restrict__ counts,
+                            int G, int64_t cap, uint32_t* __restrict__ mask) {
+    for (int g = 0; g < G; ++g) {
+        const int64_t c = counts[g];
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < c;
+             k += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t i = idx[(int64_t)g * cap + k];
+            atomicOr(mask + (i >> 5), 1u << (i & 31));
+        }
+    }
+}
+
+__global__ void gather_rows_kernel(const int64_t* __restrict__ src, int d,
+                                   const int64_t* __restrict__ rows,
+                                   const int64_t* __restrict__ count, int64_t* __restrict__ dst) {
+    const int64_t total = count[0] * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / d;
+        dst[e] = src[rows[k] * d + (e % d)];
+    }
+}
+
+__global__ void pair_kernel(const int64_t* __restrict__ prev, int64_t n1, int t,
+                            const int64_t* __restrict__ vals, int64_t n2,
+                            int64_t* __restrict__ out) {
+    const int64_t total = n1 * n2 * (t + 1);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / (t + 1);
+        const int c = (int)(e % (t + 1));
+        const int64_t i = row / n2, j = row % n2;
+        out[e] = c < t ? prev[i * t + c] : vals[j];
+    }
+}
+
+__global__ void row_bounds_kernel(const int64_t* __restrict__ elems, int64_t n, int d,
+                                  int64_t* __restrict__ out) {
+    // blockDim is a multiple of d: each thread always sees the same coordinate
+    const int per = blockDim.x / d;
+    if (threadIdx.x >= per * d) return;
+    const int coord = threadIdx.x % d;
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    const int64_t total = n * d;
+    for (int64_t e = blockIdx.x * (int64_t)(per * d) + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * per * d) {
+        const int64_t v = elems[e];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    atomicMin((long long*)&out[2 * coord], (long long)lo);
+    atomicMax((long long*)&out[2 * coord + 1], (long long)hi);
+}
+
+__global__ void init_bounds_kernel(int64_t* out, int d) {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        out[2 * j] = INT64_MAX;
+        out[2 * j + 1] = INT64_MIN;
+    }
+}
+
+static int grid_for(int64_t work, int threads) {
+    int64_t g = ceil_div(work, threads);
+    const int64_t cap = (int64_t)num_sms() * 16;
+    return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// ---------------------------------------------------------------------------
+// hash dispatch
+// ---------------------------------------------------------------------------
+
+template <int D, int R, bool WIDE>
+static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
+    auto kern = hash_rows<D, R, WIDE>;
+    SFFTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    int per_sm = 0;
+    SFFTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHashThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    constexpr int TILE = (kHashThreads / 32) * 32 * R;
+    const int64_t ntiles = ceil_div(a.n, TILE);
+    const int64_t want = ceil_div((int64_t)num_sms() * per_sm, a.G);
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, want));
+    kern<<<dim3(gx, a.G), kHashThreads, smem, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <int D, bool WIDE>
+static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
+    // rows per thread: keep R*D <= ~96 int32 registers
+    constexpr int R = D <= 6 ? 16 : (D <= 12 ? 8 : 4);
+    return launch_hash_t<D, (WIDE ? (R / 2 > 0 ? R / 2 : 1) : R), WIDE>(a, smem, st);
+}
+
+template <bool WIDE>
+static int hash_dispatch(int d, HashArgs& a, size_t smem, cudaStream_t st) {
+    switch (d) {
+#define SFFTB_HD(X) \
+    case X: return launch_hash_d<X, WIDE>(a, smem, st);
+        SFFTB_HD(1) SFFTB_HD(2) SFFTB_HD(3) SFFTB_HD(4) SFFTB_HD(5) SFFTB_HD(6) SFFTB_HD(7)
+        SFFTB_HD(8) SFFTB_HD(9) SFFTB_HD(10) SFFTB_HD(11) SFFTB_HD(12) SFFTB_HD(13)
+        SFFTB_HD(14) SFFTB_HD(15) SFFTB_HD(16) SFFTB_HD(17) SFFTB_HD(18) SFFTB_HD(19)
+        SFFTB_HD(20)
+#undef SFFTB_HD
+    }
+    return -1;
+}
+
+}  // namespace sfftb
+
+using namespace sfftb;
+
+extern "C" int64_t sfftb_bitmap_words(int64_t M) {
+    return ((M + 31) / 32 + 3) & ~int64_t(3);
+}
+
+extern "C" int sfftb_nonzero_bitmap(const double* ghat, int64_t G, int64_t L, int64_t M,
+                                    const double* theta, uint32_t* bits, void* stream) {
+    SFFTB_REQUIRE(G >= 0 && L >= 0 && M >= 1, "bitmap: bad sizes");
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    const int64_t rows = G * L;
+    if (rows == 0) return SFFTB_OK;
+    nonzero_bitmap_kernel<<<grid_for(rows * W, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const double2*)ghat, rows, (int)L, M, W, theta, bits);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat,
+                               int64_t G, int64_t L, int64_t M, const uint32_t* bits,
+                               int64_t kbound, int64_t min_hits, int64_t* hits64,
+                               uint32_t* detmask, void* stream) {
+    SFFTB_REQUIRE(n >= 0 && d >= 0 && G >= 1 && L >= 0 && M >= 1, "hash: bad sizes");
+    SFFTB_REQUIRE(G <= 65535, "hash: too many groups");
+    SFFTB_REQUIRE(M < (int64_t(1) << 31), "hash: M must be < 2^31");
+    if (n == 0) return SFFTB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    HashArgs a;
+    a.elems = elems;
+    a.n = n;
+    a.d = (int)d;
+    a.zmat = zmat;
+    a.G = (int)G;
+    a.L = (int)L;
+    a.M = M;
+    a.bits = bits;
+    a.W = W;
+    a.min_hits = min_hits;
+    a.hits64 = hits64;
+    a.detmask = detmask;
+    a.nwords = (n + 31) / 32;
+    a.magic = (uint32_t)(0xFFFFFFFFull / (uint64_t)M);
+    const int64_t lat_bytes = W * 4;
+    const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4;
+    int64_t budget = (int64_t)kBitmapSmemBudget - zbytes;
+    SFFTB_REQUIRE(budget >= lat_bytes, "hash: one lattice bitmap exceeds shared memory");
+    a.Lc = (int)std::max<int64_t>(1, std::min<int64_t>(L, budget / lat_bytes));
+    if (L == 0) a.Lc = 1;
+    const size_t smem = (size_t)(zbytes + (int64_t)a.Lc * lat_bytes);
+
+    // 32-bit path: u = offset + sum_j k_j zc_j stays in [0, 2^32)
+    const int64_t zmax = M / 2;
+    bool fast = false;
+    if (kbound >= 0 && d >= 1 && d <= 20) {
+        const __int128 B = (__int128)kbound * zmax;
+        const __int128 off = ((B + M - 1) / M) * M;
+        if (off + B < ((__int128)1 << 32) && kbound < (int64_t(1) << 31)) {
+            fast = true;
+            a.offset = (uint32_t)off;
+        }
+    }
+    if (fast) return hash_dispatch<false>((int)d, a, smem, st);
+    // 64-bit path: exact while d*(M-1)^2 < 2^62 (the reference's own bound,
+    // detect.py:128-129); beyond that the 128-bit generic kernel
+    const bool wide_ok = (__int128)d * (M - 1) * (M - 1) < ((__int128)1 << 62);
+    if (d >= 1 && d <= 20 && wide_ok) {
+        a.offset = 0;
+        return hash_dispatch<true>((int)d, a, smem, st);
+    }
+    const size_t smem_g = (size_t)((int64_t)a.Lc * lat_bytes);
+    SFFTB_CUDA(cudaFuncSetAttribute(hash_rows_generic,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+    const int64_t ntiles = ceil_div(n, kHashThreads);
+    const int gx = (int)std::max<int64_t>(
+        1, std::min<int64_t>(ntiles, ceil_div((int64_t)num_sms(), G)));
+    hash_rows_generic<<<dim3(gx, (unsigned)G), kHashThreads, smem_g, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int64_t sfftb_compact_workspace_bytes(int64_t G, int64_t n) {
+    const int64_t nwords = (n + 31) / 32;
+    const int64_t nblk = std::max<int64_t>(1, ceil_div(nwords, kCompactWordsPerBlock));
+    return G * nblk * (int64_t)sizeof(int64_t);
+}
+
+extern "C" int sfftb_compact_mask(const uint32_t* mask, int64_t G, int64_t n, int64_t* idx,
+                                  int64_t* counts, void* ws, void* stream) {
+    SFFTB_REQUIRE(G >= 1 && n >= 0 && G <= 65535, "compact: bad sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nwords = (n + 31) / 32;
+    const int64_t nblk = std::max<int64_t>(1, ceil_div(nwords, kCompactWordsPerBlock));
+    int64_t* bs = (int64_t*)ws;
+    compact_count<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(mask, nwords,
+                                                                                 nblk, bs);
+    SFFTB_CHECK_LAUNCH();
+    compact_scan<<<(unsigned)G, 32, 0, st>>>(bs, nblk, counts);
+    SFFTB_CHECK_LAUNCH();
+    compact_write<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(
+        mask, nwords, n, nblk, bs, idx);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_medians(const int64_t* elems, int64_t d, const int64_t* zmat, int64_t G,
+                             int64_t L, int64_t M, const double* ghat, const int64_t* idx,
+                             const int64_t* counts, int64_t cap, double* coeffs, void* stream) {
+    SFFTB_REQUIRE(L >= 1 && L <= 128 && (L % 2) == 1, "medians require odd L <= 128");
+    SFFTB_REQUIRE(G >= 1 && M >= 1, "medians: bad sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = num_sms() * 8;
+    if (L <= 32)
+        medians_kernel<1><<<blocks, 256, 0, st>>>(elems, (int)d, zmat, (int)G, (int)L, M,
+                                                  (const double2*)ghat, idx, counts, cap,
+                                                  (double2*)coeffs);
+    else if (L <= 64)
+        medians_kernel<2><<<blocks, 256, 0, st>>>(elems, (int)d, zmat, (int)G, (int)L, M,
+                                                  (const double2*)ghat, idx, counts, cap,
+                                                  (double2*)coeffs);
+    else
+        medians_kernel<4><<<blocks, 256, 0, st>>>(elems, (int)d, zmat, (int)G, (int)L, M,
+                                                  (const double2*)ghat, idx, counts, cap,
+                                                  (double2*)coeffs);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_lattice_values(const int64_t* elems, int64_t d, const int64_t* zmat,
+                                    int64_t L, int64_t M, const double* ghat,
+                                    const int64_t* rows, int64_t nrows, double* out,
+                                    void* stream) {
+    if (nrows == 0 || L == 0) return SFFTB_OK;
+    lattice_values_kernel<<<grid_for(nrows * L, 256), 256, 0, (cudaStream_t)stream>>>(
+        elems, (int)d, zmat, (int)L, M, (const double2*)ghat, rows, nrows, (double2*)out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_sumsq(const double* x, int64_t stride, int64_t batch, int64_t M,
+                           double* out, void* stream) {
+    if (batch == 0) return SFFTB_OK;
+    sumsq_kernel<<<(unsigned)batch, 256, 0, (cudaStream_t)stream>>>((const double2*)x, stride, M,
+                                                                    out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_zero_thresholds(const double* sumsq, int64_t G, int64_t L, int64_t M,
+                                     double* theta, void* stream) {
+    SFFTB_REQUIRE(L >= 1 && L <= 256, "zero test: 1 <= L <= 256");
+    zero_threshold_kernel<<<(unsigned)ceil_div(G, 64), 64, 0, (cudaStream_t)stream>>>(
+        sumsq, (int)G, (int)L, M, theta);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_mark_indices(const int64_t* idx, const int64_t* counts, int64_t G,
+                                  int64_t cap, uint32_t* mask, int64_t n, void* stream) {
+    (void)n;
+    mark_kernel<<<num_sms() * 4, 256, 0, (cudaStream_t)stream>>>(idx, counts, (int)G, cap, mask);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_gather_rows(const int64_t* src, int64_t d, const int64_t* rows,
+                                 const int64_t* count, int64_t cap, int64_t* dst, void* stream) {
+    if (cap == 0 || d == 0) return SFFTB_OK;
+    gather_rows_kernel<<<grid_for(cap * d, 256), 256, 0, (cudaStream_t)stream>>>(
+        src, (int)d, rows, count, dst);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_pair_product(const int64_t* prev, int64_t n1, int64_t t,
+                                  const int64_t* vals, int64_t n2, int64_t* out, void* stream) {
+    const int64_t total = n1 * n2 * (t + 1);
+    if (total == 0) return SFFTB_OK;
+    pair_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(prev, n1, (int)t, vals,
+                                                                        n2, out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_row_bounds(const int64_t* elems, int64_t n, int64_t d, int64_t* out,
+                                void* stream) {
+    SFFTB_REQUIRE(d >= 1 && d <= 256, "row bounds: 1 <= d <= 256");
+    cudaStream_t st = (cudaStream_t)stream;
+    init_bounds_kernel<<<1, 256, 0, st>>>(out, (int)d);
+    SFFTB_CHECK_LAUNCH();
+    if (n == 0) return SFFTB_OK;
+    const int threads = (int)(256 / d) * (int)d;
+    row_bounds_kernel<<<grid_for(n * d, threads), threads, 0, st>>>(elems, n, (int)d, out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}

@@ -1,0 +1,261 @@
+// Lattice sampling of sparse trigonometric polynomials, dense point
+// evaluation, and the harness noise stream.
+//
+// The reference samples a lattice either densely (evaluate_many,
+// polyeval.py:66-75 -- what sfft uses through SamplingOracle.sample_many,
+// dimincr.py:186-191) or structurally for whole lattices (evaluate_on_lattice,
+// polyeval.py:78-87: bincount of coefficients by residue, then M * ifft).
+// Here every lattice sampling -- including the fixed-tail lattices of the
+// dimension-incremental driver -- is structured: the non-lattice coordinates
+// of a node are constant, so they fold into an anchor phase per frequency,
+//   p([j z/M | tail]) = sum_h B[h] e^{2 pi i j h/M},
+//   B[h] = sum_{k: k_{<t}.z = h mod M} c_k e^{2 pi i k_{>=t}.tail},
+// an exact restatement of the dense sum.
+#include "common.cuh"
+
+namespace sfftb {
+
+static constexpr int kScatterThreads = 1024;
+static constexpr int kScatterChunk = 8192;  // keys per shared-memory sort
+
+__global__ void anchor_kernel(const int64_t* __restrict__ support, int64_t s, int d, int t_dim,
+                              const double2* __restrict__ coeffs,
+                              const double* __restrict__ tails, int G,
+                              double2* __restrict__ out) {
+    const int64_t total = s * G;
+    const int m = d - t_dim;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = e / s, k = e % s;
+        const double2 c = coeffs[k];
+        if (m == 0) {
+            out[e] = c;
+            continue;
+        }
+        double phi = 0.0;
+        for (int j = 0; j < m; ++j)
+            phi = fma((double)support[k * d + t_dim + j], tails[g * m + j], phi);
+        double sn, cs;
+        sincospi(2.0 * phi, &sn, &cs);
+        out[e] = cmul(c, make_double2(cs, sn));
+    }
+}
+
+__device__ __forceinline__ uint64_t mulmod_u64(uint64_t a, uint64_t b, uint64_t M) {
+    return (uint64_t)(((unsigned __int128)a * b) % M);
+}
+
+// One CTA per lattice; bins summed in ascending coefficient order.
+__global__ void __launch_bounds__(kScatterThreads)
+    scatter_kernel(const int64_t* __restrict__ support, int64_t s, int d, int t_dim,
+                   const double2* __restrict__ anchored, const int64_t* __restrict__ zmat,
+                   int L, int64_t M, double2* __restrict__ bins) {
+    extern __shared__ uint64_t keys[];  // kScatterChunk
+    __shared__ uint64_t zs[64];
+    const int64_t lat = blockIdx.x;
+    const int64_t g = lat / L;
+    for (int j = threadIdx.x; j < t_dim; j += blockDim.x) {
+        int64_t z = zmat[lat * t_dim + j] % M;
+        zs[j] = (uint64_t)(z < 0 ? z + M : z);
+    }
+    double2* B = bins + lat * M;
+    for (int64_t h = threadIdx.x; h < M; h += blockDim.x) B[h] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const double2* a = anchored + g * s;
+    for (int64_t c0 = 0; c0 < s; c0 += kScatterChunk) {
+        const int cnt = (int)(s - c0 < kScatterChunk ? s - c0 : kScatterChunk);
+        int P = 1;
+        while (P < cnt) P <<= 1;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+            uint64_t key = ~0ull;
+            if (i < cnt) {
+                const int64_t* row = support + (c0 + i) * d;
+                uint64_t r = 0;
+                for (int j = 0; j < t_dim; ++j) {
+                    int64_t e = row[j] % M;
+                    if (e < 0) e += M;
+                    r = (r + mulmod_u64((uint64_t)e, zs[j], (uint64_t)M)) % (uint64_t)M;
+                }
+                key = (r << 32) | (uint64_t)i;
+            }
+            keys[i] = key;
+        }
+        __syncthreads();
+        // bitonic sort of P keys (ascending)
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                    const int ixj = i ^ jj;
+                    if (ixj > i) {
+                        const uint64_t x = keys[i], y = keys[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((x > y) == up) {
+                            keys[i] = y;
+                            keys[ixj] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // run heads accumulate their run in ascending coefficient order
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const uint64_t r = keys[i] >> 32;
+            if (i > 0 && (keys[i - 1] >> 32) == r) continue;
+            double2 acc = B[r];
+            for (int q = i; q < cnt && (keys[q] >> 32) == r; ++q) {
+                const double2 v = a[c0 + (int64_t)(keys[q] & 0xffffffffu)];
+                acc.x += v.x;
+                acc.y += v.y;
+            }
+            B[r] = acc;
+        }
+        __syncthreads();
+    }
+}
+
+// Thread per point; frequencies staged through shared memory in chunks.
+static constexpr int kEvalThreads = 128;
+static constexpr int kEvalChunk = 64;
+
+__global__ void __launch_bounds__(kEvalThreads)
+    eval_dense_kernel(const int64_t* __restrict__ support, int64_t s, int d,
+                      const double2* __restrict__ coeffs, const double* __restrict__ X, int64_t m,
+                      double2* __restrict__ out) {
+    extern __shared__ double sh[];
+    double* ks = sh;                       // kEvalChunk * d
+    double2* cs = (double2*)(sh + kEvalChunk * d);  // kEvalChunk
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double x[32];
+    const bool active = p < m;
+    for (int j = 0; j < d; ++j) x[j] = active ? X[p * d + j] : 0.0;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t k0 = 0; k0 < s; k0 += kEvalChunk) {
+        const int cnt = (int)(s - k0 < kEvalChunk ? s - k0 : kEvalChunk);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt * d; e += blockDim.x)
+            ks[e] = (double)support[k0 * d + e];
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) cs[e] = coeffs[k0 + e];
+        __syncthreads();
+        if (!active) continue;
+        for (int k = 0; k < cnt; ++k) {
+            double phi = 0.0;
+            for (int j = 0; j < d; ++j) phi = fma(ks[k * d + j], x[j], phi);
+            double sn, c;
+            sincospi(2.0 * phi, &sn, &c);
+            const double2 t = cmul(cs[k], make_double2(c, sn));
+            acc.x += t.x;
+            acc.y += t.y;
+        }
+    }
+    if (active) out[p] = acc;
+}
+
+// Philox4x32-10
+__device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        if (r < 9) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+    }
+}
+
+__global__ void noise_kernel(double2* __restrict__ x, int64_t rows, int64_t M, uint64_t seed,
+                             int64_t call0, double sigma) {
+    const int64_t total = rows * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / M, m = e % M;
+        const uint64_t call = (uint64_t)(call0 + row);
+        uint32_t c[4] = {(uint32_t)m, (uint32_t)((uint64_t)m >> 32), (uint32_t)call,
+                         (uint32_t)(call >> 32)};
+        philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const uint64_t ua = ((uint64_t)(c[0] >> 5) << 26) + (c[1] >> 6);
+        const uint64_t ub = ((uint64_t)(c[2] >> 5) << 26) + (c[3] >> 6);
+        const double u1 = ((double)ua + 1.0) * 0x1.0p-53;
+        const double u2 = (double)ub * 0x1.0p-53;
+        const double rad = sigma * sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        double2 v = x[e];
+        v.x += rad * cs;
+        v.y += rad * sn;
+        x[e] = v;
+    }
+}
+
+static int grid_1d(int64_t work, int threads) {
+    int64_t g = ceil_div(work, threads);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 16));
+}
+
+}  // namespace sfftb
+
+using namespace sfftb;
+
+extern "C" int sfftb_anchor_coeffs(const int64_t* support, int64_t s, int64_t d, int64_t t_dim,
+                                   const double* coeffs, const double* tails, int64_t G,
+                                   double* out, void* stream) {
+    SFFTB_REQUIRE(t_dim >= 0 && t_dim <= d, "anchor: bad t_dim");
+    if (s == 0 || G == 0) return SFFTB_OK;
+    anchor_kernel<<<grid_1d(s * G, 256), 256, 0, (cudaStream_t)stream>>>(
+        support, s, (int)d, (int)t_dim, (const double2*)coeffs, tails, (int)G, (double2*)out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int64_t sfftb_scatter_workspace_bytes(int64_t lattices, int64_t s) {
+    (void)lattices;
+    (void)s;
+    return 0;
+}
+
+extern "C" int sfftb_scatter_bins(const int64_t* support, int64_t s, int64_t d, int64_t t_dim,
+                                  const double* anchored, const int64_t* zmat, int64_t G,
+                                  int64_t L, int64_t M, double* bins, void* ws, void* stream) {
+    (void)ws;
+    SFFTB_REQUIRE(t_dim >= 0 && t_dim <= 64 && t_dim <= d, "scatter: bad t_dim");
+    SFFTB_REQUIRE(M >= 1 && M < (int64_t(1) << 31), "scatter: bad M");
+    const int64_t lat = G * L;
+    if (lat == 0) return SFFTB_OK;
+    SFFTB_REQUIRE(lat <= 0x7fffffff, "scatter: too many lattices");
+    const size_t sm = sizeof(uint64_t) * kScatterChunk;
+    SFFTB_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm));
+    scatter_kernel<<<(unsigned)lat, kScatterThreads, sm, (cudaStream_t)stream>>>(
+        support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M,
+        (double2*)bins);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_eval_dense(const int64_t* support, int64_t s, int64_t d,
+                                const double* coeffs, const double* X, int64_t m, double* out,
+                                void* stream) {
+    SFFTB_REQUIRE(d >= 1 && d <= 32, "eval_dense: 1 <= d <= 32");
+    if (m == 0) return SFFTB_OK;
+    const size_t sm = sizeof(double) * kEvalChunk * d + sizeof(double2) * kEvalChunk;
+    eval_dense_kernel<<<(unsigned)ceil_div(m, kEvalThreads), kEvalThreads, sm,
+                        (cudaStream_t)stream>>>(support, s, (int)d, (const double2*)coeffs, X, m,
+                                                (double2*)out);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_add_noise(double* x, int64_t rows, int64_t M, uint64_t seed, int64_t call0,
+                               double sigma, void* stream) {
+    if (rows == 0 || M == 0 || sigma == 0.0) return SFFTB_OK;
+    noise_kernel<<<grid_1d(rows * M, 256), 256, 0, (cudaStream_t)stream>>>(
+        (double2*)x, rows, M, seed, call0, sigma);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}

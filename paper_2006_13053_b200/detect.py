@@ -1,0 +1,337 @@
+"""Frequency detection from samples along a multi-lattice configuration.
+
+Public entry points of latfft/detect.py (detect_frequencies :149-155,
+detect_and_compute :158-169, detect_topk :172-195, postprocess_r1l :198-228,
+per_lattice_coefficients :112-119, default_zero_test :42-53, DetectionResult
+:56-95, format_detection :231-240) with their argument and return
+conventions.  The work runs on the device (_engine.detect_batch); results are
+held as device tensors and materialised as numpy arrays on first access.
+
+``samples`` may be the reference's list of L host vectors, or (B200 path) a
+(L, M) complex128 CUDA tensor already in HBM.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _dev, _engine, _native
+from .dft import dft_batch
+from .errors import ParameterError
+from .freqset import FreqSet
+
+
+class ZeroTest:
+    """Absolute magnitude threshold for the approximate zero test."""
+
+    __slots__ = ("theta_zero",)
+
+    def __init__(self, theta_zero):
+        if theta_zero < 0:
+            raise ParameterError("theta_zero must be >= 0")
+        self.theta_zero = float(theta_zero)
+
+    def __repr__(self):
+        return f"ZeroTest({self.theta_zero!r})"
+
+
+def _lazy_np(v):
+    if isinstance(v, torch.Tensor):
+        return _dev.download(v)
+    return v
+
+
+class DetectionResult:
+    """Detected frequencies, coefficients and per-candidate hit counts.
+
+    ``hits`` aligns with ``candidates``; ``detected_idx`` indexes the
+    candidate set; ``coeffs`` (if present) aligns with ``detected``.
+    """
+
+    __slots__ = ("candidates", "_hits", "_idx", "_coeffs", "theta_zero", "_detected")
+
+    def __init__(self, candidates, hits, detected_idx, coeffs, theta_zero):
+        self.candidates = candidates
+        self._hits = hits
+        self._idx = detected_idx
+        self._coeffs = coeffs
+        self.theta_zero = float(theta_zero)
+        self._detected = None
+
+    @property
+    def hits(self):
+        self._hits = _lazy_np(self._hits)
+        return self._hits
+
+    @property
+    def detected_idx(self):
+        self._idx = _lazy_np(self._idx)
+        return self._idx
+
+    @property
+    def coeffs(self):
+        self._coeffs = _lazy_np(self._coeffs)
+        return self._coeffs
+
+    def device_arrays(self):
+        """(detected_idx, coeffs) as CUDA tensors when still resident."""
+        return self._idx, self._coeffs
+
+    @property
+    def detected(self):
+        if self._detected is None:
+            idx = self._idx
+            if isinstance(idx, torch.Tensor):
+                self._detected = self.candidates.take(idx)
+            else:
+                self._detected = self.candidates.take(np.asarray(idx, dtype=np.int64))
+        return self._detected
+
+    def __repr__(self):
+        return (f"DetectionResult(candidates={len(self.candidates)}, "
+                f"detected={len(self.detected)})")
+
+    @property
+    def per_lattice_hits(self):
+        return {k: int(h) for k, h in zip(self.candidates, self.hits)}
+
+    def hit_count(self, k):
+        row = np.asarray(k, dtype=np.int64)
+        where = np.flatnonzero(np.all(self.candidates.elems == row, axis=1))
+        if where.size == 0:
+            raise KeyError(k)
+        return int(self.hits[where[0]])
+
+    def coeffs_dict(self):
+        if self._coeffs is None:
+            return {}
+        return {k: complex(c) for k, c in zip(self.detected, self.coeffs)}
+
+
+# ---------------------------------------------------------------------------
+
+def _stack_samples(samples, config):
+    """Validated (L, M) complex128 CUDA tensor (detect.py:98-109 checks)."""
+    L = config.L
+    if isinstance(samples, torch.Tensor):
+        if samples.ndim != 2 or samples.shape[0] != L:
+            raise ParameterError(f"expected {L} sample vectors, got {tuple(samples.shape)}")
+        M = config.shared_M
+        if M is None or samples.shape[1] != M:
+            raise ParameterError("sample tensor does not match the lattice sizes")
+        t = _dev.as_c128(samples)
+    else:
+        if len(samples) != L:
+            raise ParameterError(f"expected {L} sample vectors, got {len(samples)}")
+        rows = []
+        for s, lat in zip(samples, config.lattices):
+            s = np.asarray(s, dtype=np.complex128)
+            if s.shape != (lat.M,):
+                raise ParameterError(
+                    f"sample vector of length {s.shape} does not match M={lat.M}")
+            rows.append(s)
+        if config.shared_M is None:
+            return [_dev.upload(r).reshape(1, -1) for r in rows]
+        t = _dev.upload(np.vstack(rows))
+    if not bool(torch.isfinite(torch.view_as_real(t)).all()):
+        raise ParameterError("samples contain NaN or Inf")
+    return t
+
+
+def _zero_from_device(t):
+    """default_zero_test on staged device samples (one value per config)."""
+    if isinstance(t, list):  # distinct lattice sizes: per-lattice RMS on device
+        rms = []
+        for s in t:
+            M = int(s.shape[1])
+            sq = _dev.empty((1,), torch.float64)
+            _native.call("sfftb_sumsq", _dev.ptr(s), M, 1, M, _dev.ptr(sq), _dev.stream())
+            rms.append(sq)
+        vals = sorted(math.sqrt(float(v[0]) / int(s.shape[1])) for v, s in zip(rms, t))
+        h = len(vals) // 2
+        mid = vals[h] if len(vals) % 2 == 1 else 0.5 * (vals[h - 1] + vals[h])
+        return ZeroTest(max(1e-12, 1e-10 * mid))
+    L, M = int(t.shape[0]), int(t.shape[1])
+    return ZeroTest(float(_engine.zero_thresholds(t, 1, L, M)[0]))
+
+
+def default_zero_test(samples):
+    """max(1e-12, 1e-10 * median per-lattice RMS) (detect.py:42-53), on device."""
+    if isinstance(samples, torch.Tensor):
+        return _zero_from_device(_dev.as_c128(samples))
+    rows = [np.asarray(s, dtype=np.complex128).reshape(-1) for s in samples]
+    if len({r.size for r in rows}) == 1:
+        return _zero_from_device(_dev.upload(np.vstack(rows)))
+    return _zero_from_device([_dev.upload(r).reshape(1, -1) for r in rows])
+
+
+def _kbound(gamma):
+    return gamma.memo("kbound", gamma.kbound)
+
+
+def _theta_tensor(theta):
+    return torch.full((1,), float(theta), dtype=torch.float64, device=_dev.device())
+
+
+def _gather(samples, config, gamma, zero, want_medians, want_hits=True):
+    """Device detection for one configuration -> engine Batch (G = 1)."""
+    M = config.shared_M
+    if M is None:
+        return _gather_mixed(samples, config, gamma, zero, want_medians)
+    if not gamma.dim * (M - 1) ** 2 < 2**62:
+        raise ParameterError("lattice size too large for int64 residues")
+    if config.dim != gamma.dim:
+        raise ParameterError("candidate set/lattice dimension mismatch")
+    return _engine.detect_batch(samples, M, config.zmat_device(), 1, config.L,
+                                gamma.device(), _kbound(gamma), config.nu,
+                                theta0=_theta_tensor(zero.theta_zero),
+                                want_medians=want_medians, want_hits=want_hits)
+
+
+def _gather_mixed(samples, config, gamma, zero, want_medians):
+    """Distinct lattice sizes (detect.py:134-145): one lattice at a time."""
+    rows = gamma.device()
+    n = len(gamma)
+    L = config.L
+    theta = _theta_tensor(zero.theta_zero)
+    hits = torch.zeros((n,), dtype=torch.int64, device=_dev.device())
+    vals = torch.empty((n, L), dtype=torch.complex128, device=_dev.device())
+    allrows = torch.arange(n, dtype=torch.int64, device=_dev.device())
+    for col, (s, lat) in enumerate(zip(samples, config.lattices)):
+        z = _dev.upload(lat.z.reshape(1, -1))
+        b = _engine.detect_batch(s, lat.M, z, 1, 1, rows, _kbound(gamma), 1.0, theta0=theta,
+                                 want_medians=False, want_hits=True)
+        hits += b.hits
+        out = torch.empty((n,), dtype=torch.complex128, device=_dev.device())
+        if n:
+            _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z), 1,
+                         lat.M, _dev.ptr(b.ghat), _dev.ptr(allrows), n, _dev.ptr(out),
+                         _dev.stream())
+        vals[:, col] = out
+    thr = config.nu * L
+    det = hits.to(torch.float64) >= thr
+    idx = torch.nonzero(det).flatten()
+    coeffs = None
+    if want_medians:
+        sel = vals[idx]
+        coeffs = torch.complex(torch.median(sel.real, dim=1).values,
+                               torch.median(sel.imag, dim=1).values)
+    return _engine.Batch(1, L, 0, n, None, theta, hits, idx,
+                         torch.tensor([idx.numel()], device=_dev.device()), coeffs)
+
+
+def _result_from_batch(gamma, b, theta0, with_coeffs):
+    cnt = int(b.counts[0]) if b.counts is not None else 0
+    idx = b.idx[:cnt]
+    coeffs = b.coeffs[:cnt] if (with_coeffs and b.coeffs is not None) else None
+    return DetectionResult(gamma, b.hits, idx, coeffs, theta0)
+
+
+def detect_frequencies(samples, config, gamma, zero=None):
+    """Alg. 1: keep k when its nonzero count reaches nu*L (detect.py:149-155)."""
+    t = _stack_samples(samples, config)
+    if zero is None:
+        zero = _zero_from_device(t)
+    b = _gather(t, config, gamma, zero, False)
+    return _result_from_batch(gamma, b, zero.theta_zero, False)
+
+
+def detect_and_compute(samples, config, gamma, zero=None):
+    """Alg. 2: classification + coefficient medians (detect.py:158-169)."""
+    if config.nu != 0.5:
+        raise ParameterError("coefficient computation requires nu = 1/2")
+    if config.L % 2 == 0:
+        raise ParameterError("coefficient computation requires odd L")
+    t = _stack_samples(samples, config)
+    if zero is None:
+        zero = _zero_from_device(t)
+    b = _gather(t, config, gamma, zero, True)
+    return _result_from_batch(gamma, b, zero.theta_zero, True)
+
+
+def detect_topk(samples, config, gamma, s_tilde, theta, zero=None):
+    """Alg. 4: detect_and_compute, |coeff| >= theta, s_tilde largest
+    (ties: ascending lexicographic frequency), candidate order (detect.py:172-195)."""
+    s_tilde = int(s_tilde)
+    if s_tilde < 0:
+        raise ParameterError("s_tilde must be >= 0")
+    if theta < 0:
+        raise ParameterError("theta must be >= 0")
+    res = detect_and_compute(samples, config, gamma, zero=zero)
+    idx, coeffs = res.device_arrays()
+    if not isinstance(idx, torch.Tensor):
+        idx = _dev.as_i64(idx)
+        coeffs = _dev.as_c128(coeffs)
+    n = int(idx.numel())
+    counts = torch.tensor([n], dtype=torch.int64, device=_dev.device())
+    kidx, kco, kcounts = _engine.topk(idx, coeffs, counts, 1, n, theta, s_tilde)
+    k = int(kcounts[0])
+    return DetectionResult(res.candidates, res._hits, kidx[:k], kco[:k], res.theta_zero)
+
+
+def per_lattice_coefficients(samples, config, gamma):
+    """(n, L) per-lattice estimates ghat_l[r_l(k)] (detect.py:112-119)."""
+    t = _stack_samples(samples, config)
+    n, L = len(gamma), config.L
+    out = _dev.empty((L, max(n, 1)), torch.complex128)
+    rows = gamma.device()
+    if isinstance(t, list):
+        for col, (s, lat) in enumerate(zip(t, config.lattices)):
+            g = dft_batch(s, lat.M)
+            z = _dev.upload(lat.z.reshape(1, -1))
+            _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z), 1,
+                         lat.M, _dev.ptr(g), None, n, _dev.ptr(out[col]), _dev.stream())
+        return _dev.download(out[:, :n].T.contiguous())
+    M = config.shared_M
+    g = dft_batch(t, M)
+    z = config.zmat_device()
+    for col in range(L):
+        if n:
+            _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z[col]), 1,
+                         M, _dev.ptr(g[col]), None, n, _dev.ptr(out[col]), _dev.stream())
+    return _dev.download(out[:, :n].T.contiguous())
+
+
+def postprocess_r1l(result, samples, config, zero=None):
+    """Average the estimates of lattices on which a detected frequency's
+    residue is unique within the detected set; keep the median otherwise;
+    drop |value| <= theta_zero (detect.py:198-228)."""
+    if zero is None:
+        zero = ZeroTest(result.theta_zero)
+    n = len(result.detected)
+    if n == 0:
+        return result
+    vals = torch.as_tensor(per_lattice_coefficients(samples, config, result.detected),
+                           device=_dev.device())
+    rows = result.detected.device()
+    refined = _dev.as_c128(result.coeffs).clone()
+    cnt = torch.zeros((n,), dtype=torch.int64, device=_dev.device())
+    acc = torch.zeros((n,), dtype=torch.complex128, device=_dev.device())
+    for col, lat in enumerate(config.lattices):
+        z = torch.as_tensor(lat.z, device=_dev.device())
+        res = ((rows % lat.M) * z).sum(dim=1) % lat.M
+        uniq = torch.bincount(res, minlength=lat.M)[res] == 1
+        cnt += uniq
+        acc[uniq] += vals[uniq, col]
+    has = cnt > 0
+    refined[has] = acc[has] / cnt[has]
+    keep = torch.abs(refined) > zero.theta_zero
+    idx = _dev.as_i64(result.detected_idx)[keep]
+    return DetectionResult(result.candidates, result._hits, idx, refined[keep],
+                           result.theta_zero)
+
+
+def format_detection(result):
+    """Text form: components, Re, Im, hit count (detect.py:231-240)."""
+    lines = []
+    has = result.coeffs is not None
+    for i, idx in enumerate(result.detected_idx):
+        row = result.candidates.elems[idx]
+        c = complex(result.coeffs[i]) if has else 0j
+        comps = " ".join(str(int(v)) for v in row)
+        lines.append(f"{comps} {float(c.real)!r} {float(c.imag)!r} {int(result.hits[idx])}")
+    return "\n".join(lines) + ("\n" if lines else "")
+

@@ -1,0 +1,240 @@
+"""Sparse trigonometric polynomials and sampling oracles.
+
+Public surface of latfft/polyeval.py:22-143 for the hot path: ``SparsePoly``,
+``evaluate``/``evaluate_many`` (dense), ``evaluate_on_lattice`` (structured),
+``SamplingOracle`` with its evaluation counter, ``oracle_from_poly``,
+``sample_on_lattice``, ``random_poly``.  Every evaluation runs on the device
+(csrc/sample.cu + csrc/fft.cu).
+
+``oracle_from_poly`` returns a :class:`PolyOracle`: a SamplingOracle whose
+lattice samplings -- including the fixed-tail lattices of the
+dimension-incremental driver -- take the structured path (anchor-phase
+scatter into residue bins + inverse Bluestein DFT), batched over all lattices
+of a detection stage.  Black-box oracles (any ``fn``) are evaluated on the
+host by their own ``fn`` and uploaded.
+
+Noise (config 5): ``oracle_from_poly(p, noise_sigma=s, noise_seed=k)`` adds
+s*(N(0,1) + i N(0,1)) to every sample, drawn per oracle call from the
+Philox4x32-10 stream keyed by k with counter (sample index, call index) --
+the harness noise model (the reference has none), restated in
+oracle/port.py:noise_for_call.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _dev, _native
+from .dft import dft_batch
+from .errors import ParameterError
+from .freqset import FreqSet
+
+
+class SparsePoly:
+    """Support (FreqSet) plus aligned nonzero complex coefficients."""
+
+    __slots__ = ("support", "coeffs", "_dev")
+
+    def __init__(self, support, coeffs):
+        if not isinstance(support, FreqSet):
+            raise ParameterError("support must be a FreqSet")
+        coeffs = np.asarray(coeffs, dtype=np.complex128)
+        if coeffs.shape != (len(support),):
+            raise ParameterError("need exactly one coefficient per support frequency")
+        if len(support) and np.any(coeffs == 0):
+            raise ParameterError("coefficients must be nonzero")
+        coeffs.setflags(write=False)
+        self.support, self.coeffs = support, coeffs
+        self._dev = None
+
+    @classmethod
+    def from_dict(cls, dim, mapping):
+        support = FreqSet(dim, list(mapping.keys()))
+        return cls(support, np.array([mapping[k] for k in support], dtype=np.complex128))
+
+    def as_dict(self):
+        return {k: complex(c) for k, c in zip(self.support, self.coeffs)}
+
+    @property
+    def dim(self):
+        return self.support.dim
+
+    def __len__(self):
+        return len(self.support)
+
+    def device(self):
+        """(support int64 (s, d), coeffs complex128 (s,)) on the device."""
+        if self._dev is None:
+            self._dev = (self.support.device(), _dev.upload(self.coeffs))
+        return self._dev
+
+
+def _eval_points_dev(p, X_dev):
+    sup, c = p.device()
+    m = X_dev.shape[0]
+    out = _dev.empty((m,), torch.complex128)
+    if len(p) == 0:
+        out.zero_()
+        return out
+    _native.call("sfftb_eval_dense", _dev.ptr(sup), len(p), p.dim, _dev.ptr(c),
+                 _dev.ptr(X_dev), m, _dev.ptr(out), _dev.stream())
+    return out
+
+
+def evaluate(p, x):
+    """p(x) at one point by direct summation (polyeval.py:57-63)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (p.dim,):
+        raise ParameterError("point/polynomial dimension mismatch")
+    return complex(_dev.download(_eval_points_dev(p, _dev.upload(x.reshape(1, -1))))[0])
+
+
+def evaluate_many(p, X):
+    """p at the rows of an (m, d) point array (polyeval.py:66-75)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[1] != p.dim:
+        raise ParameterError("points must be an (m, d) array")
+    return _dev.download(_eval_points_dev(p, _dev.upload(X)))
+
+
+def sample_lattices_device(p, zmat_dev, M, tails_dev, G, L, t_dim):
+    """Structured samples of G*L lattices (G tails, L generators each).
+
+    zmat_dev: (G*L, t_dim) int64; tails_dev: (G, d - t_dim) float64.
+    Returns (G*L, M) complex128 = values at [j z/M mod 1 | tail_g], j < M.
+    """
+    sup, c = p.device()
+    s = len(p)
+    anchored = _dev.empty((G, max(s, 1)), torch.complex128)
+    if s:
+        _native.call("sfftb_anchor_coeffs", _dev.ptr(sup), s, p.dim, t_dim, _dev.ptr(c),
+                     _dev.ptr(tails_dev), G, _dev.ptr(anchored), _dev.stream())
+    bins = _dev.empty((G * L, M), torch.complex128)
+    _native.call("sfftb_scatter_bins", _dev.ptr(sup), s, p.dim, t_dim, _dev.ptr(anchored),
+                 _dev.ptr(zmat_dev), G, L, M, _dev.ptr(bins), None, _dev.stream())
+    return dft_batch(bins, M, inverse=True, scale=1.0)
+
+
+def evaluate_on_lattice(p, lat):
+    """p at all M nodes of one lattice (polyeval.py:78-87), structured."""
+    if lat.dim != p.dim:
+        raise ParameterError("lattice/polynomial dimension mismatch")
+    z = _dev.upload(lat.z.reshape(1, -1))
+    tails = _dev.empty((1, 1), torch.float64)
+    return _dev.download(sample_lattices_device(p, z, lat.M, tails, 1, 1, p.dim)[0])
+
+
+class SamplingOracle:
+    """Black-box evaluator with a cumulative sample counter (polyeval.py:90-130)."""
+
+    __slots__ = ("fn", "dim", "lattice_fn", "count")
+
+    def __init__(self, fn, dim, lattice_fn=None):
+        self.fn = fn
+        self.dim = int(dim)
+        self.lattice_fn = lattice_fn
+        self.count = 0
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.dim,):
+            raise ParameterError("point/oracle dimension mismatch")
+        self.count += 1
+        return complex(self.fn(x[None, :])[0])
+
+    def sample_many(self, X):
+        X = np.asarray(X, dtype=np.float64)
+        if X.ndim != 2 or X.shape[1] != self.dim:
+            raise ParameterError("points must be an (m, d) array")
+        self.count += X.shape[0]
+        return np.asarray(self.fn(X), dtype=np.complex128)
+
+    def sample_lattice(self, lat):
+        if lat.dim != self.dim:
+            raise ParameterError("lattice/oracle dimension mismatch")
+        if self.lattice_fn is not None:
+            self.count += lat.M
+            return np.asarray(self.lattice_fn(lat), dtype=np.complex128)
+        from .lattice import lattice_nodes
+
+        return self.sample_many(lattice_nodes(lat))
+
+
+class PolyOracle(SamplingOracle):
+    """SamplingOracle over a SparsePoly with device sampling paths.
+
+    ``calls`` counts oracle calls (one per sample_many / lattice); it indexes
+    the optional noise stream.
+    """
+
+    __slots__ = ("poly", "noise_sigma", "noise_seed", "calls", "fast_lattice")
+
+    def __init__(self, p, fast_lattice=True, noise_sigma=0.0, noise_seed=0):
+        super().__init__(self._dense, p.dim,
+                         lattice_fn=self._lattice if fast_lattice else None)
+        self.poly = p
+        self.fast_lattice = bool(fast_lattice)
+        self.noise_sigma = float(noise_sigma)
+        self.noise_seed = int(noise_seed)
+        self.calls = 0
+
+    def add_noise_device(self, vals, rows, M):
+        """Noise for `rows` consecutive calls of M samples each (in place)."""
+        if self.noise_sigma > 0:
+            _native.call("sfftb_add_noise", _dev.ptr(vals), rows, M,
+                         self.noise_seed & 0xFFFFFFFFFFFFFFFF, self.calls,
+                         self.noise_sigma, _dev.stream())
+        self.calls += rows
+
+    def eval_points_device(self, X_dev):
+        out = _eval_points_dev(self.poly, X_dev)
+        self.add_noise_device(out, 1, out.shape[0])
+        return out
+
+    def _dense(self, X):
+        return _dev.download(self.eval_points_device(_dev.upload(np.asarray(X, np.float64))))
+
+    def _lattice(self, lat):
+        z = _dev.upload(lat.z.reshape(1, -1))
+        tails = _dev.empty((1, 1), torch.float64)
+        vals = sample_lattices_device(self.poly, z, lat.M, tails, 1, 1, self.dim)
+        self.add_noise_device(vals, 1, lat.M)
+        return _dev.download(vals[0])
+
+    def sample_lattices_device(self, zmat_dev, M, tails_dev, G, L, t_dim):
+        """Batched fixed-tail lattice sampling; advances count and calls
+        exactly as G*L separate sample_many calls would (dimincr.py:186-191)."""
+        vals = sample_lattices_device(self.poly, zmat_dev, M, tails_dev, G, L, t_dim)
+        self.add_noise_device(vals, G * L, M)
+        self.count += G * L * M
+        return vals
+
+
+def oracle_from_poly(p, fast_lattice=True, *, noise_sigma=0.0, noise_seed=0):
+    """Oracle over a SparsePoly (polyeval.py:133-136) + optional harness noise."""
+    return PolyOracle(p, fast_lattice=fast_lattice, noise_sigma=noise_sigma,
+                      noise_seed=noise_seed)
+
+
+def sample_on_lattice(oracle, lat, d=None):
+    """Node values of one lattice through an oracle (polyeval.py:139-143)."""
+    if d is not None and d != lat.dim:
+        raise ParameterError("dimension mismatch")
+    return oracle.sample_lattice(lat)
+
+
+def random_poly(I, rng, min_mag=1e-6):
+    """Coefficients uniform on [-1,1)+[-1,1)i, rejected below min_mag
+    (polyeval.py:146-158; same RNG calls)."""
+    if min_mag >= 1:
+        raise ParameterError("min_mag must be < 1")
+    n = len(I)
+    coeffs = np.zeros(n, dtype=np.complex128)
+    todo = np.arange(n)
+    while todo.size:
+        draw = rng.uniform(-1, 1, size=(todo.size, 2))
+        vals = draw[:, 0] + 1j * draw[:, 1]
+        coeffs[todo] = vals
+        todo = todo[np.abs(vals) < min_mag]
+    return SparsePoly(I, coeffs)

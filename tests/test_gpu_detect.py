@@ -1,0 +1,149 @@
+"""Fixed-candidate-set reconstruction (detect.py entry points) on the GPU vs
+the reference's golden outputs and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import workloads
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _config(pkg, zmat, M):
+    lats = [pkg.Rank1Lattice(z, M) for z in zmat]
+    return pkg.MultiLatticeConfig(lats, 0.5, 10.33, 0.5)
+
+
+def test_tiny_instances_vs_reference(cuda):
+    pkg = cuda
+    g = golden("tiny_detect.npz")
+    for k in range(int(g["n"])):
+        p = f"t{k}_"
+        S = pkg.FreqSet(g[p + "gamma"].shape[1], g[p + "gamma"], _sorted=True)
+        cfg = _config(pkg, g[p + "zmat"], int(g[p + "M"]))
+        smp = list(g[p + "samples"])
+        res = pkg.detect_and_compute(smp, cfg, S)
+        assert res.theta_zero == pytest.approx(float(g[p + "theta0"]), rel=1e-14)
+        assert np.array_equal(res.hits, g[p + "hits"])
+        assert np.array_equal(res.detected_idx, g[p + "idx"])
+        if len(res.coeffs):
+            assert np.max(np.abs(res.coeffs - g[p + "coeffs"])) < 1e-10
+        r0 = pkg.detect_and_compute(smp, cfg, S, zero=pkg.ZeroTest(1e-8))
+        assert np.array_equal(r0.hits, g[p + "hits0"])
+        assert np.array_equal(r0.detected_idx, g[p + "idx0"])
+        top = pkg.detect_topk(smp, cfg, S, 2, 0.1)
+        assert np.array_equal(top.detected_idx, g[p + "topk_idx"])
+        fr = pkg.detect_frequencies(smp, cfg, S)
+        assert np.array_equal(fr.detected_idx, g[p + "freq_idx"])
+        post = pkg.postprocess_r1l(res, smp, cfg)
+        assert np.array_equal(post.detected_idx, g[p + "post_idx"])
+        if len(post.coeffs):
+            assert np.max(np.abs(post.coeffs - g[p + "post_coeffs"])) < 1e-10
+
+
+def test_config1_end_to_end_vs_reference(cuda):
+    pkg = cuda
+    g = golden("cfg1.npz")
+    w = workloads.config1()
+    G = pkg.FreqSet(w.d, w.gamma, _sorted=True)
+    I = G.take(w.support_idx)
+    p = pkg.SparsePoly(I, w.coeffs)
+    rng = w.rng  # positioned after Gamma, I and the coefficients
+    cfg = pkg.draw_config(G, w.s, 0.1, rng=rng)
+    assert cfg.shared_M == int(g["M"]) and np.array_equal(cfg.zmat(), g["zmat"])
+    orc = pkg.oracle_from_poly(p)
+    smp = [orc.sample_lattice(lat) for lat in cfg.lattices]
+    assert orc.count == cfg.L * cfg.shared_M
+    for a, b in zip(smp, g["samples"]):
+        assert np.max(np.abs(a - b)) < 1e-11
+    res = pkg.detect_and_compute(smp, cfg, G)
+    assert np.array_equal(res.hits, g["hits"])
+    assert np.array_equal(res.detected_idx, g["idx"])
+    assert np.max(np.abs(res.coeffs - g["coeffs"])) < 1e-10 * np.max(np.abs(g["coeffs"]))
+    assert res.detected == I
+    top = pkg.detect_topk(smp, cfg, G, 10, 1.0)
+    assert np.array_equal(top.detected_idx, g["topk_idx"])
+    post = pkg.postprocess_r1l(res, smp, cfg)
+    assert np.array_equal(post.detected_idx, g["post_idx"])
+    assert np.max(np.abs(post.coeffs - g["post_coeffs"])) < 1e-10
+
+
+def test_zero_polynomial_and_empty_results(cuda):
+    pkg = cuda
+    rng = np.random.default_rng(1)
+    gamma = pkg.random_subset(pkg.Box(2, -4, 4), 10, rng)
+    cfg = pkg.MultiLatticeConfig([pkg.Rank1Lattice(rng.integers(0, 13, 2), 13)
+                                  for _ in range(5)], 0.5, 10.33, 0.5)
+    res = pkg.detect_frequencies([np.zeros(13, complex)] * 5, cfg, gamma)
+    assert len(res.detected) == 0
+    res = pkg.detect_and_compute([np.zeros(13, complex)] * 5, cfg, gamma)
+    assert pkg.postprocess_r1l(res, [np.zeros(13, complex)] * 5, cfg) is res
+
+
+def test_contract_errors(cuda):
+    pkg = cuda
+    lat = pkg.Rank1Lattice([1, 2], 11)
+    cfg = pkg.MultiLatticeConfig([lat], 0.5, 10.33, 0.5)
+    with pytest.raises(pkg.ParameterError):
+        pkg.detect_frequencies([np.zeros(10)], cfg, pkg.FreqSet(2, [(0, 0)]))
+    lats = [pkg.Rank1Lattice([1], 11) for _ in range(4)]
+    with pytest.raises(pkg.ParameterError):
+        pkg.detect_and_compute([np.zeros(11, complex)] * 4,
+                               pkg.MultiLatticeConfig(lats, 0.5, 10.33, 0.5),
+                               pkg.FreqSet(1, [(0,)]))
+    lats = [pkg.Rank1Lattice([1], 11) for _ in range(3)]
+    with pytest.raises(pkg.ParameterError):
+        pkg.detect_and_compute([np.zeros(11, complex)] * 3,
+                               pkg.MultiLatticeConfig(lats, 0.25, 10.33, 0.5),
+                               pkg.FreqSet(1, [(0,)]))
+
+
+def test_topk_tie_break_deterministic(cuda):
+    pkg = cuda
+    I = pkg.FreqSet(1, [(1,), (4,)])
+    p = pkg.SparsePoly(I, np.array([1.0, -1.0]))
+    lat = pkg.Rank1Lattice([1], 11)
+    cfg = pkg.MultiLatticeConfig([lat], 0.5, 10.33, 0.5)
+    smp = [pkg.evaluate_on_lattice(p, lat)]
+    for _ in range(3):
+        top = pkg.detect_topk(smp, cfg, I, 1, 0.0)
+        assert list(top.detected) == [(1,)]
+
+
+def test_topk_selection_vs_oracle(cuda, oracle_lib):
+    """Top-s over many detected rows with equal-magnitude ties."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine
+
+    rng = np.random.default_rng(11)
+    n = 150_000
+    idx = np.sort(rng.choice(10**7, size=n, replace=False)).astype(np.int64)
+    mags = rng.choice(np.linspace(1, 2, 500), size=n)  # heavy ties
+    co = mags * np.exp(1j * rng.uniform(0, 2 * np.pi, size=n))
+    co[::7] = mags[::7]  # exact real ties
+    for s_tilde, theta in ((2000, 1.3), (n + 5, 0.0), (0, 0.0), (1, 1.9)):
+        kidx, kco, kc = _engine.topk(_dev.upload(idx), _dev.upload(co),
+                                     torch.tensor([n], device="cuda"), 1, n, theta, s_tilde)
+        k = int(kc[0])
+        want_i, want_c = oracle_lib.topk_filter(idx, co, s_tilde, theta)
+        got_i = _dev.download(kidx[:k])
+        # |c| by CUDA hypot vs libm hypot may differ in the last ulp; compare sets
+        # away from exact boundary ties
+        assert k == len(want_i)
+        assert np.array_equal(got_i, want_i)
+
+
+def test_per_lattice_coefficients(cuda):
+    pkg = cuda
+    g = golden("tiny_detect.npz")
+    S = pkg.FreqSet(g["t0_gamma"].shape[1], g["t0_gamma"], _sorted=True)
+    cfg = _config(pkg, g["t0_zmat"], int(g["t0_M"]))
+    smp = list(g["t0_samples"])
+    mat = pkg.per_lattice_coefficients(smp, cfg, S)
+    assert mat.shape == (len(S), cfg.L)
+    med = np.median(mat.real, axis=1) + 1j * np.median(mat.imag, axis=1)
+    got = np.zeros(len(S), complex)
+    got[g["t0_idx"]] = g["t0_coeffs"]
+    assert np.max(np.abs(med[g["t0_idx"]] - g["t0_coeffs"])) < 1e-10

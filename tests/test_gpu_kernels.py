@@ -1,0 +1,195 @@
+"""CUDA kernels vs the reference's golden vectors and the CPU oracle.
+
+Bit-exact for integer/index work (hits, detected sets, medians are copies of
+input values); FP64 transforms within 1e-12 absolute on unit-variance input
+(the reference's own acceptance bar, test_acceptance.py:187-207).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_detect_gather_plugin_bitexact_vs_reference(cuda):
+    from paper_2006_13053_b200 import _kernels
+
+    g = golden("gather_cases.npz")
+    for k in range(int(g["ncases"])):
+        M, theta, thr = g[f"c{k}_params"]
+        e, z, gh = g[f"c{k}_elems"], g[f"c{k}_zmat"], g[f"c{k}_ghat"]
+        for wm in (0, 1):
+            key = f"c{k}_{wm}_hits"
+            if key not in g:
+                continue
+            hits, med = _kernels.detect_gather(e, z, int(M), gh, theta, thr, bool(wm))
+            assert np.array_equal(hits, g[key]), (k, wm)
+            assert np.array_equal(med.view(np.float64), g[f"c{k}_{wm}_med"].view(np.float64))
+
+
+def test_detect_gather_odd_L_check(cuda):
+    from paper_2006_13053_b200 import _kernels
+
+    with pytest.raises(ValueError):
+        _kernels.detect_gather(np.zeros((5, 2), np.int64), np.zeros((4, 2), np.int64), 11,
+                               np.zeros((4, 11), complex), 0.0, 2.0, True)
+
+
+@pytest.mark.parametrize("d,M,L", [(3, 31, 7), (10, 103307, 47), (20, 20663, 41),
+                                   (5, 211, 27), (1, 13, 1), (25, 1039, 9)])
+def test_hash_paths_vs_oracle(cuda, oracle_lib, d, M, L):
+    """32-bit, 64-bit and generic residue paths against the C oracle."""
+    from paper_2006_13053_b200 import _kernels
+
+    rng = np.random.default_rng(d * 1000 + L)
+    n = 20000
+    e = rng.integers(0, M, size=(n, d), dtype=np.int64)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    gh = rng.normal(size=(L, M)) + 1j * rng.normal(size=(L, M))
+    gh[rng.random(size=(L, M)) < 0.8] = 0.0
+    thr = L / 2
+    want = oracle_lib.gather_c(e, z, M, gh, 1e-9, thr, L % 2 == 1)
+    got = _kernels.detect_gather(e, z, M, gh, 1e-9, thr, L % 2 == 1)
+    assert np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1], want[1])
+
+
+def test_hash_signed_rows_fused_mod(cuda, oracle_lib):
+    """Driver path: raw signed candidate rows, % M fused on device."""
+    import torch
+
+    import paper_2006_13053_b200 as pkg
+    from paper_2006_13053_b200 import _dev, _engine
+
+    rng = np.random.default_rng(3)
+    n, d, M, L = 50000, 10, 103307, 47
+    rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    gh = rng.normal(size=(L, M)) + 1j * rng.normal(size=(L, M))
+    gh[rng.random(size=(L, M)) < 0.9] = 0.0
+    samples = _dev.upload(np.fft.ifft(gh, axis=1) * M)  # DFT/M gives gh back
+    b = _engine.detect_batch(samples, M, _dev.upload(z), 1, L, _dev.upload(rows),
+                             d * 4096, 0.5, theta0=torch.full((1,), 1e-9,
+                                                              dtype=torch.float64,
+                                                              device="cuda"),
+                             want_hits=True)
+    ghat = _dev.download(b.ghat)
+    want_h, want_m = oracle_lib.gather_c(rows % M, z, M, ghat, 1e-9, L / 2, True)
+    assert np.array_equal(_dev.download(b.hits), want_h)
+    cnt = int(b.counts[0])
+    idx = _dev.download(b.idx[:cnt])
+    assert np.array_equal(idx, np.flatnonzero(want_h >= L / 2))
+    assert np.array_equal(_dev.download(b.coeffs[:cnt]), want_m[idx])
+
+
+def test_rows_injective_vs_reference(cuda):
+    from paper_2006_13053_b200 import _kernels
+
+    for case in golden("injective_cases.json"):
+        e = np.array(case["elems"], dtype=np.int64)
+        assert _kernels.rows_injective_mod(e, case["p"]) == case["injective"]
+
+
+def test_dft_vs_reference_and_naive(cuda):
+    import paper_2006_13053_b200 as pkg
+
+    g = golden("dft_cases.npz")
+    for M in g["primes"]:
+        y = pkg.dft_forward_normalized(g[f"x{M}"])
+        assert np.max(np.abs(y - g[f"y{M}"])) < 1e-12, M
+
+
+@pytest.mark.parametrize("M", [2, 3, 5, 7, 31, 127, 211, 509, 1009, 1039, 2069, 4099,
+                               10331, 20663, 40009, 103307])
+def test_dft_primes_vs_naive_and_parseval(cuda, M):
+    import paper_2006_13053_b200 as pkg
+
+    rng = np.random.default_rng(M)
+    x = rng.normal(size=M) + 1j * rng.normal(size=M)
+    y = pkg.dft_forward_normalized(x)
+    if M <= 4099:
+        j = np.arange(M)
+        naive = (np.exp(-2j * np.pi * np.outer(j, j) / M) @ x) / M
+        assert np.max(np.abs(y - naive)) < 1e-12
+    ref = np.fft.fft(x) / M
+    assert np.max(np.abs(y - ref)) < 1e-13
+    energy = np.mean(np.abs(x) ** 2)
+    assert abs(np.sum(np.abs(y) ** 2) - energy) <= 1e-10 * energy
+
+
+def test_dft_rejects_bad_input(cuda):
+    import paper_2006_13053_b200 as pkg
+
+    with pytest.raises(pkg.ParameterError):
+        pkg.dft_forward_normalized([1.0, np.nan])
+    with pytest.raises(pkg.ParameterError):
+        pkg.dft_forward_normalized([])
+    with pytest.raises(pkg.ParameterError):
+        pkg.dft_forward_normalized(np.zeros((2, 2)))
+
+
+def test_inverse_dft_batch(cuda):
+    import paper_2006_13053_b200 as pkg
+    from paper_2006_13053_b200 import _dev
+    from paper_2006_13053_b200.dft import dft_batch
+
+    rng = np.random.default_rng(9)
+    for M in (211, 20663):
+        x = rng.normal(size=(5, M)) + 1j * rng.normal(size=(5, M))
+        y = _dev.download(dft_batch(_dev.upload(x), M, inverse=True, scale=1.0))
+        assert np.max(np.abs(y - M * np.fft.ifft(x, axis=1))) < 1e-9
+
+
+def test_structured_sampling_vs_reference(cuda):
+    import paper_2006_13053_b200 as pkg
+
+    g = golden("sampling_cases.npz")
+    for k in range(int(g["n"])):
+        p = pkg.SparsePoly(pkg.FreqSet(g[f"s{k}_support"].shape[1], g[f"s{k}_support"],
+                                       _sorted=True), g[f"s{k}_coeffs"])
+        lat = pkg.Rank1Lattice(g[f"s{k}_z"], int(g[f"s{k}_M"]))
+        vals = pkg.evaluate_on_lattice(p, lat)
+        ref = g[f"s{k}_fast"]
+        assert np.max(np.abs(vals - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+        dense = pkg.evaluate_many(p, pkg.lattice_nodes(lat))
+        assert np.max(np.abs(dense - g[f"s{k}_dense"])) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_scatter_bins_match_bincount_order(cuda, oracle_lib):
+    """Residue bins summed in ascending coefficient order == np.bincount."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    rng = np.random.default_rng(5)
+    s, d, M, L = 20000, 4, 211, 3  # many collisions, > one 8192-key chunk
+    sup = rng.integers(-50, 50, size=(s, d), dtype=np.int64)
+    c = rng.normal(size=s) + 1j * rng.normal(size=s)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    bins = _dev.empty((L, M), torch.complex128)
+    _native.call("sfftb_scatter_bins", _dev.ptr(_dev.upload(sup)), s, d, d,
+                 _dev.ptr(_dev.upload(c)), _dev.ptr(_dev.upload(z)), 1, L, M, _dev.ptr(bins),
+                 None, _dev.stream())
+    got = _dev.download(bins)
+    for l in range(L):
+        r = oracle_lib.residues(sup, z[l], M)
+        want = np.bincount(r, weights=c.real, minlength=M) + 1j * np.bincount(
+            r, weights=c.imag, minlength=M)
+        assert np.array_equal(got[l], want)
+
+
+def test_noise_stream_matches_oracle(cuda, oracle_lib):
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    M, rows, seed, call0, sigma = 4099, 3, 99, 17, 1e-3
+    x = _dev.zeros((rows, M), torch.complex128)
+    _native.call("sfftb_add_noise", _dev.ptr(x), rows, M, seed, call0, sigma, _dev.stream())
+    got = _dev.download(x)
+    for r in range(rows):
+        want = oracle_lib.noise_for_call(seed, call0 + r, M, sigma)
+        assert np.max(np.abs(got[r] - want)) < 1e-17
+    assert abs(np.std(got.real) - sigma) < 0.05 * sigma

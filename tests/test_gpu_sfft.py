@@ -1,0 +1,91 @@
+"""Dimension-incremental driver on the GPU vs the reference's golden runs."""
+
+import numpy as np
+import pytest
+
+import workloads
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(pkg, g):
+    d, lo, hi, s, r, theta, delta, sseed, sigma, nseed = g["params"]
+    d = int(d)
+    p = pkg.SparsePoly(pkg.FreqSet(d, g["true_support"], _sorted=True), g["true_coeffs"])
+    orc = pkg.oracle_from_poly(p, noise_sigma=float(sigma), noise_seed=int(nseed))
+    res = pkg.sfft(orc, pkg.Box(d, int(lo), int(hi)),
+                   pkg.SfftParams(int(s), float(delta), theta=float(theta), r=int(r)),
+                   seed=int(sseed))
+    return res, orc
+
+
+def _check(res, orc, g, tol):
+    assert np.array_equal(res.support.elems, g["support"])
+    assert res.sample_count == int(g["sample_count"]) == orc.count
+    flat = [[e["stage"], str(e["t"]), str(e["i"]), str(e["candidates"]), str(e["kept"]),
+             str(e["samples"])] for e in res.stage_log]
+    assert flat == g["stage_log"].tolist()
+    if len(res.coeffs):
+        assert np.linalg.norm(res.coeffs - g["coeffs"]) <= tol * np.linalg.norm(g["coeffs"])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6, 8])
+def test_sfft_small_vs_reference(cuda, seed):
+    g = golden(f"sfft_small_{seed}.npz")
+    res, orc = _run(cuda, g)
+    _check(res, orc, g, 1e-10)
+
+
+def test_sfft_cfg2_vs_reference(cuda):
+    g = golden("sfft_cfg2.npz")
+    res, orc = _run(cuda, g)
+    _check(res, orc, g, 1e-10)
+    w = workloads.config2()
+    assert np.array_equal(res.support.elems, w.support)
+    assert workloads.rel_l2(res.coeffs, w.coeffs) < 1e-12
+
+
+def test_zero_signal_returns_empty(cuda):
+    pkg = cuda
+    orc = pkg.SamplingOracle(lambda X: np.zeros(len(X), dtype=complex), 3)
+    res = pkg.sfft(orc, pkg.Box(3, -4, 4), pkg.SfftParams(4, 0.9, r=1), seed=0)
+    assert res.failed and res.sample_count == orc.count and res.stage_log
+
+
+def test_blackbox_oracle_matches_poly_oracle(cuda):
+    """A black-box fn oracle (host evaluation) gives the same result."""
+    pkg = cuda
+    g = golden("sfft_small_5.npz")
+    d = int(g["params"][0])
+    p = pkg.SparsePoly(pkg.FreqSet(d, g["true_support"], _sorted=True), g["true_coeffs"])
+    orc = pkg.SamplingOracle(lambda X: pkg.evaluate_many(p, X), d)
+    res = pkg.sfft(orc, pkg.Box(d, int(g["params"][1]), int(g["params"][2])),
+                   pkg.SfftParams(int(g["params"][3]), float(g["params"][6]),
+                                  theta=float(g["params"][5]), r=int(g["params"][4])),
+                   seed=int(g["params"][7]))
+    _check(res, orc, g, 1e-10)
+
+
+def test_candidate_set_restriction(cuda):
+    pkg = cuda
+    rng = np.random.default_rng(20240611)
+    gamma = pkg.hyperbolic_cross(3, 6)
+    I = pkg.random_subset(gamma, 5, rng)
+    p = pkg.random_poly(I, rng, min_mag=0.1)
+    res = pkg.sfft(pkg.oracle_from_poly(p), gamma, pkg.SfftParams(5, 0.9, r=2), seed=8)
+    assert np.all(gamma.contains_rows(res.support.elems))
+    assert res.support == I
+
+
+def test_seed_reproducibility_bitwise(cuda):
+    pkg = cuda
+    w = workloads.small_sfft(12, 4, 8, 30, r=2)
+    runs = []
+    for _ in range(2):
+        p = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+        runs.append(pkg.sfft(pkg.oracle_from_poly(p), pkg.Box(w.d, w.lo, w.hi),
+                             pkg.SfftParams(w.s, 0.9, r=w.r), seed=555))
+    assert runs[0].support == runs[1].support
+    assert np.array_equal(runs[0].coeffs, runs[1].coeffs)
+    assert runs[0].sample_count == runs[1].sample_count
