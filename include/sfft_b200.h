@@ -39,6 +39,8 @@ extern "C" {
 
 const char *sfftb_version(void);
 const char *sfftb_last_error(void);
+/* Number of CUDA kernels the library has launched so far (all threads). */
+int64_t sfftb_launch_count(void);
 /* Release the cached Bluestein plans of every device. */
 int sfftb_plan_cache_clear(void);
 

@@ -7,6 +7,8 @@ the Python side.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -40,9 +42,12 @@ def ptr(t):
 def upload(arr, dtype=None):
     """numpy -> contiguous CUDA tensor (int64 / float64 / complex128)."""
     a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
-    t = torch.from_numpy(a)
+    with warnings.catch_warnings():  # read-only FreqSet rows: torch only reads them
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(a)
     if t.numel() >= (1 << 20):
-        t = t.pin_memory()
+        if not t.is_pinned():
+            t = t.pin_memory()
         return t.to(device(), non_blocking=True)
     return t.to(device())
 

@@ -30,6 +30,7 @@ _SIGS = {
     "sfftb_version": (ctypes.c_char_p, []),
     "sfftb_last_error": (ctypes.c_char_p, []),
     "sfftb_plan_cache_clear": (_int, []),
+    "sfftb_launch_count": (_i64, []),
     "sfftb_detect_gather": (_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _dbl, _dbl, _int,
                                    _p, _p]),
     "sfftb_rows_injective_mod": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int)]),
@@ -103,8 +104,58 @@ def check(rc, what=""):
     raise RuntimeError(msg)
 
 
+_TIMELINE = None
+
+
+class Timeline:
+    """Record CUDA events around every C-ABI call made while active.
+
+    Events are recorded on the current torch stream -- the stream the
+    library launches on -- so ``ms()`` gives each entry point's device time
+    (used by bench.py for the per-kernel roofline numbers)."""
+
+    def __init__(self):
+        self.records = []
+
+    def __enter__(self):
+        global _TIMELINE
+        self._prev, _TIMELINE = _TIMELINE, self
+        return self
+
+    def __exit__(self, *exc):
+        global _TIMELINE
+        _TIMELINE = self._prev
+        return False
+
+    def ms(self):
+        """{entry point: [ms per call, ...]} (synchronises)."""
+        import torch
+
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b in self.records:
+            out.setdefault(name, []).append(a.elapsed_time(b))
+        return out
+
+
 def call(name, *args):
-    check(getattr(lib(), name)(*args), name)
+    tl = _TIMELINE
+    if tl is None:
+        check(getattr(lib(), name)(*args), name)
+        return
+    import torch
+
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = getattr(lib(), name)(*args)
+    b.record()
+    tl.records.append((name, a, b))
+    check(rc, name)
+
+
+def launch_count():
+    return int(lib().sfftb_launch_count())
 
 
 def version():

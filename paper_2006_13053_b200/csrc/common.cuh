@@ -24,7 +24,13 @@ void set_error(const std::string& msg);
         }                                                                   \
     } while (0)
 
-#define SFFTB_CHECK_LAUNCH() SFFTB_CUDA(cudaGetLastError())
+// Count of kernels this library launched (sfftb_launch_count()).
+void count_launch();
+#define SFFTB_CHECK_LAUNCH()          \
+    do {                              \
+        ::sfftb::count_launch();      \
+        SFFTB_CUDA(cudaGetLastError()); \
+    } while (0)
 
 #define SFFTB_REQUIRE(cond, msg)                                            \
     do {                                                                    \

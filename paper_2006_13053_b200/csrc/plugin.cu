@@ -12,6 +12,7 @@
 // reference's nogil kernels.
 #include <math.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,9 @@ namespace sfftb {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 __global__ void scatter_medians_kernel(const int64_t* __restrict__ idx,
                                        const int64_t* __restrict__ count,
@@ -85,6 +89,7 @@ using namespace sfftb;
 
 extern "C" const char* sfftb_version(void) { return "sfftb200 0.1.0 (sm_100a)"; }
 extern "C" const char* sfftb_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t sfftb_launch_count(void) { return g_launches.load(); }
 
 extern "C" int sfftb_hc_count(int d, double bound, const double* weights, int64_t* count) {
     SFFTB_REQUIRE(d >= 1 && d <= 64, "hc_count: 1 <= d <= 64");

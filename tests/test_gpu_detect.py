@@ -10,6 +10,25 @@ from conftest import golden
 pytestmark = pytest.mark.gpu
 
 
+def assert_topk_equivalent(got, want, cand_idx, cand_coeffs, rtol=1e-12):
+    """Top-s sets agree, up to roundoff-level ties at the cut-off.
+
+    An exact magnitude tie in the reference (broken by candidate index) can
+    come from two different FFT bins that pocketfft happened to round
+    identically; the B200 Bluestein rounds them within ~1e-16 relative but
+    not bit-identically, so such a tie may resolve the other way.  Every
+    element in the symmetric difference must sit at the cut-off magnitude
+    within rtol."""
+    got, want = np.asarray(got), np.asarray(want)
+    if np.array_equal(got, want):
+        return
+    assert len(got) == len(want)
+    mags = dict(zip(np.asarray(cand_idx).tolist(), np.abs(cand_coeffs).tolist()))
+    cutoff = min(mags[i] for i in want.tolist())
+    for e in set(got.tolist()) ^ set(want.tolist()):
+        assert abs(mags[e] - cutoff) <= rtol * cutoff, (e, mags[e], cutoff)
+
+
 def _config(pkg, zmat, M):
     lats = [pkg.Rank1Lattice(z, M) for z in zmat]
     return pkg.MultiLatticeConfig(lats, 0.5, 10.33, 0.5)
@@ -33,7 +52,8 @@ def test_tiny_instances_vs_reference(cuda):
         assert np.array_equal(r0.hits, g[p + "hits0"])
         assert np.array_equal(r0.detected_idx, g[p + "idx0"])
         top = pkg.detect_topk(smp, cfg, S, 2, 0.1)
-        assert np.array_equal(top.detected_idx, g[p + "topk_idx"])
+        assert_topk_equivalent(top.detected_idx, g[p + "topk_idx"], g[p + "idx"],
+                               g[p + "coeffs"])
         fr = pkg.detect_frequencies(smp, cfg, S)
         assert np.array_equal(fr.detected_idx, g[p + "freq_idx"])
         post = pkg.postprocess_r1l(res, smp, cfg)
@@ -63,7 +83,7 @@ def test_config1_end_to_end_vs_reference(cuda):
     assert np.max(np.abs(res.coeffs - g["coeffs"])) < 1e-10 * np.max(np.abs(g["coeffs"]))
     assert res.detected == I
     top = pkg.detect_topk(smp, cfg, G, 10, 1.0)
-    assert np.array_equal(top.detected_idx, g["topk_idx"])
+    assert_topk_equivalent(top.detected_idx, g["topk_idx"], g["idx"], g["coeffs"])
     post = pkg.postprocess_r1l(res, smp, cfg)
     assert np.array_equal(post.detected_idx, g["post_idx"])
     assert np.max(np.abs(post.coeffs - g["post_coeffs"])) < 1e-10
@@ -112,7 +132,8 @@ def test_topk_tie_break_deterministic(cuda):
 
 
 def test_topk_selection_vs_oracle(cuda, oracle_lib):
-    """Top-s over many detected rows with equal-magnitude ties."""
+    """Top-s over many detected rows with exact magnitude ties (purely real or
+    imaginary coefficients: |c| is exact in both libms)."""
     import torch
 
     from paper_2006_13053_b200 import _dev, _engine
@@ -120,19 +141,17 @@ def test_topk_selection_vs_oracle(cuda, oracle_lib):
     rng = np.random.default_rng(11)
     n = 150_000
     idx = np.sort(rng.choice(10**7, size=n, replace=False)).astype(np.int64)
-    mags = rng.choice(np.linspace(1, 2, 500), size=n)  # heavy ties
-    co = mags * np.exp(1j * rng.uniform(0, 2 * np.pi, size=n))
-    co[::7] = mags[::7]  # exact real ties
-    for s_tilde, theta in ((2000, 1.3), (n + 5, 0.0), (0, 0.0), (1, 1.9)):
-        kidx, kco, kc = _engine.topk(_dev.upload(idx), _dev.upload(co),
-                                     torch.tensor([n], device="cuda"), 1, n, theta, s_tilde)
+    mags = rng.choice(np.linspace(1, 2, 500), size=n) * rng.choice([-1.0, 1.0], size=n)
+    co = np.where(rng.random(n) < 0.5, mags + 0j, 1j * mags)
+    idx_d, co_d = _dev.upload(idx), _dev.upload(co)
+    cnt = torch.tensor([n], device="cuda")
+    for s_tilde, theta in ((2000, 1.3), (n + 5, 0.0), (0, 0.0), (1, 1.9), (70_000, 1.0)):
+        kidx, kco, kc = _engine.topk(idx_d, co_d, cnt, 1, n, theta, s_tilde)
         k = int(kc[0])
         want_i, want_c = oracle_lib.topk_filter(idx, co, s_tilde, theta)
-        got_i = _dev.download(kidx[:k])
-        # |c| by CUDA hypot vs libm hypot may differ in the last ulp; compare sets
-        # away from exact boundary ties
         assert k == len(want_i)
-        assert np.array_equal(got_i, want_i)
+        assert np.array_equal(_dev.download(kidx[:k]), want_i)
+        assert np.array_equal(_dev.download(kco[:k]), want_c)
 
 
 def test_per_lattice_coefficients(cuda):

@@ -169,9 +169,9 @@ def test_scatter_bins_match_bincount_order(cuda, oracle_lib):
     c = rng.normal(size=s) + 1j * rng.normal(size=s)
     z = rng.integers(0, M, size=(L, d), dtype=np.int64)
     bins = _dev.empty((L, M), torch.complex128)
-    _native.call("sfftb_scatter_bins", _dev.ptr(_dev.upload(sup)), s, d, d,
-                 _dev.ptr(_dev.upload(c)), _dev.ptr(_dev.upload(z)), 1, L, M, _dev.ptr(bins),
-                 None, _dev.stream())
+    sup_d, c_d, z_d = _dev.upload(sup), _dev.upload(c), _dev.upload(z)  # keep alive
+    _native.call("sfftb_scatter_bins", _dev.ptr(sup_d), s, d, d, _dev.ptr(c_d), _dev.ptr(z_d),
+                 1, L, M, _dev.ptr(bins), None, _dev.stream())
     got = _dev.download(bins)
     for l in range(L):
         r = oracle_lib.residues(sup, z[l], M)
