@@ -21,8 +21,8 @@
 
 namespace sfftb {
 
-static constexpr int kHashThreads = 256;
-static constexpr size_t kBitmapSmemBudget = 192 * 1024;
+static constexpr int kHashThreads = 512;
+static constexpr size_t kBitmapSmemBudget = 200 * 1024;
 
 struct HashArgs {
     const int64_t* elems;
@@ -34,6 +34,7 @@ struct HashArgs {
     const uint32_t* bits;  // G*L*W
     int64_t W;
     int Lc;              // lattices per shared-memory chunk
+    int nbuf;            // 1 (all bitmaps resident) or 2 (double-buffered chunks)
     uint32_t offset;     // multiple of M >= |residue sum| (32-bit path)
     uint32_t magic;      // floor((2^32-1)/M)
     int64_t min_hits;
@@ -42,9 +43,12 @@ struct HashArgs {
     int64_t nwords;
 };
 
-__device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t M, uint32_t magic) {
-    uint32_t q = __umulhi(u, magic);  // q in {floor(u/M)-1, floor(u/M)}
-    uint32_t r = u - q * M;           // r in [0, 2M)
+// r = u mod M for u < 2^32: q = umulhi(u, floor((2^32-1)/M)) is floor(u/M)
+// or one less, so u + q*(-M) lies in [0, 2M) and one unsigned min finishes.
+__device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t M, uint32_t negM,
+                                            uint32_t magic) {
+    const uint32_t q = __umulhi(u, magic);
+    const uint32_t r = u + q * negM;
     return min(r, r - M);
 }
 
@@ -57,31 +61,74 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t M, double invM)
     return (uint64_t)r;
 }
 
-// Load the bitmaps of lattices [l0, l0+cnt) of group g into shared memory.
+// Synchronous cooperative copy (generic fallback kernel only).
 __device__ __forceinline__ void load_bits(uint32_t* dst, const HashArgs& a, int g, int l0,
                                           int cnt) {
     const uint4* src = reinterpret_cast<const uint4*>(a.bits + ((int64_t)g * a.L + l0) * a.W);
     const int64_t words = (int64_t)cnt * a.W;
     uint4* d4 = reinterpret_cast<uint4*>(dst);
-    // a.W is padded to a multiple of 4 words by the host
     for (int64_t i = threadIdx.x; i < words / 4; i += blockDim.x) d4[i] = __ldg(src + i);
+}
+
+// Candidate rows of one warp slice into registers (row = base + q*32 + lane).
+template <int D, int R, bool WIDE>
+__device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int lane,
+                                          int32_t (&k)[R][D], uint32_t (&ku)[WIDE ? R : 1][WIDE ? D : 1],
+                                          bool (&valid)[R]) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int64_t i = base + q * 32 + lane;
+        valid[q] = i < a.n;
+        const int64_t* row = a.elems + (valid[q] ? i : 0) * D;
+        int64_t v[D];
+        if (D % 2 == 0) {
+#pragma unroll
+            for (int j = 0; j < D; j += 2) {
+                const longlong2 p = __ldg(reinterpret_cast<const longlong2*>(row + j));
+                v[j] = p.x;
+                v[j + 1] = p.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) v[j] = __ldg(row + j);
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if (!valid[q]) v[j] = 0;
+            if (WIDE) {
+                int64_t m = v[j] % a.M;
+                if (m < 0) m += a.M;
+                ku[WIDE ? q : 0][WIDE ? j : 0] = (uint32_t)m;
+                k[q][j] = 0;
+            } else {
+                k[q][j] = (int32_t)v[j];
+            }
+        }
+    }
 }
 
 // WIDE = false: 32-bit residue path (values truncated to int32, exact by the
 // host's bound check); WIDE = true: exact 64-bit path for any int64 input.
+//
+// Shared memory: [z (L*D int32)] [2 mbarriers] [bitmap buffer 0] [buffer 1].
+// With nbuf == 2 the bitmaps of Lc lattices at a time stream through two
+// buffers: thread 0 issues a 1-D bulk copy (TMA engine, completion on an
+// mbarrier) for chunk q+2 as soon as every warp is done with chunk q, so the
+// L2 -> SMEM transfer overlaps the hashing of chunk q+1.
 template <int D, int R, bool WIDE>
-__global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
-    extern __shared__ uint32_t smem_u32[];
+__global__ void __launch_bounds__(kHashThreads, 1) hash_rows(HashArgs a) {
+    extern __shared__ __align__(16) uint32_t smem_u32[];
     const int g = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int WARPS = kHashThreads / 32;
     constexpr int TILE = WARPS * 32 * R;
-    const uint32_t M32 = (uint32_t)a.M;
+    const uint32_t M32 = (uint32_t)a.M, negM = 0u - M32;
 
-    // generators of this group, centered (32-bit path) or as-is (64-bit path)
     int32_t* zc = reinterpret_cast<int32_t*>(smem_u32);
     const int zwords = ((a.L * D + 3) & ~3);
-    uint32_t* bm = smem_u32 + zwords;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_u32 + zwords);
+    uint32_t* buf0 = smem_u32 + zwords + 4;
+    uint32_t* buf1 = buf0 + (int64_t)a.Lc * a.W;
     for (int i = threadIdx.x; i < a.L * D; i += blockDim.x) {
         int64_t z = a.zmat[(int64_t)g * a.L * D + i] % a.M;
         if (z < 0) z += a.M;
@@ -89,33 +136,45 @@ __global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
         zc[i] = (int32_t)z;
     }
     const int nchunks = (a.L + a.Lc - 1) / a.Lc;
-    if (nchunks == 1) load_bits(bm, a, g, 0, a.L);
+    const bool resident = nchunks == 1;
+    const int64_t ntiles = (a.n + TILE - 1) / TILE;
+    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total_q = resident ? (my_tiles ? 1 : 0) : my_tiles * nchunks;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
+    auto issue = [&](int64_t qi) {
+        const int c = resident ? 0 : (int)(qi % nchunks);
+        const int l0 = c * a.Lc;
+        const int cnt = min(a.L, l0 + a.Lc) - l0;
+        const uint32_t bytes = (uint32_t)(cnt * a.W * 4);
+        uint64_t* bar = &bars[qi & 1];
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_g2s((qi & 1) ? buf1 : buf0, a.bits + ((int64_t)g * a.L + l0) * a.W, bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        if (total_q > 0) issue(0);
+        if (total_q > 1) issue(1);
+    }
 
     const double invM = 1.0 / (double)a.M;
-    const int64_t ntiles = (a.n + TILE - 1) / TILE;
+    int64_t qc = 0;  // chunk counter of this CTA
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t base = tile * TILE + (int64_t)warp * 32 * R;
-        // rows in registers: row base + q*32 + lane
         int32_t k[R][D];
         uint32_t ku[WIDE ? R : 1][WIDE ? D : 1];
         bool valid[R];
+        load_rows<D, R, WIDE>(a, base, lane, k, ku, valid);
+        {  // warm L2 with the next tile's rows while this one is hashed
+            const int64_t nb = (tile + gridDim.x) * TILE + (int64_t)warp * 32 * R;
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const int64_t i = base + q * 32 + lane;
-            valid[q] = i < a.n;
-            const int64_t* row = a.elems + (valid[q] ? i : 0) * D;
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                int64_t v = valid[q] ? __ldg(row + j) : 0;
-                if (WIDE) {
-                    int64_t m = v % a.M;
-                    if (m < 0) m += a.M;
-                    ku[WIDE ? q : 0][WIDE ? j : 0] = (uint32_t)m;
-                    k[q][j] = 0;
-                } else {
-                    k[q][j] = (int32_t)v;
-                }
+            for (int q = 0; q < R; ++q) {
+                const int64_t i = nb + q * 32 + lane;
+                if (i < a.n) prefetch_l2(a.elems + i * D);
             }
         }
         int hits[R];
@@ -123,19 +182,17 @@ __global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
         for (int q = 0; q < R; ++q) hits[q] = 0;
 
         for (int c = 0; c < nchunks; ++c) {
+            const int64_t qq = resident ? 0 : qc;
+            mbar_wait(&bars[qq & 1], (uint32_t)((qq >> 1) & 1));
+            const uint32_t* buf = (qq & 1) ? buf1 : buf0;
             const int l0 = c * a.Lc;
             const int lend = min(a.L, l0 + a.Lc);
-            if (nchunks > 1) {
-                __syncthreads();
-                load_bits(bm, a, g, l0, lend - l0);
-                __syncthreads();
-            }
             for (int l = l0; l < lend; ++l) {
                 const int32_t* z = zc + l * D;
                 int32_t zr[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) zr[j] = z[j];
-                const uint32_t* bl = bm + (int64_t)(l - l0) * a.W;
+                const uint32_t* bl = buf + (int64_t)(l - l0) * a.W;
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     uint32_t r;
@@ -143,7 +200,7 @@ __global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
                         uint32_t u = a.offset;
 #pragma unroll
                         for (int j = 0; j < D; ++j) u += (uint32_t)k[q][j] * (uint32_t)zr[j];
-                        r = mod_u32(u, M32, a.magic);
+                        r = mod_u32(u, M32, negM, a.magic);
                     } else {
                         uint64_t acc = 0;
 #pragma unroll
@@ -154,6 +211,11 @@ __global__ void __launch_bounds__(kHashThreads) hash_rows(HashArgs a) {
                     const uint32_t w = bl[r >> 5];
                     hits[q] += (w >> (r & 31)) & 1u;
                 }
+            }
+            if (!resident) {
+                __syncthreads();  // every warp is done with this buffer
+                if (threadIdx.x == 0 && qc + 2 < total_q) issue(qc + 2);
+                ++qc;
             }
         }
 #pragma unroll
@@ -545,7 +607,7 @@ static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
 template <int D, bool WIDE>
 static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
     // rows per thread: keep R*D <= ~96 int32 registers
-    constexpr int R = D <= 6 ? 16 : (D <= 12 ? 8 : 4);
+    constexpr int R = D <= 4 ? 16 : (D <= 10 ? 8 : 4);
     return launch_hash_t<D, (WIDE ? (R / 2 > 0 ? R / 2 : 1) : R), WIDE>(a, smem, st);
 }
 
@@ -609,12 +671,17 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     a.nwords = (n + 31) / 32;
     a.magic = (uint32_t)(0xFFFFFFFFull / (uint64_t)M);
     const int64_t lat_bytes = W * 4;
-    const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4;
-    int64_t budget = (int64_t)kBitmapSmemBudget - zbytes;
-    SFFTB_REQUIRE(budget >= lat_bytes, "hash: one lattice bitmap exceeds shared memory");
-    a.Lc = (int)std::max<int64_t>(1, std::min<int64_t>(L, budget / lat_bytes));
-    if (L == 0) a.Lc = 1;
-    const size_t smem = (size_t)(zbytes + (int64_t)a.Lc * lat_bytes);
+    const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4 + 16;
+    const int64_t budget = (int64_t)kBitmapSmemBudget - zbytes;
+    SFFTB_REQUIRE(budget >= 2 * lat_bytes, "hash: one lattice bitmap exceeds shared memory");
+    if (L * lat_bytes <= budget) {  // every bitmap resident for the whole launch
+        a.Lc = (int)std::max<int64_t>(L, 1);
+        a.nbuf = 1;
+    } else {                        // two streaming buffers of Lc lattices each
+        a.Lc = (int)(budget / (2 * lat_bytes));
+        a.nbuf = 2;
+    }
+    const size_t smem = (size_t)(zbytes + (int64_t)a.nbuf * a.Lc * lat_bytes);
 
     // 32-bit path: u = offset + sum_j k_j zc_j stays in [0, 2^32)
     const int64_t zmax = M / 2;
@@ -635,6 +702,8 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
         a.offset = 0;
         return hash_dispatch<true>((int)d, a, smem, st);
     }
+    a.Lc = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(L, 1),
+                                                         budget / lat_bytes));
     const size_t smem_g = (size_t)((int64_t)a.Lc * lat_bytes);
     SFFTB_CUDA(cudaFuncSetAttribute(hash_rows_generic,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
