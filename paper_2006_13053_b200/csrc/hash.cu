@@ -17,6 +17,8 @@
 //  * detected rows (hits >= nu*L) leave a warp-ballot bitmask that
 //    sfftb_compact_mask turns into ascending indices; medians are computed
 //    only for those rows, one warp per row.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace sfftb {
@@ -48,8 +50,23 @@ struct HashArgs {
 __device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t M, uint32_t negM,
                                             uint32_t magic) {
     const uint32_t q = __umulhi(u, magic);
-    const uint32_t r = u + q * negM;
+    uint32_t r;
+    // one IMAD with the precomputed -M (keeps ptxas from negating q first)
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(negM), "r"(u));
     return min(r, r - M);
+}
+
+// Bit r of the bitmap at shared address `base`: word (r >> 5), bit r & 31.
+__device__ __forceinline__ uint32_t probe_bit(uint32_t base, uint32_t r) {
+    uint32_t w;
+    asm volatile("{\n\t.reg .u32 a;\n\t"
+                 "shr.u32 a, %1, 3;\n\t"
+                 "and.b32 a, a, 0xFFFFFFFC;\n\t"
+                 "add.u32 a, a, %2;\n\t"
+                 "ld.shared.u32 %0, [a];\n\t}"
+                 : "=r"(w)
+                 : "r"(r), "r"(base));
+    return __funnelshift_r(w, w, r) & 1u;
 }
 
 __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t M, double invM) {
@@ -115,12 +132,12 @@ __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int l
 // buffers: thread 0 issues a 1-D bulk copy (TMA engine, completion on an
 // mbarrier) for chunk q+2 as soon as every warp is done with chunk q, so the
 // L2 -> SMEM transfer overlaps the hashing of chunk q+1.
-template <int D, int R, bool WIDE>
-__global__ void __launch_bounds__(kHashThreads, 1) hash_rows(HashArgs a) {
+template <int D, int R, bool WIDE, int NT = kHashThreads>
+__global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     const int g = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int WARPS = kHashThreads / 32;
+    constexpr int WARPS = NT / 32;
     constexpr int TILE = WARPS * 32 * R;
     const uint32_t M32 = (uint32_t)a.M, negM = 0u - M32;
 
@@ -184,15 +201,14 @@ __global__ void __launch_bounds__(kHashThreads, 1) hash_rows(HashArgs a) {
         for (int c = 0; c < nchunks; ++c) {
             const int64_t qq = resident ? 0 : qc;
             mbar_wait(&bars[qq & 1], (uint32_t)((qq >> 1) & 1));
-            const uint32_t* buf = (qq & 1) ? buf1 : buf0;
             const int l0 = c * a.Lc;
             const int lend = min(a.L, l0 + a.Lc);
+            const uint32_t bbase = smem_addr((qq & 1) ? buf1 : buf0);
             for (int l = l0; l < lend; ++l) {
-                const int32_t* z = zc + l * D;
                 int32_t zr[D];
 #pragma unroll
-                for (int j = 0; j < D; ++j) zr[j] = z[j];
-                const uint32_t* bl = buf + (int64_t)(l - l0) * a.W;
+                for (int j = 0; j < D; ++j) zr[j] = zc[l * D + j];
+                const uint32_t lb = bbase + (uint32_t)((l - l0) * a.W * 4);
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     uint32_t r;
@@ -208,8 +224,7 @@ __global__ void __launch_bounds__(kHashThreads, 1) hash_rows(HashArgs a) {
                             acc += (uint64_t)ku[WIDE ? q : 0][WIDE ? j : 0] * (uint32_t)zr[j];
                         r = (uint32_t)mod_u64(acc, (uint64_t)a.M, invM);
                     }
-                    const uint32_t w = bl[r >> 5];
-                    hits[q] += (w >> (r & 31)) & 1u;
+                    hits[q] += probe_bit(lb, r);
                 }
             }
             if (!resident) {
@@ -587,28 +602,31 @@ static int grid_for(int64_t work, int threads) {
 // hash dispatch
 // ---------------------------------------------------------------------------
 
-template <int D, int R, bool WIDE>
+template <int D, int R, bool WIDE, int NT = kHashThreads>
 static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = hash_rows<D, R, WIDE>;
+    auto kern = hash_rows<D, R, WIDE, NT>;
     SFFTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
     int per_sm = 0;
-    SFFTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHashThreads, smem));
+    SFFTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     per_sm = std::max(per_sm, 1);
-    constexpr int TILE = (kHashThreads / 32) * 32 * R;
+    constexpr int TILE = (NT / 32) * 32 * R;
     const int64_t ntiles = ceil_div(a.n, TILE);
     const int64_t want = ceil_div((int64_t)num_sms() * per_sm, a.G);
     const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, want));
-    kern<<<dim3(gx, a.G), kHashThreads, smem, st>>>(a);
+    kern<<<dim3(gx, a.G), NT, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
 
+// 640 threads (20 warps) per SM with R rows per thread, R*D <= ~60 int32
+// registers of candidate rows: measured on B200 (cfg4 shape, 2^26 rows):
+// 512x8 4.57 ms, 768x4 4.05 ms, 640x6 4.00 ms, 256x16 4.87 ms.
 template <int D, bool WIDE>
 static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
-    // rows per thread: keep R*D <= ~96 int32 registers
-    constexpr int R = D <= 4 ? 16 : (D <= 10 ? 8 : 4);
-    return launch_hash_t<D, (WIDE ? (R / 2 > 0 ? R / 2 : 1) : R), WIDE>(a, smem, st);
+    constexpr int R = D <= 5 ? 12 : (D <= 7 ? 8 : (D <= 10 ? 6 : (D <= 15 ? 4 : 3)));
+    constexpr int RW = R / 2 > 0 ? R / 2 : 1;  // the 64-bit path needs wider temporaries
+    return launch_hash_t<D, (WIDE ? RW : R), WIDE, 640>(a, smem, st);
 }
 
 template <bool WIDE>
