@@ -36,6 +36,8 @@ struct BluesteinPlan {
     double2* bhat = nullptr;   // N (natural if N <= 8192, else [k2][k1] = B^[k2 + N2 k1])
     double2* tw_hi = nullptr;  // N/64 : e^{-2 pi i 64k/N}
     double2* tw_lo = nullptr;  // 64   : e^{-2 pi i k/N}
+    double2* tw_n1 = nullptr;  // N1   : e^{-2 pi i k/N1} (four-step only)
+    double2* tw_n2 = nullptr;  // N2   : e^{-2 pi i k/N2}
 };
 
 static std::mutex g_plan_mu;
@@ -100,6 +102,15 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
     const int N = p->N;
     const long double PI = 3.141592653589793238462643383279502884L;
     std::vector<double2> chirp(M), thi(N / 64), tlo(64), bh(N);
+    std::vector<double2> tn1(p->N1 ? p->N1 : 1), tn2(p->N2 ? p->N2 : 1);
+    for (int k = 0; k < p->N1; ++k) {
+        long double a = -2.0L * PI * k / p->N1;
+        tn1[k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    for (int k = 0; k < p->N2; ++k) {
+        long double a = -2.0L * PI * k / p->N2;
+        tn2[k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
     std::vector<long double> br(N, 0.0L), bi(N, 0.0L);
     for (int64_t j = 0; j < M; ++j) {
         const int64_t q = (int64_t)((__int128)j * j % (2 * M));  // exact j^2 mod 2M
@@ -137,11 +148,14 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
     };
     cudaError_t e;
     if ((e = up(&p->chirp, chirp)) != cudaSuccess || (e = up(&p->bhat, bh)) != cudaSuccess ||
-        (e = up(&p->tw_hi, thi)) != cudaSuccess || (e = up(&p->tw_lo, tlo)) != cudaSuccess) {
+        (e = up(&p->tw_hi, thi)) != cudaSuccess || (e = up(&p->tw_lo, tlo)) != cudaSuccess ||
+        (e = up(&p->tw_n1, tn1)) != cudaSuccess || (e = up(&p->tw_n2, tn2)) != cudaSuccess) {
         cudaFree(p->chirp);
         cudaFree(p->bhat);
         cudaFree(p->tw_hi);
         cudaFree(p->tw_lo);
+        cudaFree(p->tw_n1);
+        cudaFree(p->tw_n2);
         delete p;
         set_error(std::string("Bluestein plan upload: ") + cudaGetErrorString(e));
         return e == cudaErrorMemoryAllocation ? SFFTB_ENOMEM : SFFTB_ECUDA;
@@ -183,7 +197,10 @@ struct DftArgs {
     const double2* bhat;
     const double2* tw_hi;
     const double2* tw_lo;
+    const double2* tw_n1;
+    const double2* tw_n2;
     double2* work;  // four-step workspace, batch * N
+    int hi_in_smem;  // four-step: copy tw_hi into shared memory
 };
 
 template <bool C>
@@ -191,13 +208,23 @@ __device__ __forceinline__ double2 conj_if(double2 v) {
     return C ? make_double2(v.x, -v.y) : v;
 }
 
-// One CTA per transform; N/16 threads.
+// cooperative copy of n double2 into shared memory
+__device__ __forceinline__ void stage(double2* dst, const double2* __restrict__ src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+// One CTA per transform; N/16 threads.  Shared: data | tw_hi (N/64) | tw_lo (64).
 template <int N, bool INV>
 __global__ void __launch_bounds__(N / 16) bluestein_small(DftArgs a) {
     extern __shared__ double2 smem[];
+    constexpr int DATA = N + N / 16;
+    double2* hi = smem + DATA;
+    double2* lo = hi + N / 64;
     const int tid = threadIdx.x;
     constexpr int T = N / 16;
     const int64_t b = blockIdx.x;
+    stage(hi, a.tw_hi, N / 64);
+    stage(lo, a.tw_lo, 64);
     const double2* x = a.x + b * a.xs;
     for (int i = tid; i < N; i += T) {
         double2 v = make_double2(0.0, 0.0);
@@ -205,10 +232,11 @@ __global__ void __launch_bounds__(N / 16) bluestein_small(DftArgs a) {
         smem[pad16(i)] = v;
     }
     __syncthreads();
-    fft_smem<N, false>(smem, tid, a.tw_hi, a.tw_lo, 1);
+    const TwTwoLevel tw{hi, lo, 1};
+    fft_smem<N, false>(smem, tid, tw);
     for (int i = tid; i < N; i += T) smem[pad16(i)] = cmul(smem[pad16(i)], a.bhat[i]);
     __syncthreads();
-    fft_smem<N, true>(smem, tid, a.tw_hi, a.tw_lo, 1);
+    fft_smem<N, true>(smem, tid, tw);
     double2* y = a.y + b * a.ys;
     for (int h = tid; h < a.M; h += T) {
         double2 v = cmul(a.chirp[h], smem[pad16(h)]);
@@ -216,15 +244,34 @@ __global__ void __launch_bounds__(N / 16) bluestein_small(DftArgs a) {
     }
 }
 
+// four-step shared layout: F slots of SLOT (+1 pad slot: the column gathers
+// of F lanes then spread over all 16-byte bank groups) | sub-FFT table |
+// tw_lo (64) | tw_hi (N/64, when it fits)
+template <int LEN>
+struct FsLayout {
+    static constexpr int TPF = LEN / 16;
+    static constexpr int F = 256 / TPF;
+    static constexpr int SLOT = LEN + LEN / 16 + 1;
+    static constexpr int DATA = F * SLOT;
+};
+
 // colA: CTA = F columns n1 of the N1 x N2 view, length-N2 forward FFTs.
 template <int N2, bool INV>
-__global__ void __launch_bounds__(256) fs_colA(DftArgs a, int N1) {
-    constexpr int TPF = N2 / 16, F = 256 / TPF, SLOT = N2 + N2 / 16;
+__global__ void __launch_bounds__(256, 2) fs_colA(DftArgs a, int N1) {
+    using Lay = FsLayout<N2>;
+    constexpr int TPF = Lay::TPF, F = Lay::F, SLOT = Lay::SLOT;
     extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
+    double2* lo = tw2 + N2;
+    double2* hi_s = lo + 64;
     const int tid = threadIdx.x;
     const int64_t b = blockIdx.y;
     const int n1_0 = blockIdx.x * F;
     const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
     const double2* x = a.x + b * a.xs;
     for (int e = tid; e < F * N2; e += 256) {
         const int f = e % F, n2 = e / F;
@@ -235,27 +282,35 @@ __global__ void __launch_bounds__(256) fs_colA(DftArgs a, int N1) {
     }
     __syncthreads();
     const int f_me = tid / TPF;
-    fft_smem<N2, false>(smem + f_me * SLOT, tid % TPF, a.tw_hi, a.tw_lo, N1);
+    fft_smem<N2, false>(smem + f_me * SLOT, tid % TPF, TwDirect{tw2});
     double2* T = a.work + b * (int64_t)N;
     for (int e = tid; e < F * N2; e += 256) {
         const int f = e % F, k2 = e / F;
         const int n1 = n1_0 + f;
         double2 v = smem[f * SLOT + pad16(k2)];
         const int ex = n1 * k2;  // < N
-        if (ex) v = cmul(v, twiddle2<false>(a.tw_hi, a.tw_lo, ex));
+        if (ex) v = cmul(v, twiddle2<false>(hi, lo, ex));
         T[(int64_t)k2 * N1 + n1] = v;
     }
 }
 
 // rowB: CTA = F rows k2, forward FFT_N1 -> * B^ -> inverse FFT_N1 -> conj twiddle.
 template <int N1>
-__global__ void __launch_bounds__(256) fs_rowB(DftArgs a, int N2) {
-    constexpr int TPF = N1 / 16, F = 256 / TPF, SLOT = N1 + N1 / 16;
+__global__ void __launch_bounds__(256, 2) fs_rowB(DftArgs a, int N2) {
+    using Lay = FsLayout<N1>;
+    constexpr int TPF = Lay::TPF, F = Lay::F, SLOT = Lay::SLOT;
     extern __shared__ double2 smem[];
+    double2* tw1 = smem + Lay::DATA;
+    double2* lo = tw1 + N1;
+    double2* hi_s = lo + 64;
     const int tid = threadIdx.x;
     const int64_t b = blockIdx.y;
     const int k2_0 = blockIdx.x * F;
     const int N = N1 * N2;
+    stage(tw1, a.tw_n1, N1);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
     double2* T = a.work + b * (int64_t)N;
     for (int e = tid; e < F * N1; e += 256) {
         const int f = e / N1, n1 = e % N1;
@@ -264,33 +319,37 @@ __global__ void __launch_bounds__(256) fs_rowB(DftArgs a, int N2) {
     __syncthreads();
     const int f_me = tid / TPF;
     double2* mine = smem + f_me * SLOT;
-    fft_smem<N1, false>(mine, tid % TPF, a.tw_hi, a.tw_lo, N2);
+    const TwDirect tw{tw1};
+    fft_smem<N1, false>(mine, tid % TPF, tw);
     for (int e = tid; e < F * N1; e += 256) {
         const int f = e / N1, k1 = e % N1;
         smem[f * SLOT + pad16(k1)] =
             cmul(smem[f * SLOT + pad16(k1)], a.bhat[(int64_t)(k2_0 + f) * N1 + k1]);
     }
     __syncthreads();
-    fft_smem<N1, true>(mine, tid % TPF, a.tw_hi, a.tw_lo, N2);
+    fft_smem<N1, true>(mine, tid % TPF, tw);
     for (int e = tid; e < F * N1; e += 256) {
         const int f = e / N1, m1 = e % N1;
         const int k2 = k2_0 + f;
         double2 v = smem[f * SLOT + pad16(m1)];
         const int ex = m1 * k2;
-        if (ex) v = cmul(v, twiddle2<true>(a.tw_hi, a.tw_lo, ex));
+        if (ex) v = cmul(v, twiddle2<true>(hi, lo, ex));
         T[(int64_t)k2 * N1 + m1] = v;
     }
 }
 
 // colC: CTA = F columns m1, inverse length-N2 FFTs, chirp, scale, output.
 template <int N2, bool INV>
-__global__ void __launch_bounds__(256) fs_colC(DftArgs a, int N1) {
-    constexpr int TPF = N2 / 16, F = 256 / TPF, SLOT = N2 + N2 / 16;
+__global__ void __launch_bounds__(256, 2) fs_colC(DftArgs a, int N1) {
+    using Lay = FsLayout<N2>;
+    constexpr int TPF = Lay::TPF, F = Lay::F, SLOT = Lay::SLOT;
     extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
     const int tid = threadIdx.x;
     const int64_t b = blockIdx.y;
     const int m1_0 = blockIdx.x * F;
     const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
     const double2* T = a.work + b * (int64_t)N;
     for (int e = tid; e < F * N2; e += 256) {
         const int f = e % F, k2 = e / F;
@@ -298,7 +357,7 @@ __global__ void __launch_bounds__(256) fs_colC(DftArgs a, int N1) {
     }
     __syncthreads();
     const int f_me = tid / TPF;
-    fft_smem<N2, true>(smem + f_me * SLOT, tid % TPF, a.tw_hi, a.tw_lo, N1);
+    fft_smem<N2, true>(smem + f_me * SLOT, tid % TPF, TwDirect{tw2});
     double2* y = a.y + b * a.ys;
     for (int e = tid; e < F * N2; e += 256) {
         const int f = e % F, m2 = e / F;
@@ -322,7 +381,7 @@ static cudaError_t allow_smem(K kernel, size_t bytes) {
 
 template <int N, bool INV>
 static int launch_small(const DftArgs& a, int64_t batch, cudaStream_t st) {
-    const size_t sm = sizeof(double2) * (N + N / 16);
+    const size_t sm = sizeof(double2) * (N + N / 16 + N / 64 + 64);
     SFFTB_CUDA(allow_smem(bluestein_small<N, INV>, sm));
     bluestein_small<N, INV><<<(unsigned)batch, N / 16, sm, st>>>(a);
     SFFTB_CHECK_LAUNCH();
@@ -345,8 +404,10 @@ static int small_dispatch(int lg, const DftArgs& a, int64_t batch, cudaStream_t 
 
 template <int N2, bool INV>
 static int launch_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bool first) {
-    constexpr int F = 256 / (N2 / 16);
-    const size_t sm = sizeof(double2) * F * (N2 + N2 / 16);
+    using Lay = FsLayout<N2>;
+    constexpr int F = Lay::F;
+    const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
+    const size_t sm = sizeof(double2) * (Lay::DATA + N2 + (first ? 64 + hi : 0));
     dim3 grid(N1 / F, (unsigned)batch);
     if (first) {
         SFFTB_CUDA(allow_smem(fs_colA<N2, INV>, sm));
@@ -361,8 +422,10 @@ static int launch_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st,
 
 template <int N1>
 static int launch_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
-    constexpr int F = 256 / (N1 / 16);
-    const size_t sm = sizeof(double2) * F * (N1 + N1 / 16);
+    using Lay = FsLayout<N1>;
+    constexpr int F = Lay::F;
+    const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
+    const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
     SFFTB_CUDA(allow_smem(fs_rowB<N1>, sm));
     fs_rowB<N1><<<dim3(N2 / F, (unsigned)batch), 256, sm, st>>>(a, N2);
     SFFTB_CHECK_LAUNCH();
@@ -426,7 +489,10 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
     a.bhat = p->bhat;
     a.tw_hi = p->tw_hi;
     a.tw_lo = p->tw_lo;
+    a.tw_n1 = p->tw_n1;
+    a.tw_n2 = p->tw_n2;
     a.work = (double2*)ws;
+    a.hi_in_smem = p->N / 64 <= 2048;  // <= 32 KB of shared memory
     if (p->logN <= kSmallMaxLog)
         return inverse ? small_dispatch<true>(p->logN, a, batch, st)
                        : small_dispatch<false>(p->logN, a, batch, st);
@@ -450,6 +516,8 @@ extern "C" int sfftb_plan_cache_clear(void) {
         cudaFree(kv.second->bhat);
         cudaFree(kv.second->tw_hi);
         cudaFree(kv.second->tw_lo);
+        cudaFree(kv.second->tw_n1);
+        cudaFree(kv.second->tw_n2);
         cudaSetDevice(cur);
         delete kv.second;
     }

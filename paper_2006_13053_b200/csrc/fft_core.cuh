@@ -102,16 +102,36 @@ __host__ __device__ constexpr int pass_radix(int rem_log) {
     return rem_log >= 4 ? 16 : (1 << rem_log);
 }
 
-// One Stockham pass of radix R over FPC FFTs of length N (threads per FFT
-// TPF = N/16, each thread owns 16 elements = 16/R butterflies).
-// Twiddle exponent for butterfly j, output r: (j mod Ns) * r * (N/(Ns R)) in
-// units of e^{-2 pi i / N}; global exponent scale `tscale` maps it into the
-// table's NT (NT = N * tscale).
-template <int N, int R, bool INV>
+// Twiddle sources for a length-N sub-FFT:
+//  * TwDirect: shared-memory table tw[m] = e^{-2 pi i m/N}, m < N (one load)
+//  * TwTwoLevel: e^{-2 pi i e/NT} = hi[e >> 6] * lo[e & 63] (tables of the
+//    full transform length NT; e = m * (NT/N)) for lengths whose direct table
+//    would not fit next to the data.
+struct TwDirect {
+    const double2* tw;
+    template <bool INV>
+    __device__ __forceinline__ double2 get(int m) const {
+        double2 w = tw[m];
+        if (INV) w.y = -w.y;
+        return w;
+    }
+};
+struct TwTwoLevel {
+    const double2* hi;
+    const double2* lo;
+    int scale;
+    template <bool INV>
+    __device__ __forceinline__ double2 get(int m) const {
+        return twiddle2<INV>(hi, lo, m * scale);
+    }
+};
+
+// One Stockham pass of radix R over a length-N FFT held at buf (threads per
+// FFT TPF = N/16, each thread owns 16 elements = 16/R butterflies).  The
+// twiddle of butterfly j, output r is e^{-+2 pi i (j mod Ns) r / (Ns R)}.
+template <int N, int R, bool INV, class TW>
 __device__ __forceinline__ void stockham_pass(double2* __restrict__ buf, int tpf_id, int Ns,
-                                              const double2* __restrict__ tw_hi,
-                                              const double2* __restrict__ tw_lo,
-                                              int tscale) {
+                                              const TW& tw) {
     constexpr int TPF = N / 16;
     constexpr int BPT = 16 / R;  // butterflies per thread
     double2 v[BPT][R];
@@ -125,8 +145,8 @@ __device__ __forceinline__ void stockham_pass(double2* __restrict__ buf, int tpf
             const int step = jm * (N / (Ns * R));
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const int e = (step * r) % N;
-                if (e) v[q][r] = cmul(v[q][r], twiddle2<INV>(tw_hi, tw_lo, e * tscale));
+                const int m = (step * r) & (N - 1);
+                if (m) v[q][r] = cmul(v[q][r], tw.template get<INV>(m));
             }
         }
         dft_reg<R, INV>(v[q]);
@@ -142,25 +162,23 @@ __device__ __forceinline__ void stockham_pass(double2* __restrict__ buf, int tpf
     __syncthreads();
 }
 
-template <int N, int NS, int REM, bool INV>
+template <int N, int NS, int REM, bool INV, class TW>
 struct StockhamRun {
-    __device__ __forceinline__ static void run(double2* buf, int tpf_id, const double2* tw_hi,
-                                               const double2* tw_lo, int tscale) {
+    __device__ __forceinline__ static void run(double2* buf, int tpf_id, const TW& tw) {
         constexpr int R = pass_radix(REM);
-        stockham_pass<N, R, INV>(buf, tpf_id, NS, tw_hi, tw_lo, tscale);
-        StockhamRun<N, NS * R, REM - ilog2c(R), INV>::run(buf, tpf_id, tw_hi, tw_lo, tscale);
+        stockham_pass<N, R, INV, TW>(buf, tpf_id, NS, tw);
+        StockhamRun<N, NS * R, REM - ilog2c(R), INV, TW>::run(buf, tpf_id, tw);
     }
 };
-template <int N, int NS, bool INV>
-struct StockhamRun<N, NS, 0, INV> {
-    __device__ __forceinline__ static void run(double2*, int, const double2*, const double2*, int) {}
+template <int N, int NS, bool INV, class TW>
+struct StockhamRun<N, NS, 0, INV, TW> {
+    __device__ __forceinline__ static void run(double2*, int, const TW&) {}
 };
 
 // Full length-N FFT on buf (caller syncs before; ends synced).  N >= 16.
-template <int N, bool INV>
-__device__ __forceinline__ void fft_smem(double2* buf, int tpf_id, const double2* tw_hi,
-                                         const double2* tw_lo, int tscale) {
-    StockhamRun<N, 1, ilog2c(N), INV>::run(buf, tpf_id, tw_hi, tw_lo, tscale);
+template <int N, bool INV, class TW>
+__device__ __forceinline__ void fft_smem(double2* buf, int tpf_id, const TW& tw) {
+    StockhamRun<N, 1, ilog2c(N), INV, TW>::run(buf, tpf_id, tw);
 }
 
 }  // namespace sfftb
