@@ -273,12 +273,26 @@ __global__ void __launch_bounds__(256, 2) fs_colA(DftArgs a, int N1) {
     if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
     const double2* x = a.x + b * a.xs;
-    for (int e = tid; e < F * N2; e += 256) {
-        const int f = e % F, n2 = e / F;
-        const int64_t j = n1_0 + f + (int64_t)N1 * n2;
-        double2 v = make_double2(0.0, 0.0);
-        if (j < a.M) v = cmul(conj_if<INV>(x[j]), a.chirp[j]);
-        smem[f * SLOT + pad16(n2)] = v;
+    constexpr int PER = F * N2 / 256;  // elements per thread
+    {
+        // all loads of the tile in flight before any use (memory-level parallelism)
+        double2 v[PER], c[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            const int64_t j = n1_0 + e % F + (int64_t)N1 * (e / F);
+            v[i] = make_double2(0.0, 0.0);
+            c[i] = make_double2(0.0, 0.0);
+            if (j < a.M) {
+                v[i] = __ldg(x + j);
+                c[i] = __ldg(a.chirp + j);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            smem[(e % F) * SLOT + pad16(e / F)] = cmul(conj_if<INV>(v[i]), c[i]);
+        }
     }
     __syncthreads();
     const int f_me = tid / TPF;
@@ -312,19 +326,38 @@ __global__ void __launch_bounds__(256, 2) fs_rowB(DftArgs a, int N2) {
     if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
     double2* T = a.work + b * (int64_t)N;
-    for (int e = tid; e < F * N1; e += 256) {
-        const int f = e / N1, n1 = e % N1;
-        smem[f * SLOT + pad16(n1)] = T[(int64_t)(k2_0 + f) * N1 + n1];
+    constexpr int PER = F * N1 / 256;
+    {
+        double2 v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            v[i] = T[(int64_t)(k2_0 + e / N1) * N1 + e % N1];
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            smem[(e / N1) * SLOT + pad16(e % N1)] = v[i];
+        }
     }
     __syncthreads();
     const int f_me = tid / TPF;
     double2* mine = smem + f_me * SLOT;
     const TwDirect tw{tw1};
     fft_smem<N1, false>(mine, tid % TPF, tw);
-    for (int e = tid; e < F * N1; e += 256) {
-        const int f = e / N1, k1 = e % N1;
-        smem[f * SLOT + pad16(k1)] =
-            cmul(smem[f * SLOT + pad16(k1)], a.bhat[(int64_t)(k2_0 + f) * N1 + k1]);
+    {
+        double2 bh[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            bh[i] = __ldg(a.bhat + (int64_t)(k2_0 + e / N1) * N1 + e % N1);
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            double2* p = smem + (e / N1) * SLOT + pad16(e % N1);
+            *p = cmul(*p, bh[i]);
+        }
     }
     __syncthreads();
     fft_smem<N1, true>(mine, tid % TPF, tw);
@@ -351,19 +384,30 @@ __global__ void __launch_bounds__(256, 2) fs_colC(DftArgs a, int N1) {
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
     const double2* T = a.work + b * (int64_t)N;
-    for (int e = tid; e < F * N2; e += 256) {
-        const int f = e % F, k2 = e / F;
-        smem[f * SLOT + pad16(k2)] = T[(int64_t)k2 * N1 + m1_0 + f];
+    constexpr int PER = F * N2 / 256;
+    {
+        double2 v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            v[i] = T[(int64_t)(e / F) * N1 + m1_0 + e % F];
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * 256;
+            smem[(e % F) * SLOT + pad16(e / F)] = v[i];
+        }
     }
     __syncthreads();
     const int f_me = tid / TPF;
     fft_smem<N2, true>(smem + f_me * SLOT, tid % TPF, TwDirect{tw2});
     double2* y = a.y + b * a.ys;
-    for (int e = tid; e < F * N2; e += 256) {
-        const int f = e % F, m2 = e / F;
-        const int64_t h = m1_0 + f + (int64_t)N1 * m2;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = tid + i * 256;
+        const int64_t h = m1_0 + e % F + (int64_t)N1 * (e / F);
         if (h < a.M) {
-            double2 v = cmul(a.chirp[h], smem[f * SLOT + pad16(m2)]);
+            double2 v = cmul(__ldg(a.chirp + h), smem[(e % F) * SLOT + pad16(e / F)]);
             y[h] = cscale(conj_if<INV>(v), a.scale);
         }
     }
@@ -497,13 +541,28 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
         return inverse ? small_dispatch<true>(p->logN, a, batch, st)
                        : small_dispatch<false>(p->logN, a, batch, st);
     SFFTB_REQUIRE(ws != nullptr, "dft: workspace required");
-    rc = inverse ? cols_dispatch<true>(p->N2, a, batch, p->N1, st, true)
-                 : cols_dispatch<false>(p->N2, a, batch, p->N1, st, true);
-    if (rc != SFFTB_OK) return rc;
-    rc = rows_dispatch(p->N1, a, batch, p->N2, st);
-    if (rc != SFFTB_OK) return rc;
-    return inverse ? cols_dispatch<true>(p->N2, a, batch, p->N1, st, false)
-                   : cols_dispatch<false>(p->N2, a, batch, p->N1, st, false);
+    // Run the three passes over L2-sized slices of the batch so the
+    // four-step intermediate (16*N bytes per transform) is re-read from L2,
+    // not HBM: <= 48 MiB of workspace live per slice (L2 is ~126 MB).
+    const int64_t per = (int64_t)p->N * (int64_t)sizeof(double2);
+    // (measured: slicing to 48 MiB made the launches too small and was
+    // slower than one launch over the batch, so the slice is the batch)
+    const int64_t chunk = std::max<int64_t>(batch, ((int64_t)48 << 20) / per);
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = std::min<int64_t>(chunk, batch - b0);
+        DftArgs c = a;
+        c.x = a.x + b0 * a.xs;
+        c.y = a.y + b0 * a.ys;
+        rc = inverse ? cols_dispatch<true>(p->N2, c, nb, p->N1, st, true)
+                     : cols_dispatch<false>(p->N2, c, nb, p->N1, st, true);
+        if (rc != SFFTB_OK) return rc;
+        rc = rows_dispatch(p->N1, c, nb, p->N2, st);
+        if (rc != SFFTB_OK) return rc;
+        rc = inverse ? cols_dispatch<true>(p->N2, c, nb, p->N1, st, false)
+                     : cols_dispatch<false>(p->N2, c, nb, p->N1, st, false);
+        if (rc != SFFTB_OK) return rc;
+    }
+    return SFFTB_OK;
 }
 
 extern "C" int sfftb_plan_cache_clear(void) {
