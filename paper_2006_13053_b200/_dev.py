@@ -15,11 +15,14 @@ import torch
 from . import _native
 
 _CHECKED = False
+_SCOPE = None  # (device, stream handle) pinned by stream_scope()
 
 
 def device():
     """The CUDA device; raises if there is none (no CPU fallback exists)."""
     global _CHECKED
+    if _SCOPE is not None:
+        return _SCOPE[0]
     if not _CHECKED:
         if not torch.cuda.is_available():
             raise RuntimeError(
@@ -32,7 +35,27 @@ def device():
 
 def stream():
     """cudaStream_t of the current torch stream, as an int for ctypes."""
+    if _SCOPE is not None:
+        return _SCOPE[1]
     return torch.cuda.current_stream().cuda_stream
+
+
+class stream_scope:
+    """Pin the current device and stream for the duration of one API call
+    (saves a torch query per launch on the driver's hot loop)."""
+
+    def __enter__(self):
+        global _SCOPE
+        self._prev = _SCOPE
+        if _SCOPE is None:
+            dev = device()
+            _SCOPE = (dev, torch.cuda.current_stream(dev).cuda_stream)
+        return self
+
+    def __exit__(self, *exc):
+        global _SCOPE
+        _SCOPE = self._prev
+        return False
 
 
 def ptr(t):

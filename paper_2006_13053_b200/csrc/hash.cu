@@ -402,16 +402,20 @@ __global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords,
 
 __device__ __forceinline__ int64_t residue_exact(const int64_t* row, const int64_t* z, int d,
                                                  int64_t M) {
+    // sum_j (row_j mod M)(z_j mod M) < d (M-1)^2 < 2^62 (the caller's bound,
+    // detect.py:128-129), so one 64-bit accumulation and a final mod suffice
     uint64_t acc = 0;
     for (int j = 0; j < d; ++j) {
         int64_t e = row[j] % M;
         if (e < 0) e += M;
-        int64_t zz = z[j] % M;
-        if (zz < 0) zz += M;
-        acc = (acc + (uint64_t)(((unsigned __int128)e * (uint64_t)zz) % (uint64_t)M)) %
-              (uint64_t)M;
+        int64_t zz = z[j];
+        if (zz < 0 || zz >= M) {
+            zz %= M;
+            if (zz < 0) zz += M;
+        }
+        acc += (uint64_t)e * (uint64_t)zz;
     }
-    return (int64_t)acc;
+    return (int64_t)(acc % (uint64_t)M);
 }
 
 template <int S>
@@ -512,23 +516,44 @@ __global__ void sumsq_kernel(const double2* __restrict__ x, int64_t stride, int6
     if (threadIdx.x == 0) out[b] = red[0];
 }
 
+// One warp per group: lane l owns rms of lattices l, l+32, ...; the median
+// is found by stable ranking (L <= 256).
 __global__ void zero_threshold_kernel(const double* __restrict__ sumsq, int G, int L, int64_t M,
                                       double* __restrict__ theta) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (g >= G) return;
-    double v[256];
-    int n = 0;
-    for (int l = 0; l < L && l < 256; ++l) {
-        const double r = sqrt(sumsq[(int64_t)g * L + l] / (double)M);
-        int j = n++;
-        while (j > 0 && v[j - 1] > r) {
-            v[j] = v[j - 1];
-            --j;
-        }
-        v[j] = r;
+    double v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int l = lane + 32 * s;
+        v[s] = l < L ? sqrt(sumsq[(int64_t)g * L + l] / (double)M) : 0.0;
     }
-    const double mid = (n % 2 == 1) ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
-    theta[g] = fmax(1e-12, 1e-10 * mid);
+    const int lo = (L - 1) / 2, hi = L / 2;  // middle pair (equal when L is odd)
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int i = lane + 32 * s;
+        int rank = 0;
+        for (int so = 0; so < 8; ++so) {
+            if (32 * so >= L) break;
+            for (int src = 0; src < 32; ++src) {
+                const double o = __shfl_sync(0xffffffffu, v[so], src);
+                const int j = src + 32 * so;
+                rank += (j < L) && ((o < v[s]) || (o == v[s] && j < i));
+            }
+        }
+        if (i < L && rank == lo) a = v[s];
+        if (i < L && rank == hi) b = v[s];
+    }
+    for (int o = 16; o > 0; o >>= 1) {  // exactly one lane holds each value
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+        const double mid = (L % 2 == 1) ? a : 0.5 * (a + b);
+        theta[g] = fmax(1e-12, 1e-10 * mid);
+    }
 }
 
 __global__ void mark_kernel(const int64_t* __restrict__ idx, const int64_t* __restrict__ counts,
@@ -803,7 +828,7 @@ extern "C" int sfftb_sumsq(const double* x, int64_t stride, int64_t batch, int64
 extern "C" int sfftb_zero_thresholds(const double* sumsq, int64_t G, int64_t L, int64_t M,
                                      double* theta, void* stream) {
     SFFTB_REQUIRE(L >= 1 && L <= 256, "zero test: 1 <= L <= 256");
-    zero_threshold_kernel<<<(unsigned)ceil_div(G, 64), 64, 0, (cudaStream_t)stream>>>(
+    zero_threshold_kernel<<<(unsigned)ceil_div(G, 4), 128, 0, (cudaStream_t)stream>>>(
         sumsq, (int)G, (int)L, M, theta);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;

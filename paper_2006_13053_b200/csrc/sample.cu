@@ -114,41 +114,35 @@ __global__ void __launch_bounds__(kScatterThreads)
     }
 }
 
-// Thread per point; frequencies staged through shared memory in chunks.
-static constexpr int kEvalThreads = 128;
-static constexpr int kEvalChunk = 64;
+// One warp per point: lane q accumulates coefficients q, q+32, ... in order,
+// then a fixed shuffle tree adds the 32 partial sums (deterministic).
+static constexpr int kEvalThreads = 256;
 
 __global__ void __launch_bounds__(kEvalThreads)
     eval_dense_kernel(const int64_t* __restrict__ support, int64_t s, int d,
                       const double2* __restrict__ coeffs, const double* __restrict__ X, int64_t m,
                       double2* __restrict__ out) {
-    extern __shared__ double sh[];
-    double* ks = sh;                       // kEvalChunk * d
-    double2* cs = (double2*)(sh + kEvalChunk * d);  // kEvalChunk
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t p = blockIdx.x * (int64_t)(kEvalThreads / 32) + (threadIdx.x >> 5);
+    if (p >= m) return;
     double x[32];
-    const bool active = p < m;
-    for (int j = 0; j < d; ++j) x[j] = active ? X[p * d + j] : 0.0;
+    for (int j = 0; j < d; ++j) x[j] = X[p * d + j];
     double2 acc = make_double2(0.0, 0.0);
-    for (int64_t k0 = 0; k0 < s; k0 += kEvalChunk) {
-        const int cnt = (int)(s - k0 < kEvalChunk ? s - k0 : kEvalChunk);
-        __syncthreads();
-        for (int e = threadIdx.x; e < cnt * d; e += blockDim.x)
-            ks[e] = (double)support[k0 * d + e];
-        for (int e = threadIdx.x; e < cnt; e += blockDim.x) cs[e] = coeffs[k0 + e];
-        __syncthreads();
-        if (!active) continue;
-        for (int k = 0; k < cnt; ++k) {
-            double phi = 0.0;
-            for (int j = 0; j < d; ++j) phi = fma(ks[k * d + j], x[j], phi);
-            double sn, c;
-            sincospi(2.0 * phi, &sn, &c);
-            const double2 t = cmul(cs[k], make_double2(c, sn));
-            acc.x += t.x;
-            acc.y += t.y;
-        }
+    for (int64_t k = lane; k < s; k += 32) {
+        double phi = 0.0;
+        for (int j = 0; j < d; ++j) phi = fma((double)support[k * d + j], x[j], phi);
+        double sn, c;
+        sincospi(2.0 * phi, &sn, &c);
+        const double2 t = cmul(coeffs[k], make_double2(c, sn));
+        acc.x += t.x;
+        acc.y += t.y;
     }
-    if (active) out[p] = acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) out[p] = acc;
 }
 
 // Philox4x32-10
@@ -243,8 +237,7 @@ extern "C" int sfftb_eval_dense(const int64_t* support, int64_t s, int64_t d,
                                 void* stream) {
     SFFTB_REQUIRE(d >= 1 && d <= 32, "eval_dense: 1 <= d <= 32");
     if (m == 0) return SFFTB_OK;
-    const size_t sm = sizeof(double) * kEvalChunk * d + sizeof(double2) * kEvalChunk;
-    eval_dense_kernel<<<(unsigned)ceil_div(m, kEvalThreads), kEvalThreads, sm,
+    eval_dense_kernel<<<(unsigned)ceil_div(m, kEvalThreads / 32), kEvalThreads, 0,
                         (cudaStream_t)stream>>>(support, s, (int)d, (const double2*)coeffs, X, m,
                                                 (double2*)out);
     SFFTB_CHECK_LAUNCH();
