@@ -201,6 +201,7 @@ struct DftArgs {
     const double2* tw_n2;
     double2* work;  // four-step workspace, batch * N
     int hi_in_smem;  // four-step: copy tw_hi into shared memory
+    int64_t ntiles;  // four-step: tiles of the current kernel (persistent grid)
 };
 
 template <bool C>
@@ -265,15 +266,19 @@ __global__ void __launch_bounds__(256, 2) fs_colA(DftArgs a, int N1) {
     double2* lo = tw2 + N2;
     double2* hi_s = lo + 64;
     const int tid = threadIdx.x;
-    const int64_t b = blockIdx.y;
-    const int n1_0 = blockIdx.x * F;
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
     stage(lo, a.tw_lo, 64);
     if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
-    const double2* x = a.x + b * a.xs;
     constexpr int PER = F * N2 / 256;  // elements per thread
+    const int per_b = N1 / F;
+    // persistent: tables staged once, then tiles (transform b, columns n1_0..)
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int64_t b = tile / per_b;
+    const int n1_0 = (int)(tile % per_b) * F;
+    const double2* x = a.x + b * a.xs;
+    __syncthreads();
     {
         // all loads of the tile in flight before any use (memory-level parallelism)
         double2 v[PER], c[PER];
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(256, 2) fs_colA(DftArgs a, int N1) {
         if (ex) v = cmul(v, twiddle2<false>(hi, lo, ex));
         T[(int64_t)k2 * N1 + n1] = v;
     }
+    }
 }
 
 // rowB: CTA = F rows k2, forward FFT_N1 -> * B^ -> inverse FFT_N1 -> conj twiddle.
@@ -318,15 +324,18 @@ __global__ void __launch_bounds__(256, 2) fs_rowB(DftArgs a, int N2) {
     double2* lo = tw1 + N1;
     double2* hi_s = lo + 64;
     const int tid = threadIdx.x;
-    const int64_t b = blockIdx.y;
-    const int k2_0 = blockIdx.x * F;
     const int N = N1 * N2;
     stage(tw1, a.tw_n1, N1);
     stage(lo, a.tw_lo, 64);
     if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
-    double2* T = a.work + b * (int64_t)N;
     constexpr int PER = F * N1 / 256;
+    const int per_b = N2 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int64_t b = tile / per_b;
+    const int k2_0 = (int)(tile % per_b) * F;
+    double2* T = a.work + b * (int64_t)N;
+    __syncthreads();
     {
         double2 v[PER];
 #pragma unroll
@@ -369,6 +378,7 @@ __global__ void __launch_bounds__(256, 2) fs_rowB(DftArgs a, int N2) {
         if (ex) v = cmul(v, twiddle2<true>(hi, lo, ex));
         T[(int64_t)k2 * N1 + m1] = v;
     }
+    }
 }
 
 // colC: CTA = F columns m1, inverse length-N2 FFTs, chirp, scale, output.
@@ -379,12 +389,15 @@ __global__ void __launch_bounds__(256, 2) fs_colC(DftArgs a, int N1) {
     extern __shared__ double2 smem[];
     double2* tw2 = smem + Lay::DATA;
     const int tid = threadIdx.x;
-    const int64_t b = blockIdx.y;
-    const int m1_0 = blockIdx.x * F;
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
-    const double2* T = a.work + b * (int64_t)N;
     constexpr int PER = F * N2 / 256;
+    const int per_b = N1 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int64_t b = tile / per_b;
+    const int m1_0 = (int)(tile % per_b) * F;
+    const double2* T = a.work + b * (int64_t)N;
+    __syncthreads();
     {
         double2 v[PER];
 #pragma unroll
@@ -410,6 +423,7 @@ __global__ void __launch_bounds__(256, 2) fs_colC(DftArgs a, int N1) {
             double2 v = cmul(__ldg(a.chirp + h), smem[(e % F) * SLOT + pad16(e / F)]);
             y[h] = cscale(conj_if<INV>(v), a.scale);
         }
+    }
     }
 }
 
@@ -452,13 +466,15 @@ static int launch_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st,
     constexpr int F = Lay::F;
     const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
     const size_t sm = sizeof(double2) * (Lay::DATA + N2 + (first ? 64 + hi : 0));
-    dim3 grid(N1 / F, (unsigned)batch);
+    DftArgs c = a;
+    c.ntiles = (int64_t)(N1 / F) * batch;
+    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
     if (first) {
         SFFTB_CUDA(allow_smem(fs_colA<N2, INV>, sm));
-        fs_colA<N2, INV><<<grid, 256, sm, st>>>(a, N1);
+        fs_colA<N2, INV><<<grid, 256, sm, st>>>(c, N1);
     } else {
         SFFTB_CUDA(allow_smem(fs_colC<N2, INV>, sm));
-        fs_colC<N2, INV><<<grid, 256, sm, st>>>(a, N1);
+        fs_colC<N2, INV><<<grid, 256, sm, st>>>(c, N1);
     }
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
@@ -471,7 +487,10 @@ static int launch_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
     const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
     SFFTB_CUDA(allow_smem(fs_rowB<N1>, sm));
-    fs_rowB<N1><<<dim3(N2 / F, (unsigned)batch), 256, sm, st>>>(a, N2);
+    DftArgs c = a;
+    c.ntiles = (int64_t)(N2 / F) * batch;
+    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    fs_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
