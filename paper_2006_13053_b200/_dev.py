@@ -14,6 +14,9 @@ import torch
 
 from . import _native
 
+import os
+
+_PINNED_SMALL = os.environ.get("SFFTB_PINNED_SMALL", "1") == "1"
 _CHECKED = False
 _SCOPE = None  # (device, stream handle) pinned by stream_scope()
 
@@ -72,6 +75,12 @@ def upload(arr, dtype=None):
         if not t.is_pinned():
             t = t.pin_memory()
         return t.to(device(), non_blocking=True)
+    if _PINNED_SMALL:
+        # small arrays staged through torch's caching pinned-host allocator: the
+        # copy is stream-ordered and asynchronous (no host sync per upload)
+        staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        staged.copy_(t)
+        return staged.to(device(), non_blocking=True)
     return t.to(device())
 
 

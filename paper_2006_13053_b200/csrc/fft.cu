@@ -20,6 +20,7 @@
 //    Each kernel moves its CTA's tile once in and once out, coalesced in
 //    runs of F consecutive complex numbers.
 #include <math.h>
+#include <stdlib.h>
 
 #include <map>
 #include <mutex>
