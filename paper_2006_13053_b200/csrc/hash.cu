@@ -24,7 +24,8 @@
 namespace sfftb {
 
 static constexpr int kHashThreads = 512;
-static constexpr size_t kBitmapSmemBudget = 200 * 1024;
+static constexpr size_t kBitmapSmemBudget = 224 * 1024;
+static constexpr size_t kStreamSmemBudget = 160 * 1024;
 
 struct HashArgs {
     const int64_t* elems;
@@ -37,6 +38,7 @@ struct HashArgs {
     int64_t W;
     int Lc;              // lattices per shared-memory chunk
     int nbuf;            // 1 (all bitmaps resident) or 2 (double-buffered chunks)
+    int slot_words;      // power-of-two smem stride per lattice bitmap (>= W)
     uint32_t offset;     // multiple of M >= |residue sum| (32-bit path)
     uint32_t magic;      // floor((2^32-1)/M)
     int64_t min_hits;
@@ -54,6 +56,20 @@ __device__ __forceinline__ uint32_t mod_u32(uint32_t u, uint32_t M, uint32_t neg
     // one IMAD with the precomputed -M (keeps ptxas from negating q first)
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(negM), "r"(u));
     return min(r, r - M);
+}
+
+// Bit r of a bitmap whose shared address `slot` is aligned to a power of two
+// larger than its size: the word address is slot | ((r >> 3) & ~3), two ALU
+// ops (SHF + LOP3) and no IMAD-pipe add.
+__device__ __forceinline__ uint32_t probe_slot(uint32_t slot, uint32_t r) {
+    uint32_t w;
+    asm volatile("{\n\t.reg .u32 a;\n\t"
+                 "shr.u32 a, %1, 3;\n\t"
+                 "lop3.b32 a, a, 0xFFFFFFFC, %2, 0xEA;\n\t"
+                 "ld.shared.u32 %0, [a];\n\t}"
+                 : "=r"(w)
+                 : "r"(r), "r"(slot));
+    return __funnelshift_r(w, w, r) & 1u;
 }
 
 // Bit r of the bitmap at shared address `base`: word (r >> 5), bit r & 31.
@@ -132,7 +148,7 @@ __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int l
 // buffers: thread 0 issues a 1-D bulk copy (TMA engine, completion on an
 // mbarrier) for chunk q+2 as soon as every warp is done with chunk q, so the
 // L2 -> SMEM transfer overlaps the hashing of chunk q+1.
-template <int D, int R, bool WIDE, int NT = kHashThreads>
+template <int D, int R, bool WIDE, int NT = kHashThreads, bool SLOT = false>
 __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     const int g = blockIdx.y;
@@ -144,8 +160,12 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     int32_t* zc = reinterpret_cast<int32_t*>(smem_u32);
     const int zwords = ((a.L * D + 3) & ~3);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_u32 + zwords);
-    uint32_t* buf0 = smem_u32 + zwords + 4;
-    uint32_t* buf1 = buf0 + (int64_t)a.Lc * a.W;
+    // bitmap slots: one per lattice, stride slot_words (a power of two >= W),
+    // from the first shared address aligned to the stride
+    const uint32_t slot_bytes = (uint32_t)a.slot_words * 4u;
+    const uint32_t after = smem_addr(smem_u32 + zwords + 4);
+    const uint32_t slot0 = SLOT ? (after + slot_bytes - 1) & ~(slot_bytes - 1) : after;
+    const uint32_t slot1 = slot0 + (uint32_t)a.Lc * slot_bytes;
     for (int i = threadIdx.x; i < a.L * D; i += blockDim.x) {
         int64_t z = a.zmat[(int64_t)g * a.L * D + i] % a.M;
         if (z < 0) z += a.M;
@@ -168,10 +188,13 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
         const int c = resident ? 0 : (int)(qi % nchunks);
         const int l0 = c * a.Lc;
         const int cnt = min(a.L, l0 + a.Lc) - l0;
-        const uint32_t bytes = (uint32_t)(cnt * a.W * 4);
+        const uint32_t bytes = (uint32_t)(a.W * 4);
         uint64_t* bar = &bars[qi & 1];
-        mbar_arrive_expect_tx(bar, bytes);
-        bulk_g2s((qi & 1) ? buf1 : buf0, a.bits + ((int64_t)g * a.L + l0) * a.W, bytes, bar);
+        mbar_arrive_expect_tx(bar, bytes * (uint32_t)cnt);
+        const uint32_t dst0 = (qi & 1) ? slot1 : slot0;
+        for (int l = 0; l < cnt; ++l)
+            bulk_g2s_addr(dst0 + (uint32_t)l * slot_bytes,
+                          a.bits + ((int64_t)g * a.L + l0 + l) * a.W, bytes, bar);
     };
     if (threadIdx.x == 0) {
         if (total_q > 0) issue(0);
@@ -203,12 +226,12 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
             mbar_wait(&bars[qq & 1], (uint32_t)((qq >> 1) & 1));
             const int l0 = c * a.Lc;
             const int lend = min(a.L, l0 + a.Lc);
-            const uint32_t bbase = smem_addr((qq & 1) ? buf1 : buf0);
+            const uint32_t bbase = (qq & 1) ? slot1 : slot0;
             for (int l = l0; l < lend; ++l) {
                 int32_t zr[D];
 #pragma unroll
                 for (int j = 0; j < D; ++j) zr[j] = zc[l * D + j];
-                const uint32_t lb = bbase + (uint32_t)((l - l0) * a.W * 4);
+                const uint32_t lb = bbase + (uint32_t)(l - l0) * slot_bytes;
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     uint32_t r;
@@ -224,7 +247,7 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
                             acc += (uint64_t)ku[WIDE ? q : 0][WIDE ? j : 0] * (uint32_t)zr[j];
                         r = (uint32_t)mod_u64(acc, (uint64_t)a.M, invM);
                     }
-                    hits[q] += probe_bit(lb, r);
+                    hits[q] += SLOT ? probe_slot(lb, r) : probe_bit(lb, r);
                 }
             }
             if (!resident) {
@@ -627,9 +650,9 @@ static int grid_for(int64_t work, int threads) {
 // hash dispatch
 // ---------------------------------------------------------------------------
 
-template <int D, int R, bool WIDE, int NT = kHashThreads>
-static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = hash_rows<D, R, WIDE, NT>;
+template <int D, int R, bool WIDE, int NT, bool SLOT>
+static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
+    auto kern = hash_rows<D, R, WIDE, NT, SLOT>;
     SFFTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
     int per_sm = 0;
@@ -642,6 +665,13 @@ static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
     kern<<<dim3(gx, a.G), NT, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
+}
+
+template <int D, int R, bool WIDE, int NT = kHashThreads>
+static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
+    const bool pow2 = (a.slot_words & (a.slot_words - 1)) == 0;
+    return pow2 ? launch_hash_s<D, R, WIDE, NT, true>(a, smem, st)
+                : launch_hash_s<D, R, WIDE, NT, false>(a, smem, st);
 }
 
 // 640 threads (20 warps) per SM with R rows per thread, R*D <= ~60 int32
@@ -714,17 +744,34 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     a.nwords = (n + 31) / 32;
     a.magic = (uint32_t)(0xFFFFFFFFull / (uint64_t)M);
     const int64_t lat_bytes = W * 4;
+    int64_t pow2_words = 4;
+    while (pow2_words < W) pow2_words <<= 1;
     const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4 + 16;
-    const int64_t budget = (int64_t)kBitmapSmemBudget - zbytes;
-    SFFTB_REQUIRE(budget >= 2 * lat_bytes, "hash: one lattice bitmap exceeds shared memory");
-    if (L * lat_bytes <= budget) {  // every bitmap resident for the whole launch
+    int64_t slot_bytes, smem_i;
+    // (a) resident: power-of-two slots (OR addressing) when all L fit
+    const int64_t pow2_bytes = pow2_words * 4;
+    if (zbytes + pow2_bytes + L * pow2_bytes <= (int64_t)kBitmapSmemBudget) {
+        slot_bytes = pow2_bytes;
         a.Lc = (int)std::max<int64_t>(L, 1);
         a.nbuf = 1;
-    } else {                        // two streaming buffers of Lc lattices each
-        a.Lc = (int)(budget / (2 * lat_bytes));
+        smem_i = zbytes + slot_bytes + (int64_t)a.Lc * slot_bytes;
+    } else if (zbytes + L * lat_bytes <= (int64_t)kBitmapSmemBudget) {
+        slot_bytes = lat_bytes;  // (b) resident, dense
+        a.Lc = (int)std::max<int64_t>(L, 1);
+        a.nbuf = 1;
+        smem_i = zbytes + (int64_t)a.Lc * slot_bytes;
+    } else {
+        // (c) streamed, dense, in two buffers; leave L1 room for the row
+        // loads (measured: 160 KB of bitmaps beats 224 KB at cfg4)
+        slot_bytes = lat_bytes;
+        const int64_t budget = (int64_t)kStreamSmemBudget - zbytes;
+        SFFTB_REQUIRE(budget >= 2 * slot_bytes, "hash: one lattice bitmap exceeds shared memory");
+        a.Lc = (int)(budget / (2 * slot_bytes));
         a.nbuf = 2;
+        smem_i = zbytes + 2 * (int64_t)a.Lc * slot_bytes;
     }
-    const size_t smem = (size_t)(zbytes + (int64_t)a.nbuf * a.Lc * lat_bytes);
+    a.slot_words = (int)(slot_bytes / 4);
+    const size_t smem = (size_t)smem_i;
 
     // 32-bit path: u = offset + sum_j k_j zc_j stays in [0, 2^32)
     const int64_t zmax = M / 2;
@@ -745,8 +792,9 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
         a.offset = 0;
         return hash_dispatch<true>((int)d, a, smem, st);
     }
-    a.Lc = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(L, 1),
-                                                         budget / lat_bytes));
+    a.Lc = (int)std::max<int64_t>(
+        1, std::min<int64_t>(std::max<int64_t>(L, 1),
+                             ((int64_t)kBitmapSmemBudget - 16) / lat_bytes));
     const size_t smem_g = (size_t)((int64_t)a.Lc * lat_bytes);
     SFFTB_CUDA(cudaFuncSetAttribute(hash_rows_generic,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
