@@ -429,6 +429,139 @@ __global__ void __launch_bounds__(256, 2) fs_colC(DftArgs a, int N1) {
 }
 
 // ---------------------------------------------------------------------------
+// Register-pass four-step kernels for sub-FFT lengths 128 and 256 (the sfft
+// sizes N = 32768, 65536): global -> registers (pass 1) -> one smem
+// transpose -> registers (pass 2) -> global.  rowB keeps the forward
+// outputs in registers through the B^ product and the inverse pass 1.
+// ---------------------------------------------------------------------------
+
+// smem: F slots | sub-FFT table (LEN) | tw_lo (64) | tw_hi (N/64, optional)
+template <int LEN>
+struct Fs2Layout {
+    static constexpr int T = LEN / 16;
+    static constexpr int F = 256 / T;
+    static constexpr int SLOT = LEN + LEN / 16 + 1;
+    static constexpr int DATA = F * SLOT;
+};
+
+template <int N2, bool INV>
+__global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
+    using Lay = Fs2Layout<N2>;
+    constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
+    extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
+    double2* lo = tw2 + N2;
+    double2* hi_s = lo + 64;
+    const int tid = threadIdx.x;
+    const int f = tid % F, t = tid / F;  // columns fastest: coalesced rows
+    const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    double2* slot = smem + f * SLOT;
+    const int per_b = N1 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int n1 = (int)(tile % per_b) * F + f;
+        const double2* x = a.x + b * a.xs;
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int64_t j = n1 + (int64_t)N1 * (t + r * T);
+            v[r] = make_double2(0.0, 0.0);
+            if (j < a.M) v[r] = cmul(conj_if<INV>(__ldg(x + j)), __ldg(a.chirp + j));
+        }
+        __syncthreads();  // previous tile done with the slots
+        fft2pass<N2, false>(v, slot, t, tw2);
+        double2* Tw = a.work + b * (int64_t)N;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int k2 = fft2_out_index<N2>(t, e);
+            const int ex = n1 * k2;
+            double2 w = v[e];
+            if (ex) w = cmul(w, twiddle2<false>(hi, lo, ex));
+            Tw[(int64_t)k2 * N1 + n1] = w;
+        }
+    }
+}
+
+template <int N1>
+__global__ void __launch_bounds__(256, 2) fs2_rowB(DftArgs a, int N2) {
+    using Lay = Fs2Layout<N1>;
+    constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
+    extern __shared__ double2 smem[];
+    double2* tw1 = smem + Lay::DATA;
+    double2* lo = tw1 + N1;
+    double2* hi_s = lo + 64;
+    const int tid = threadIdx.x;
+    const int f = tid / T, t = tid % T;  // row elements fastest: coalesced
+    const int N = N1 * N2;
+    stage(tw1, a.tw_n1, N1);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    double2* slot = smem + f * SLOT;
+    const int per_b = N2 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int k2 = (int)(tile % per_b) * F + f;
+        double2* row = a.work + b * (int64_t)N + (int64_t)k2 * N1;
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = row[t + r * T];
+        __syncthreads();
+        fft2pass<N1, false>(v, slot, t, tw1);
+        const double2* bh = a.bhat + (int64_t)k2 * N1;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = cmul(v[e], __ldg(bh + fft2_out_index<N1>(t, e)));
+        fft2_out_to_in<N1>(v);
+        fft2pass<N1, true>(v, slot, t, tw1);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int m1 = fft2_out_index<N1>(t, e);
+            const int ex = m1 * k2;
+            double2 w = v[e];
+            if (ex) w = cmul(w, twiddle2<true>(hi, lo, ex));
+            row[m1] = w;
+        }
+    }
+}
+
+template <int N2, bool INV>
+__global__ void __launch_bounds__(256, 2) fs2_colC(DftArgs a, int N1) {
+    using Lay = Fs2Layout<N2>;
+    constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
+    extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
+    const int tid = threadIdx.x;
+    const int f = tid % F, t = tid / F;
+    const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
+    double2* slot = smem + f * SLOT;
+    const int per_b = N1 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int m1 = (int)(tile % per_b) * F + f;
+        const double2* Tw = a.work + b * (int64_t)N;
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = Tw[(int64_t)(t + r * T) * N1 + m1];
+        __syncthreads();
+        fft2pass<N2, true>(v, slot, t, tw2);
+        double2* y = a.y + b * a.ys;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int64_t h = m1 + (int64_t)N1 * fft2_out_index<N2>(t, e);
+            if (h < a.M) {
+                const double2 w = cmul(__ldg(a.chirp + h), v[e]);
+                y[h] = cscale(conj_if<INV>(w), a.scale);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 
@@ -520,6 +653,55 @@ static int rows_dispatch(int N1, const DftArgs& a, int64_t batch, int N2, cudaSt
     return SFFTB_EINVAL;
 }
 
+template <int N2, bool INV>
+static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bool first) {
+    using Lay = Fs2Layout<N2>;
+    const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
+    const size_t sm = sizeof(double2) * (Lay::DATA + N2 + (first ? 64 + hi : 0));
+    DftArgs c = a;
+    c.ntiles = (int64_t)(N1 / Lay::F) * batch;
+    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    if (first) {
+        SFFTB_CUDA(allow_smem(fs2_colA<N2, INV>, sm));
+        fs2_colA<N2, INV><<<grid, 256, sm, st>>>(c, N1);
+    } else {
+        SFFTB_CUDA(allow_smem(fs2_colC<N2, INV>, sm));
+        fs2_colC<N2, INV><<<grid, 256, sm, st>>>(c, N1);
+    }
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <int N1>
+static int fs2_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
+    using Lay = Fs2Layout<N1>;
+    const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
+    const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
+    DftArgs c = a;
+    c.ntiles = (int64_t)(N2 / Lay::F) * batch;
+    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    SFFTB_CUDA(allow_smem(fs2_rowB<N1>, sm));
+    fs2_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <bool INV>
+static int fs2_all(const BluesteinPlan* p, const DftArgs& a, int64_t batch, cudaStream_t st) {
+    int rc = p->N2 == 256 ? fs2_cols<256, INV>(a, batch, p->N1, st, true)
+                          : fs2_cols<128, INV>(a, batch, p->N1, st, true);
+    if (rc) return rc;
+    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    if (rc) return rc;
+    return p->N2 == 256 ? fs2_cols<256, INV>(a, batch, p->N1, st, false)
+                        : fs2_cols<128, INV>(a, batch, p->N1, st, false);
+}
+
+static int fs2_dispatch(const BluesteinPlan* p, const DftArgs& a, int64_t batch, bool inverse,
+                        cudaStream_t st) {
+    return inverse ? fs2_all<true>(p, a, batch, st) : fs2_all<false>(p, a, batch, st);
+}
+
 }  // namespace sfftb
 
 using namespace sfftb;
@@ -561,6 +743,8 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
         return inverse ? small_dispatch<true>(p->logN, a, batch, st)
                        : small_dispatch<false>(p->logN, a, batch, st);
     SFFTB_REQUIRE(ws != nullptr, "dft: workspace required");
+    if ((p->N1 == 128 || p->N1 == 256) && (p->N2 == 128 || p->N2 == 256))
+        return fs2_dispatch(p, a, batch, inverse != 0, st);
     // Run the three passes over L2-sized slices of the batch so the
     // four-step intermediate (16*N bytes per transform) is re-read from L2,
     // not HBM: <= 48 MiB of workspace live per slice (L2 is ~126 MB).

@@ -182,3 +182,75 @@ __device__ __forceinline__ void fft_smem(double2* buf, int tpf_id, const TW& tw)
 }
 
 }  // namespace sfftb
+
+namespace sfftb {
+
+// ---------------------------------------------------------------------------
+// Two-pass register FFT of length N = 16 * R2 (R2 in {8, 16}) by T = N/16
+// threads holding 16 elements each.  Pass 1 (radix 16) runs on the inputs
+// the thread loaded itself, one shared-memory transpose feeds pass 2
+// (radix R2), and the outputs stay in registers -- one smem round trip per
+// FFT instead of one per pass plus staging.
+//
+//   in : v[r]  = x[t + r*T],            r < 16
+//   out: v[e]  = X[fft2_out_index<N>(t, e)] = X[t + (e / R2) * T + 16 * (e % R2)]
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ int fft2_out_index(int t, int e) {
+    constexpr int R2 = N / 16, T = N / 16;
+    return t + (e / R2) * T + 16 * (e % R2);
+}
+
+// Reorder pass outputs (index fft2_out_index) into the next FFT's pass-1
+// input order (x[t + r*T]) -- the same set of indices, permuted.
+template <int N>
+__device__ __forceinline__ void fft2_out_to_in(double2 (&v)[16]) {
+    constexpr int R2 = N / 16, T = N / 16;
+    if constexpr (R2 == 16) {
+        return;  // k = t + 16 e == t + T e
+    } else {
+        // out e = q*R2 + r holds t + q*T + 16 r; input slot rr holds t + rr*T,
+        // so rr = q + r * (16 / T)
+        double2 w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int q = e / R2, r = e % R2;
+            w[q + r * (16 / T)] = v[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = w[e];
+    }
+}
+
+template <int N, bool INV>
+__device__ __forceinline__ void fft2pass(double2 (&v)[16], double2* __restrict__ slot, int t,
+                                         const double2* __restrict__ tw) {
+    constexpr int R2 = N / 16, T = N / 16, BPT = 16 / R2;
+    dft_reg<16, INV>(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) slot[pad16(t * 16 + r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int j = t + q * T;
+        double2 u[R2];
+#pragma unroll
+        for (int r = 0; r < R2; ++r) u[r] = slot[pad16(j + 16 * r)];
+        const int jm = j & 15;
+#pragma unroll
+        for (int r = 1; r < R2; ++r) {
+            const int m = jm * r;  // exponent of e^{-2 pi i / N}
+            if (m) {
+                double2 w = tw[m];
+                if (INV) w.y = -w.y;
+                u[r] = cmul(u[r], w);
+            }
+        }
+        dft_reg<R2, INV>(u);
+#pragma unroll
+        for (int r = 0; r < R2; ++r) v[q * R2 + r] = u[r];
+    }
+    __syncthreads();
+}
+
+}  // namespace sfftb
