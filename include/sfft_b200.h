@@ -102,6 +102,21 @@ int sfftb_dft(const double *x, int64_t x_stride, double *y, int64_t y_stride,
               int64_t batch, int64_t M, int inverse, double scale, void *ws,
               void *stream);
 
+/*
+ * Fused sampler -> detection transforms for G groups of L lattices (the
+ * dimension-incremental stage): samples = M*ifft(bins) (+ harness noise for
+ * oracle call call0 + row, sigma > 0), theta[g] = default zero test of the
+ * group's samples, ghat = fft(samples)/M, bits = |ghat| > theta[g].  The
+ * samples themselves stay on chip.  Only for Bluestein sizes whose four-step
+ * factors are 128/256 (M in [8192, 32768]); SFFTB_EINVAL otherwise (use the
+ * unfused sfftb_dft / sfftb_sumsq / sfftb_zero_thresholds / bitmap chain).
+ * ws: sfftb_sample_detect_workspace_bytes(G*L, M).
+ */
+int64_t sfftb_sample_detect_workspace_bytes(int64_t batch, int64_t M);
+int sfftb_sample_detect_dft(const double *bins, int64_t G, int64_t L, int64_t M,
+                            uint64_t seed, int64_t call0, double sigma, double *ghat,
+                            double *theta, uint32_t *bits, void *ws, void *stream);
+
 /* out[b] = sum_j |x[b, j]|^2 (for default_zero_test, detect.py:42-53). */
 int sfftb_sumsq(const double *x, int64_t stride, int64_t batch, int64_t M,
                 double *out, void *stream);

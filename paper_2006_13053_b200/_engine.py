@@ -56,14 +56,8 @@ def min_hits_for(nu, L):
     return int(math.ceil(nu * L))
 
 
-def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
-                 want_medians=True, want_hits=False):
-    """Run the full detection chain on device tensors.
-
-    samples (G*L, M) c128; zmat (G*L, d) i64; rows (n, d) i64 (any signs);
-    theta0: (G,) f64 tensor or None (default zero test per group).
-    """
-    n, d = int(rows.shape[0]), int(rows.shape[1])
+def spectra(samples, M, G, L, theta0=None):
+    """Zero test, DFT and nonzero bitmaps of (G*L, M) samples."""
     st = _dev.stream()
     if theta0 is None:
         theta0 = zero_thresholds(samples, G, L, M)
@@ -72,6 +66,32 @@ def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
     bits = _dev.empty((G * L * W,), torch.int32)
     _native.call("sfftb_nonzero_bitmap", _dev.ptr(ghat), G, L, M, _dev.ptr(theta0),
                  _dev.ptr(bits), st)
+    return ghat, theta0, bits
+
+
+def fused_ok(M):
+    """The fused sampler->detection transforms cover M with N1, N2 in {128, 256}."""
+    return 4097 <= M <= 32768
+
+
+def sample_spectra_fused(bins, M, G, L, noise_seed, call0, sigma):
+    """samples = M*ifft(bins) (+noise) kept on chip -> theta, ghat, bitmaps."""
+    W = int(_native.lib().sfftb_bitmap_words(M))
+    ghat = _dev.empty((G * L, M), torch.complex128)
+    theta = _dev.empty((G,), torch.float64)
+    bits = _dev.empty((G * L * W,), torch.int32)
+    ws = _dev.workspace(_native.lib().sfftb_sample_detect_workspace_bytes(G * L, M))
+    _native.call("sfftb_sample_detect_dft", _dev.ptr(bins), G, L, M,
+                 int(noise_seed) & 0xFFFFFFFFFFFFFFFF, int(call0), float(sigma),
+                 _dev.ptr(ghat), _dev.ptr(theta), _dev.ptr(bits), _dev.ptr(ws), _dev.stream())
+    return ghat, theta, bits
+
+
+def gather(ghat, theta0, bits, M, zmat, G, L, rows, kbound, nu, want_medians=True,
+           want_hits=False):
+    """Hash, hit counts, compaction and medians from the spectra."""
+    n, d = int(rows.shape[0]), int(rows.shape[1])
+    st = _dev.stream()
     nwords = (n + 31) // 32
     detmask = _dev.empty((G * max(nwords, 1),), torch.int32)
     hits = _dev.empty((G * n,), torch.int64) if want_hits else None
@@ -94,6 +114,17 @@ def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
                          _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(counts), n, _dev.ptr(coeffs),
                          st)
     return Batch(G, L, M, n, ghat, theta0, hits, idx, counts, coeffs)
+
+
+def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
+                 want_medians=True, want_hits=False):
+    """Run the full detection chain on device tensors.
+
+    samples (G*L, M) c128; zmat (G*L, d) i64; rows (n, d) i64 (any signs);
+    theta0: (G,) f64 tensor or None (default zero test per group).
+    """
+    ghat, theta0, bits = spectra(samples, M, G, L, theta0)
+    return gather(ghat, theta0, bits, M, zmat, G, L, rows, kbound, nu, want_medians, want_hits)
 
 
 def topk(idx, coeffs, counts, G, cap, theta, s_tilde):

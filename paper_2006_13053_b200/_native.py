@@ -39,6 +39,9 @@ _SIGS = {
     "sfftb_dft_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_dft": (_int, [_p, _i64, _p, _i64, _i64, _i64, _int, _dbl, _p, _p]),
     "sfftb_sumsq": (_int, [_p, _i64, _i64, _i64, _p, _p]),
+    "sfftb_sample_detect_workspace_bytes": (_i64, [_i64, _i64]),
+    "sfftb_sample_detect_dft": (_int, [_p, _i64, _i64, _i64, _u64, _i64, _dbl, _p, _p, _p, _p,
+                                       _p]),
     "sfftb_zero_thresholds": (_int, [_p, _i64, _i64, _i64, _p, _p]),
     "sfftb_bitmap_words": (_i64, [_i64]),
     "sfftb_nonzero_bitmap": (_int, [_p, _i64, _i64, _i64, _p, _p, _p]),

@@ -88,6 +88,43 @@ __device__ __forceinline__ int64_t mod_floor(int64_t a, int64_t M) {
 
 }  // namespace sfftb
 
+// ---- harness noise: Philox4x32-10 + 53-bit Box-Muller (oracle/port.py:
+// noise_for_call restates it) ----
+namespace sfftb {
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        if (r < 9) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+    }
+}
+
+// sigma * (N(0,1) + i N(0,1)) for sample m of oracle call `call`
+__device__ __forceinline__ double2 harness_noise(uint64_t seed, uint64_t call, int64_t m,
+                                                 double sigma) {
+    uint32_t c[4] = {(uint32_t)m, (uint32_t)((uint64_t)m >> 32), (uint32_t)call,
+                     (uint32_t)(call >> 32)};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t ua = ((uint64_t)(c[0] >> 5) << 26) + (c[1] >> 6);
+    const uint64_t ub = ((uint64_t)(c[2] >> 5) << 26) + (c[3] >> 6);
+    const double u1 = ((double)ua + 1.0) * 0x1.0p-53;
+    const double u2 = (double)ub * 0x1.0p-53;
+    const double rad = sigma * sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincospi(2.0 * u2, &sn, &cs);
+    return make_double2(rad * cs, rad * sn);
+}
+}  // namespace sfftb
+
 // ---- mbarrier + 1-D bulk copy (TMA engine) helpers, sm_90+/sm_100a ----
 namespace sfftb {
 

@@ -203,6 +203,15 @@ struct DftArgs {
     double2* work;  // four-step workspace, batch * N
     int hi_in_smem;  // four-step: copy tw_hi into shared memory
     int64_t ntiles;  // four-step: tiles of the current kernel (persistent grid)
+    // fused sampler -> detection path (sfftb_sample_detect_dft)
+    double* sumsq_part;     // [batch][N1/F] partial sums of |sample|^2
+    uint64_t noise_seed;
+    int64_t noise_call0;
+    double noise_sigma;
+    const double* theta;    // [batch / L] zero-test thresholds
+    int L;
+    uint32_t* bits;         // [batch][W] nonzero bitmaps
+    int64_t W;
 };
 
 template <bool C>
@@ -562,6 +571,148 @@ __global__ void __launch_bounds__(256, 2) fs2_colC(DftArgs a, int N1) {
 }
 
 // ---------------------------------------------------------------------------
+// Fused sampler -> detection chain for the register-pass sizes.
+//
+// colCA = (sampler inverse colC) + (detection forward colA) on the same
+// column tile: inverse column FFT -> samples y = conj(w c) (+ harness noise)
+// -> per-tile sum |y|^2 for the zero test -> x = y w -> forward column FFT ->
+// four-step twiddle.  Samples never reach HBM.  colC_bits = detection colC
+// that also emits the nonzero bitmap (|ghat| > theta, _core.pyx:195).
+// ---------------------------------------------------------------------------
+template <int N2>
+__global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
+    using Lay = Fs2Layout<N2>;
+    constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
+    extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
+    double2* lo = tw2 + N2;
+    double2* hi_s = lo + 64;
+    __shared__ double red[8];
+    const int tid = threadIdx.x;
+    const int f = tid % F, t = tid / F;
+    const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    double2* slot = smem + f * SLOT;
+    const int per_b = N1 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int m1 = (int)(tile % per_b) * F + f;
+        double2* Tw = a.work + b * (int64_t)N;
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = Tw[(int64_t)(t + r * T) * N1 + m1];
+        __syncthreads();
+        fft2pass<N2, true>(v, slot, t, tw2);
+        double ss = 0.0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int64_t h = m1 + (int64_t)N1 * fft2_out_index<N2>(t, e);
+            double2 x = make_double2(0.0, 0.0);
+            if (h < a.M) {
+                const double2 w = __ldg(a.chirp + h);
+                double2 y = cmul(w, v[e]);
+                y.y = -y.y;  // sample: conj(w c), the M*ifft of the bins
+                if (a.noise_sigma > 0.0) {
+                    const double2 nz = harness_noise(a.noise_seed,
+                                                     (uint64_t)(a.noise_call0 + b), h,
+                                                     a.noise_sigma);
+                    y.x += nz.x;
+                    y.y += nz.y;
+                }
+                ss = fma(y.x, y.x, fma(y.y, y.y, ss));
+                x = cmul(y, w);  // detection chirp
+            }
+            v[e] = x;
+        }
+        // per-tile sum of |y|^2 in a fixed order (deterministic zero test)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+        if ((tid & 31) == 0) red[tid >> 5] = ss;
+        fft2_out_to_in<N2>(v);
+        fft2pass<N2, false>(v, slot, t, tw2);  // (its syncs also publish red[])
+        if (tid == 0) {
+            double s8 = 0.0;
+            for (int w8 = 0; w8 < 8; ++w8) s8 += red[w8];
+            a.sumsq_part[b * per_b + tile % per_b] = s8;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int k2 = fft2_out_index<N2>(t, e);
+            const int ex = m1 * k2;
+            double2 w = v[e];
+            if (ex) w = cmul(w, twiddle2<false>(hi, lo, ex));
+            Tw[(int64_t)k2 * N1 + m1] = w;
+        }
+    }
+}
+
+template <int N2>
+__global__ void __launch_bounds__(256, 2) fs2_colC_bits(DftArgs a, int N1) {
+    using Lay = Fs2Layout<N2>;
+    constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
+    static_assert(F == 16 || F == 32, "bit groups of F consecutive bins");
+    extern __shared__ double2 smem[];
+    double2* tw2 = smem + Lay::DATA;
+    const int tid = threadIdx.x;
+    const int f = tid % F, t = tid / F;
+    const int lane = tid & 31;
+    const int N = N1 * N2;
+    stage(tw2, a.tw_n2, N2);
+    double2* slot = smem + f * SLOT;
+    const int per_b = N1 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int m1_0 = (int)(tile % per_b) * F;
+        const int m1 = m1_0 + f;
+        const double th = a.theta[b / a.L];
+        const double2* Tw = a.work + b * (int64_t)N;
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = Tw[(int64_t)(t + r * T) * N1 + m1];
+        __syncthreads();
+        fft2pass<N2, true>(v, slot, t, tw2);
+        double2* y = a.y + b * a.ys;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int64_t m2 = fft2_out_index<N2>(t, e);
+            const int64_t h = m1 + (int64_t)N1 * m2;
+            bool nz = false;
+            if (h < a.M) {
+                const double2 g = cscale(cmul(__ldg(a.chirp + h), v[e]), a.scale);
+                y[h] = g;
+                nz = nonzero_test(g.x, g.y, th);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, nz);
+            // lanes hold F consecutive bins of 32/F rows m2: bins m1_0 + N1*m2
+            // start on an F-aligned bit, so each F-bit group is one store
+            if (F == 32) {
+                if (lane == 0 && (m1_0 + (int64_t)N1 * m2) < a.M)
+                    a.bits[b * a.W + ((m1_0 + (int64_t)N1 * m2) >> 5)] = bal;
+            } else if (f == 0) {
+                const int64_t h0 = m1_0 + (int64_t)N1 * m2;
+                if (h0 < a.M) {
+                    uint16_t* b16 = reinterpret_cast<uint16_t*>(a.bits + b * a.W);
+                    b16[h0 >> 4] = (uint16_t)(bal >> (lane & 16));
+                }
+            }
+        }
+    }
+}
+
+__global__ void partial_sumsq_reduce(const double* __restrict__ part, int64_t rows, int per_b,
+                                     double* __restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < per_b; ++k) s += part[r * per_b + k];
+        out[r] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 
@@ -765,6 +916,109 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
         rc = inverse ? cols_dispatch<true>(p->N2, c, nb, p->N1, st, false)
                      : cols_dispatch<false>(p->N2, c, nb, p->N1, st, false);
         if (rc != SFFTB_OK) return rc;
+    }
+    return SFFTB_OK;
+}
+
+extern "C" int64_t sfftb_sample_detect_workspace_bytes(int64_t batch, int64_t M) {
+    if (batch <= 0 || M <= 0) return 0;
+    const int lg = bluestein_log(M);
+    if (lg <= kSmallMaxLog) return 0;
+    const int64_t N = int64_t(1) << lg;
+    return batch * N * (int64_t)sizeof(double2) + batch * 64 * (int64_t)sizeof(double) +
+           batch * (int64_t)sizeof(double);
+}
+
+extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L, int64_t M,
+                                       uint64_t seed, int64_t call0, double sigma,
+                                       double* ghat, double* theta, uint32_t* bits,
+                                       void* ws, void* stream) {
+    SFFTB_REQUIRE(G >= 1 && L >= 1 && M >= 1, "sample_detect: bad sizes");
+    BluesteinPlan* p = nullptr;
+    int rc = get_plan(M, &p);
+    if (rc != SFFTB_OK) return rc;
+    if (!((p->N1 == 128 || p->N1 == 256) && (p->N2 == 128 || p->N2 == 256))) {
+        set_error("sample_detect: fused path needs N1, N2 in {128, 256}");
+        return SFFTB_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t batch = G * L;
+    SFFTB_REQUIRE(batch <= 65535, "sample_detect: batch too large");
+    const int64_t N = p->N;
+    DftArgs a;
+    a.x = (const double2*)bins;
+    a.xs = M;
+    a.y = (double2*)ghat;
+    a.ys = M;
+    a.M = M;
+    a.chirp = p->chirp;
+    a.bhat = p->bhat;
+    a.tw_hi = p->tw_hi;
+    a.tw_lo = p->tw_lo;
+    a.tw_n1 = p->tw_n1;
+    a.tw_n2 = p->tw_n2;
+    a.work = (double2*)ws;
+    a.hi_in_smem = p->N / 64 <= 2048;
+    a.sumsq_part = (double*)((char*)ws + batch * N * sizeof(double2));
+    double* sumsq = a.sumsq_part + batch * 64;
+    a.noise_seed = seed;
+    a.noise_call0 = call0;
+    a.noise_sigma = sigma;
+    a.theta = theta;
+    a.L = (int)L;
+    a.bits = bits;
+    a.W = sfftb_bitmap_words(M);
+    // sampler: inverse DFT (scale 1) -- colA (conj input) and rowB
+    a.scale = 1.0;
+    rc = p->N2 == 256 ? fs2_cols<256, true>(a, batch, p->N1, st, true)
+                      : fs2_cols<128, true>(a, batch, p->N1, st, true);
+    if (rc) return rc;
+    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    if (rc) return rc;
+    // fused colC(sampler) + colA(detection)
+    {
+        const int F = p->N2 == 256 ? Fs2Layout<256>::F : Fs2Layout<128>::F;
+        DftArgs c = a;
+        c.ntiles = (int64_t)(p->N1 / F) * batch;
+        const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+        const size_t hi = a.hi_in_smem ? (size_t)(N / 64) : 0;
+        if (p->N2 == 256) {
+            const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256 + 64 + hi);
+            SFFTB_CUDA(allow_smem(fs2_colCA<256>, sm));
+            fs2_colCA<256><<<grid, 256, sm, st>>>(c, p->N1);
+        } else {
+            const size_t sm = sizeof(double2) * (Fs2Layout<128>::DATA + 128 + 64 + hi);
+            SFFTB_CUDA(allow_smem(fs2_colCA<128>, sm));
+            fs2_colCA<128><<<grid, 256, sm, st>>>(c, p->N1);
+        }
+        SFFTB_CHECK_LAUNCH();
+        const int per_b = p->N1 / F;
+        partial_sumsq_reduce<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(a.sumsq_part, batch,
+                                                                             per_b, sumsq);
+        SFFTB_CHECK_LAUNCH();
+    }
+    rc = sfftb_zero_thresholds(sumsq, G, L, M, theta, st);
+    if (rc) return rc;
+    // detection: rowB, then colC emitting ghat (scale 1/M) and the bitmap
+    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    if (rc) return rc;
+    SFFTB_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * batch * a.W, st));
+    {
+        DftArgs c = a;
+        c.scale = 1.0 / (double)M;
+        const int F = p->N2 == 256 ? Fs2Layout<256>::F : Fs2Layout<128>::F;
+        c.ntiles = (int64_t)(p->N1 / F) * batch;
+        const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+        if (p->N2 == 256) {
+            const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256);
+            SFFTB_CUDA(allow_smem(fs2_colC_bits<256>, sm));
+            fs2_colC_bits<256><<<grid, 256, sm, st>>>(c, p->N1);
+        } else {
+            const size_t sm = sizeof(double2) * (Fs2Layout<128>::DATA + 128);
+            SFFTB_CUDA(allow_smem(fs2_colC_bits<128>, sm));
+            fs2_colC_bits<128><<<grid, 256, sm, st>>>(c, p->N1);
+        }
+        SFFTB_CHECK_LAUNCH();
     }
     return SFFTB_OK;
 }

@@ -145,44 +145,16 @@ __global__ void __launch_bounds__(kEvalThreads)
     if (lane == 0) out[p] = acc;
 }
 
-// Philox4x32-10
-__device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
-        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-        c[0] = n0;
-        c[1] = lo1;
-        c[2] = n2;
-        c[3] = lo0;
-        if (r < 9) {
-            k0 += 0x9E3779B9u;
-            k1 += 0xBB67AE85u;
-        }
-    }
-}
-
 __global__ void noise_kernel(double2* __restrict__ x, int64_t rows, int64_t M, uint64_t seed,
                              int64_t call0, double sigma) {
     const int64_t total = rows * M;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = e / M, m = e % M;
-        const uint64_t call = (uint64_t)(call0 + row);
-        uint32_t c[4] = {(uint32_t)m, (uint32_t)((uint64_t)m >> 32), (uint32_t)call,
-                         (uint32_t)(call >> 32)};
-        philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
-        const uint64_t ua = ((uint64_t)(c[0] >> 5) << 26) + (c[1] >> 6);
-        const uint64_t ub = ((uint64_t)(c[2] >> 5) << 26) + (c[3] >> 6);
-        const double u1 = ((double)ua + 1.0) * 0x1.0p-53;
-        const double u2 = (double)ub * 0x1.0p-53;
-        const double rad = sigma * sqrt(-2.0 * log(u1));
-        double sn, cs;
-        sincospi(2.0 * u2, &sn, &cs);
+        const double2 nz = harness_noise(seed, (uint64_t)(call0 + row), m, sigma);
         double2 v = x[e];
-        v.x += rad * cs;
-        v.y += rad * sn;
+        v.x += nz.x;
+        v.y += nz.y;
         x[e] = v;
     }
 }

@@ -98,6 +98,20 @@ def evaluate_many(p, X):
     return _dev.download(_eval_points_dev(p, _dev.upload(X)))
 
 
+def lattice_bins_device(p, zmat_dev, M, tails_dev, G, L, t_dim):
+    """Residue bins B (G*L, M) of the anchored coefficients (polyeval.py:85-86)."""
+    sup, c = p.device()
+    s = len(p)
+    anchored = _dev.empty((G, max(s, 1)), torch.complex128)
+    if s:
+        _native.call("sfftb_anchor_coeffs", _dev.ptr(sup), s, p.dim, t_dim, _dev.ptr(c),
+                     _dev.ptr(tails_dev), G, _dev.ptr(anchored), _dev.stream())
+    bins = _dev.empty((G * L, M), torch.complex128)
+    _native.call("sfftb_scatter_bins", _dev.ptr(sup), s, p.dim, t_dim, _dev.ptr(anchored),
+                 _dev.ptr(zmat_dev), G, L, M, _dev.ptr(bins), None, _dev.stream())
+    return bins
+
+
 def sample_lattices_device(p, zmat_dev, M, tails_dev, G, L, t_dim):
     """Structured samples of G*L lattices (G tails, L generators each).
 
@@ -201,6 +215,21 @@ class PolyOracle(SamplingOracle):
         vals = sample_lattices_device(self.poly, z, lat.M, tails, 1, 1, self.dim)
         self.add_noise_device(vals, 1, lat.M)
         return _dev.download(vals[0])
+
+    def sample_spectra_device(self, zmat_dev, M, tails_dev, G, L, t_dim):
+        """Fused sampling + detection transforms (samples stay on chip):
+        returns (ghat, theta0 per group, bitmaps) or None when M is outside
+        the fused path.  Counts and calls advance as G*L sample_many calls."""
+        from . import _engine
+
+        if not _engine.fused_ok(M):
+            return None
+        bins = lattice_bins_device(self.poly, zmat_dev, M, tails_dev, G, L, t_dim)
+        out = _engine.sample_spectra_fused(bins, M, G, L, self.noise_seed, self.calls,
+                                           self.noise_sigma)
+        self.calls += G * L
+        self.count += G * L * M
+        return out
 
     def sample_lattices_device(self, zmat_dev, M, tails_dev, G, L, t_dim):
         """Batched fixed-tail lattice sampling; advances count and calls

@@ -193,3 +193,32 @@ def test_noise_stream_matches_oracle(cuda, oracle_lib):
         want = oracle_lib.noise_for_call(seed, call0 + r, M, sigma)
         assert np.max(np.abs(got[r] - want)) < 1e-17
     assert abs(np.std(got.real) - sigma) < 0.05 * sigma
+
+
+@pytest.mark.parametrize("M,G,L,sigma", [(20663, 2, 5, 0.0), (10331, 3, 3, 1e-3), (4099, 1, 7, 0.0)])
+def test_fused_sample_detect_matches_unfused(cuda, M, G, L, sigma):
+    """sfftb_sample_detect_dft (samples kept on chip) == inverse DFT + noise +
+    zero test + forward DFT + bitmap run as separate kernels."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine, _native
+    from paper_2006_13053_b200.dft import dft_batch
+
+    rng = np.random.default_rng(M + G)
+    bins = np.zeros((G * L, M), dtype=np.complex128)
+    for row in bins:  # sparse bins: clear zero / nonzero margins
+        nz = rng.choice(M, size=300, replace=False)
+        row[nz] = rng.normal(size=300) + 1j * rng.normal(size=300)
+    b = _dev.upload(bins)
+    seed, call0 = 77, 5
+    ghat_f, theta_f, bits_f = _engine.sample_spectra_fused(b, M, G, L, seed, call0, sigma)
+    samples = dft_batch(b, M, inverse=True, scale=1.0)
+    if sigma > 0:
+        _native.call("sfftb_add_noise", _dev.ptr(samples), G * L, M, seed, call0, sigma,
+                     _dev.stream())
+    ghat_u, theta_u, bits_u = _engine.spectra(samples, M, G, L)
+    assert np.allclose(_dev.download(theta_f), _dev.download(theta_u), rtol=1e-12, atol=0)
+    assert np.max(np.abs(_dev.download(ghat_f) - _dev.download(ghat_u))) < 1e-13
+    assert np.array_equal(_dev.download(bits_f), _dev.download(bits_u))
+    if sigma == 0:
+        assert np.max(np.abs(_dev.download(ghat_f) - bins)) < 1e-12

@@ -89,3 +89,26 @@ def test_seed_reproducibility_bitwise(cuda):
     assert runs[0].support == runs[1].support
     assert np.array_equal(runs[0].coeffs, runs[1].coeffs)
     assert runs[0].sample_count == runs[1].sample_count
+
+
+@pytest.mark.parametrize("sigma", [0.0, 1e-3])
+def test_sfft_fused_path_vs_oracle(cuda, oracle_lib, sigma):
+    """A stage size on the fused sampler->detection path (M = 9311) against
+    the oracle's structured sfft with the same harness noise."""
+    pkg = cuda
+    w = workloads.small_sfft(31, 4, 8, 450, r=1, sigma=sigma, decaying=sigma > 0,
+                             theta=1e-6 if sigma else 1e-12)
+    p = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+    orc = pkg.oracle_from_poly(p, noise_sigma=w.sigma, noise_seed=w.noise_seed)
+    res = pkg.sfft(orc, pkg.Box(w.d, w.lo, w.hi),
+                   pkg.SfftParams(w.s, 0.9, theta=w.theta, r=w.r), seed=w.seed)
+    ref = oracle_lib.sfft(oracle_lib.PolyOracle(w.support, w.coeffs, mode="structured",
+                                                sigma=w.sigma, noise_seed=w.noise_seed),
+                          oracle_lib.Box(w.d, w.lo, w.hi), w.s, 0.9, w.seed, theta=w.theta,
+                          r=w.r)
+    assert any(e["samples"] % 9311 == 0 for e in res.stage_log)  # fused size exercised
+    assert np.array_equal(res.support.elems, ref[0])
+    assert res.sample_count == ref[2]
+    assert [(e["candidates"], e["kept"]) for e in res.stage_log] == \
+        [(e["candidates"], e["kept"]) for e in ref[3]]
+    assert workloads.rel_l2(res.coeffs, ref[1]) < 1e-10
