@@ -256,6 +256,97 @@ int sfftb_add_noise(double *x, int64_t rows, int64_t M, uint64_t seed,
 int sfftb_injective_mod_dev(const int64_t *elems, int64_t n, int64_t d,
                             int64_t p, int *injective, void *stream);
 
+/* ---------------------------------------------------------------------
+ * One dimension-incremental detection stage (dimincr.py:178-192 + the union
+ * of :239-240) as ONE host call: the r iterations of coordinate t share M and
+ * L and run as a batch of G groups.  The call enqueues, on `stream`:
+ *   prefix  = gather_rows(prev_J, prev_uidx, prev_ucount)     if prev_J
+ *   J       = prefix x vals (lexicographic)                     if vals
+ *   zmat, tails <- host (pinned) copies
+ *   anchored/bins = structured sampler of the polynomial (support, coeffs)
+ *   ghat, theta0, bits = fused sampler->detection transforms, or the unfused
+ *       inverse DFT / noise / zero test / forward DFT / bitmap chain
+ *   detmask = hash(J, zmat, bits); idx, counts = compaction; medians
+ *   kidx, kcoeffs, kcounts = threshold + top-s_tilde per group
+ *   uidx, ucount = ascending union of the kept indices      if uidx
+ *   host_counts[0:G] = kcounts, host_counts[G] = ucount   (async D2H)
+ * Every buffer is caller-owned (device unless noted); sizes in the comments.
+ * The caller synchronises the stream before reading host_counts.
+ * ------------------------------------------------------------------- */
+typedef struct {
+    /* candidates: J (n x tdim), n = n1 * n2, tdim = t + 1 */
+    const int64_t *prev_J;      /* (n_prev x t) or NULL: prefix given */
+    const int64_t *prev_uidx;   /* indices into prev_J */
+    const int64_t *prev_ucount; /* device count (1) */
+    int64_t *prefix;            /* (n1 x t) */
+    const int64_t *vals;        /* (n2) or NULL: J given */
+    int64_t n1, n2, t;
+    int64_t *J;                 /* (n x tdim) */
+    int64_t n, tdim;
+    /* polynomial of the structured oracle (support (s x d), coeffs (s) c128) */
+    const int64_t *support;
+    const double *coeffs;
+    int64_t s, d;
+    /* lattices: G groups x L, shared M */
+    int64_t G, L, M;
+    const int64_t *zmat_host;   /* pinned (G*L x tdim) */
+    const double *tails_host;   /* pinned (G x tail_w) */
+    int64_t tail_w;             /* max(d - tdim, 1) */
+    int64_t *zmat;              /* (G*L x tdim) */
+    double *tails;              /* (G x tail_w) */
+    uint64_t noise_seed;
+    int64_t call0;
+    double sigma;
+    int fused;                  /* 1: sfftb_sample_detect_dft */
+    /* detection */
+    int64_t kbound, min_hits, s_tilde;
+    double theta;
+    /* buffers */
+    double *anchored;           /* (G x s) c128 */
+    double *bins;               /* (G*L x M) c128 */
+    double *samples;            /* (G*L x M) c128, unfused only */
+    double *ghat;               /* (G*L x M) c128 */
+    double *theta0;             /* (G) */
+    double *sumsq;              /* (G*L), unfused only */
+    uint32_t *bits;             /* (G*L x W) */
+    void *ws_dft;               /* max(sample_detect, dft) workspace */
+    uint32_t *detmask;          /* (G x ceil(n/32)) */
+    int64_t *idx;               /* (G x n) */
+    int64_t *counts;            /* (G) */
+    double *med;                /* (G x n) c128 */
+    void *ws_compact;           /* compact_workspace_bytes(G, n) */
+    int64_t *kidx;              /* (G x n) */
+    double *kco;                /* (G x n) c128 */
+    int64_t *kcounts;           /* (G) */
+    void *ws_topk;              /* topk_workspace_bytes(G, n) */
+    uint32_t *umask;            /* (ceil(n/32)) or NULL: no union */
+    int64_t *uidx;              /* (n) */
+    int64_t *ucount;            /* (1) */
+    int64_t *host_counts;       /* pinned (G + 1) */
+} sfftb_stage_t;
+
+int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Host seed streams (csrc/hostrng.cpp): numpy Generator(PCG64(SeedSequence(
+ * entropy))) restated, for the driver's per-iteration streams
+ * (dimincr.py:99-100).  State = 6 x uint64 per stream (state hi/lo, inc
+ * hi/lo, has_uint32, uinteger).  Host memory only; no device work.
+ * ------------------------------------------------------------------- */
+
+/* rows streams; row r's SeedSequence entropy words (uint32, assembled as
+ * numpy's _coerce_to_uint32_array) are words[r*nwords:(r+1)*nwords]. */
+int sfftb_pcg64_seed(const uint32_t *words, int64_t rows, int64_t nwords,
+                     uint64_t *states);
+
+/* out (rows, count): Generator.random() / uniform(0, 1) draws per stream. */
+int sfftb_pcg64_random(uint64_t *states, int64_t rows, int64_t count,
+                       double *out);
+
+/* out (rows, count): Generator.integers(low, high_incl + 1, dtype=int64). */
+int sfftb_pcg64_integers(uint64_t *states, int64_t rows, int64_t low,
+                         int64_t high_incl, int64_t count, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,10 @@ _SIGS = {
     "sfftb_eval_dense": (_int, [_p, _i64, _i64, _p, _p, _i64, _p, _p]),
     "sfftb_add_noise": (_int, [_p, _i64, _i64, _u64, _i64, _dbl, _p]),
     "sfftb_injective_mod_dev": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int), _p]),
+    "sfftb_sfft_stage": (_int, [_p, _p]),
+    "sfftb_pcg64_seed": (_int, [_p, _i64, _i64, _p]),
+    "sfftb_pcg64_random": (_int, [_p, _i64, _i64, _p]),
+    "sfftb_pcg64_integers": (_int, [_p, _i64, _i64, _i64, _i64, _p]),
 }
 
 _LIB = None

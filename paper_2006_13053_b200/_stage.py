@@ -1,0 +1,123 @@
+"""One dimension-incremental detection stage per host call (sfftb_sfft_stage).
+
+The structured-oracle path of the driver (dimincr.py) hands a whole stage --
+candidate pairing, sampler, fused transforms, hashing, compaction, medians,
+top-s and the union -- to csrc/stage.cu in one ctypes call.  Buffers come from
+a per-reconstruction ``Arena`` that grows to the largest stage and is reused
+(stream order makes reuse safe; J/union buffers alternate between stages
+because stage t+1 gathers its prefix from stage t's J).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _dev, _native
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+
+
+class StageDesc(ctypes.Structure):
+    """Mirror of sfftb_stage_t (include/sfft_b200.h), field for field."""
+
+    _fields_ = [
+        ("prev_J", _p), ("prev_uidx", _p), ("prev_ucount", _p), ("prefix", _p),
+        ("vals", _p), ("n1", _i64), ("n2", _i64), ("t", _i64), ("J", _p), ("n", _i64),
+        ("tdim", _i64),
+        ("support", _p), ("coeffs", _p), ("s", _i64), ("d", _i64),
+        ("G", _i64), ("L", _i64), ("M", _i64), ("zmat_host", _p), ("tails_host", _p),
+        ("tail_w", _i64), ("zmat", _p), ("tails", _p), ("noise_seed", ctypes.c_uint64),
+        ("call0", _i64), ("sigma", ctypes.c_double), ("fused", ctypes.c_int),
+        ("kbound", _i64), ("min_hits", _i64), ("s_tilde", _i64), ("theta", ctypes.c_double),
+        ("anchored", _p), ("bins", _p), ("samples", _p), ("ghat", _p), ("theta0", _p),
+        ("sumsq", _p), ("bits", _p), ("ws_dft", _p), ("detmask", _p), ("idx", _p),
+        ("counts", _p), ("med", _p), ("ws_compact", _p), ("kidx", _p), ("kco", _p),
+        ("kcounts", _p), ("ws_topk", _p), ("umask", _p), ("uidx", _p), ("ucount", _p),
+        ("host_counts", _p),
+    ]
+
+
+class Arena:
+    """Named, growing device (and pinned host) buffers for one reconstruction."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name, numel, dtype=torch.int64, pinned=False):
+        numel = max(int(numel), 1)
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < numel:
+            grow = numel if buf is None else max(numel, buf.numel() * 5 // 4)
+            if pinned:
+                buf = torch.empty(grow, dtype=dtype, pin_memory=True)
+            else:
+                buf = torch.empty(grow, dtype=dtype, device=_dev.device())
+            self._bufs[name] = buf
+        return buf[:numel]
+
+    def bytes(self, name, nbytes):
+        return self.get(name, (int(nbytes) + 7) // 8, torch.int64)
+
+
+def run(desc):
+    lib = _native.lib()
+    _native.check(lib.sfftb_sfft_stage(ctypes.addressof(desc), _dev.stream()),
+                  "sfftb_sfft_stage")
+
+
+def buffers(A, desc, G, L, M, n, s, fused, slot):
+    """Point desc's work buffers at arena storage sized for this stage."""
+    lib = _native.lib()
+    rows = G * L
+    W = int(lib.sfftb_bitmap_words(M))
+    nw = max((n + 31) // 32, 1)
+    cap = max(n, 1)
+    ptr = _dev.ptr
+    desc.anchored = ptr(A.get("anchored", 2 * G * max(s, 1), torch.float64))
+    desc.bins = ptr(A.get("bins", 2 * rows * M, torch.float64))
+    desc.ghat = ptr(A.get("ghat", 2 * rows * M, torch.float64))
+    desc.theta0 = ptr(A.get("theta0", G, torch.float64))
+    desc.bits = ptr(A.get("bits", rows * W, torch.int32))
+    if fused:
+        desc.samples = None
+        desc.sumsq = None
+        desc.ws_dft = ptr(A.bytes("ws_dft", lib.sfftb_sample_detect_workspace_bytes(rows, M)))
+    else:
+        desc.samples = ptr(A.get("samples", 2 * rows * M, torch.float64))
+        desc.sumsq = ptr(A.get("sumsq", rows, torch.float64))
+        desc.ws_dft = ptr(A.bytes("ws_dft", lib.sfftb_dft_workspace_bytes(min(rows, 65535), M)))
+    desc.detmask = ptr(A.get("detmask", G * nw, torch.int32))
+    desc.idx = ptr(A.get("idx", G * cap))
+    desc.counts = ptr(A.get("counts", G))
+    desc.med = ptr(A.get("med", 2 * G * cap, torch.float64))
+    desc.ws_compact = ptr(A.bytes("ws_compact", max(lib.sfftb_compact_workspace_bytes(G, n),
+                                                    lib.sfftb_compact_workspace_bytes(1, n))))
+    kidx = A.get("kidx", G * cap)
+    kco = A.get("kco", 2 * G * cap, torch.float64)
+    desc.kidx, desc.kco = ptr(kidx), ptr(kco)
+    desc.kcounts = ptr(A.get("kcounts", G))
+    desc.ws_topk = ptr(A.bytes("ws_topk", lib.sfftb_topk_workspace_bytes(G, cap)))
+    desc.umask = ptr(A.get("umask", nw, torch.int32))
+    uidx = A.get(f"uidx{slot}", cap)
+    ucount = A.get(f"ucount{slot}", 1)
+    desc.uidx, desc.ucount = ptr(uidx), ptr(ucount)
+    hc = A.get("host_counts", G + 1, torch.int64, pinned=True)
+    desc.host_counts = ptr(hc)
+    return kidx, kco, uidx, ucount, hc
+
+
+def host_inputs(A, zs, tails, tail_w):
+    """Copy generators/tails into pinned staging buffers; returns the tensors."""
+    G, L, tdim = zs.shape
+    zh = A.get("zmat_host", G * L * tdim, torch.int64, pinned=True)
+    zh.numpy()[:] = zs.reshape(-1)
+    th = A.get("tails_host", G * tail_w, torch.float64, pinned=True)
+    tn = th.numpy().reshape(G, tail_w)
+    tn[:] = 0.0
+    for g, tl in enumerate(tails):
+        tn[g, :len(tl)] = tl
+    return zh, th
+

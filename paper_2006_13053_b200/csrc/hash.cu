@@ -45,7 +45,21 @@ struct HashArgs {
     int64_t* hits64;     // may be null
     uint32_t* detmask;   // G * ceil(n/32)
     int64_t nwords;
+    int xsplit;          // FP64 coordinates of the 32-bit path (0: all IMAD)
+    int variant;         // tuning-table entry (d = 10)
 };
+
+// FP64/IMAD split of the 32-bit dot product (see hash_rows)
+constexpr int hash_fp64_coords(int D) { return D >= 4 ? D / 2 : 0; }
+
+static int hash_x_for(int d, int variant) {
+    if (variant < 0) return 0;
+    if (d == 10) {
+        static const int xs[6] = {5, 4, 5, 6, 5, 4};
+        return xs[variant >= 0 && variant < 6 ? variant : 0];
+    }
+    return hash_fp64_coords(d);
+}
 
 // r = u mod M for u < 2^32: q = umulhi(u, floor((2^32-1)/M)) is floor(u/M)
 // or one less, so u + q*(-M) lies in [0, 2M) and one unsigned min finishes.
@@ -148,7 +162,13 @@ __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int l
 // buffers: thread 0 issues a 1-D bulk copy (TMA engine, completion on an
 // mbarrier) for chunk q+2 as soon as every warp is done with chunk q, so the
 // L2 -> SMEM transfer overlaps the hashing of chunk q+1.
-template <int D, int R, bool WIDE, int NT = kHashThreads, bool SLOT = false>
+// X > 0 (32-bit path only): the first X coordinates of each dot product run
+// as FP64 FMAs on the FP64 pipe, the remaining D - X as IMADs on the FMA-heavy
+// pipe, so the two pipes share the multiply work.  The FP64 accumulator starts
+// at 1.5*2^52 + offset: every partial sum is an exact integer in [2^52, 2^53)
+// whose low 32 mantissa bits are (offset + sum_{j<X} k_j z_j) mod 2^32, and
+// that word seeds the integer chain -- bit-identical to the all-IMAD sum.
+template <int D, int R, bool WIDE, int NT = kHashThreads, bool SLOT = false, int X = 0>
 __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     const int g = blockIdx.y;
@@ -160,10 +180,12 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     int32_t* zc = reinterpret_cast<int32_t*>(smem_u32);
     const int zwords = ((a.L * D + 3) & ~3);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_u32 + zwords);
+    double* zd = reinterpret_cast<double*>(smem_u32 + zwords + 4);
+    const int zdwords = X > 0 ? ((a.L * X * 2 + 3) & ~3) : 0;
     // bitmap slots: one per lattice, stride slot_words (a power of two >= W),
     // from the first shared address aligned to the stride
     const uint32_t slot_bytes = (uint32_t)a.slot_words * 4u;
-    const uint32_t after = smem_addr(smem_u32 + zwords + 4);
+    const uint32_t after = smem_addr(smem_u32 + zwords + 4 + zdwords);
     const uint32_t slot0 = SLOT ? (after + slot_bytes - 1) & ~(slot_bytes - 1) : after;
     const uint32_t slot1 = slot0 + (uint32_t)a.Lc * slot_bytes;
     for (int i = threadIdx.x; i < a.L * D; i += blockDim.x) {
@@ -171,7 +193,9 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
         if (z < 0) z += a.M;
         if (!WIDE && z > a.M / 2) z -= a.M;
         zc[i] = (int32_t)z;
+        if (X > 0 && (i % D) < X) zd[(i / D) * X + (i % D)] = (double)z;
     }
+    const double dmagic = 6755399441055744.0 + (double)a.offset;  // 1.5*2^52 + offset
     const int nchunks = (a.L + a.Lc - 1) / a.Lc;
     const bool resident = nchunks == 1;
     const int64_t ntiles = (a.n + TILE - 1) / TILE;
@@ -209,6 +233,11 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
         uint32_t ku[WIDE ? R : 1][WIDE ? D : 1];
         bool valid[R];
         load_rows<D, R, WIDE>(a, base, lane, k, ku, valid);
+        double kd[R][X > 0 ? X : 1];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int j = 0; j < X; ++j) kd[q][j] = (double)k[q][j];
         {  // warm L2 with the next tile's rows while this one is hashed
             const int64_t nb = (tile + gridDim.x) * TILE + (int64_t)warp * 32 * R;
 #pragma unroll
@@ -230,15 +259,24 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
             for (int l = l0; l < lend; ++l) {
                 int32_t zr[D];
 #pragma unroll
-                for (int j = 0; j < D; ++j) zr[j] = zc[l * D + j];
+                for (int j = X; j < D; ++j) zr[j] = zc[l * D + j];
+                double zdr[X > 0 ? X : 1];
+#pragma unroll
+                for (int j = 0; j < X; ++j) zdr[j] = zd[l * X + j];
                 const uint32_t lb = bbase + (uint32_t)(l - l0) * slot_bytes;
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     uint32_t r;
                     if (!WIDE) {
                         uint32_t u = a.offset;
+                        if (X > 0) {
+                            double acc = dmagic;
 #pragma unroll
-                        for (int j = 0; j < D; ++j) u += (uint32_t)k[q][j] * (uint32_t)zr[j];
+                            for (int j = 0; j < X; ++j) acc = __fma_rn(kd[q][j], zdr[j], acc);
+                            u = (uint32_t)__double2loint(acc);
+                        }
+#pragma unroll
+                        for (int j = X; j < D; ++j) u += (uint32_t)k[q][j] * (uint32_t)zr[j];
                         r = mod_u32(u, M32, negM, a.magic);
                     } else {
                         uint64_t acc = 0;
@@ -650,9 +688,9 @@ static int grid_for(int64_t work, int threads) {
 // hash dispatch
 // ---------------------------------------------------------------------------
 
-template <int D, int R, bool WIDE, int NT, bool SLOT>
+template <int D, int R, bool WIDE, int NT, bool SLOT, int X>
 static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = hash_rows<D, R, WIDE, NT, SLOT>;
+    auto kern = hash_rows<D, R, WIDE, NT, SLOT, X>;
     SFFTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
     int per_sm = 0;
@@ -667,11 +705,11 @@ static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
     return SFFTB_OK;
 }
 
-template <int D, int R, bool WIDE, int NT = kHashThreads>
+template <int D, int R, bool WIDE, int NT = kHashThreads, int X = 0>
 static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
     const bool pow2 = (a.slot_words & (a.slot_words - 1)) == 0;
-    return pow2 ? launch_hash_s<D, R, WIDE, NT, true>(a, smem, st)
-                : launch_hash_s<D, R, WIDE, NT, false>(a, smem, st);
+    return pow2 ? launch_hash_s<D, R, WIDE, NT, true, X>(a, smem, st)
+                : launch_hash_s<D, R, WIDE, NT, false, X>(a, smem, st);
 }
 
 // 640 threads (20 warps) per SM with R rows per thread, R*D <= ~60 int32
@@ -681,6 +719,21 @@ template <int D, bool WIDE>
 static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
     constexpr int R = D <= 5 ? 12 : (D <= 7 ? 8 : (D <= 10 ? 6 : (D <= 15 ? 4 : 3)));
     constexpr int RW = R / 2 > 0 ? R / 2 : 1;  // the 64-bit path needs wider temporaries
+    if (!WIDE && a.xsplit > 0) {
+        if (D == 10) {  // tuning table (SFFTB_HASH_VARIANT), default first
+            switch (a.variant) {
+                case 1: return launch_hash_t<D, 4, false, 640, 4>(a, smem, st);
+                case 2: return launch_hash_t<D, 5, false, 640, 5>(a, smem, st);
+                case 3: return launch_hash_t<D, 4, false, 640, 6>(a, smem, st);
+                case 4: return launch_hash_t<D, 3, false, 640, 5>(a, smem, st);
+                case 5: return launch_hash_t<D, 6, false, 640, 4>(a, smem, st);
+                default: return launch_hash_t<D, 4, false, 640, 5>(a, smem, st);
+            }
+        }
+        constexpr int XS = hash_fp64_coords(D);
+        constexpr int RS = 60 / (D + XS) < 1 ? 1 : (60 / (D + XS) < R ? 60 / (D + XS) : R);
+        return launch_hash_t<D, RS, false, 640, XS>(a, smem, st);
+    }
     return launch_hash_t<D, (WIDE ? RW : R), WIDE, 640>(a, smem, st);
 }
 
@@ -746,7 +799,24 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     const int64_t lat_bytes = W * 4;
     int64_t pow2_words = 4;
     while (pow2_words < W) pow2_words <<= 1;
-    const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4 + 16;
+    // 32-bit path: u = offset + sum_j k_j zc_j stays in [0, 2^32)
+    const int64_t zmax = M / 2;
+    bool fast = false;
+    if (kbound >= 0 && d >= 1 && d <= 20) {
+        const __int128 B = (__int128)kbound * zmax;
+        const __int128 off = ((B + M - 1) / M) * M;
+        if (off + B < ((__int128)1 << 32) && kbound < (int64_t(1) << 31)) {
+            fast = true;
+            a.offset = (uint32_t)off;
+        }
+    }
+    {
+        const char* v = getenv("SFFTB_HASH_VARIANT");
+        a.variant = v ? atoi(v) : 0;
+    }
+    a.xsplit = fast ? hash_x_for((int)d, a.variant) : 0;
+    const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4 + 16 +
+                           ((L * a.xsplit * 2 + 3) & ~int64_t(3)) * 4;
     int64_t slot_bytes, smem_i;
     // (a) resident: power-of-two slots (OR addressing) when all L fit
     const int64_t pow2_bytes = pow2_words * 4;
@@ -773,17 +843,6 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     a.slot_words = (int)(slot_bytes / 4);
     const size_t smem = (size_t)smem_i;
 
-    // 32-bit path: u = offset + sum_j k_j zc_j stays in [0, 2^32)
-    const int64_t zmax = M / 2;
-    bool fast = false;
-    if (kbound >= 0 && d >= 1 && d <= 20) {
-        const __int128 B = (__int128)kbound * zmax;
-        const __int128 off = ((B + M - 1) / M) * M;
-        if (off + B < ((__int128)1 << 32) && kbound < (int64_t(1) << 31)) {
-            fast = true;
-            a.offset = (uint32_t)off;
-        }
-    }
     if (fast) return hash_dispatch<false>((int)d, a, smem, st);
     // 64-bit path: exact while d*(M-1)^2 < 2^62 (the reference's own bound,
     // detect.py:128-129); beyond that the 128-bit generic kernel

@@ -1,0 +1,106 @@
+// One detection stage of the dimension-incremental driver as a single host
+// call (include/sfft_b200.h: sfftb_sfft_stage).  No new device code: the
+// stage is the sequence of the library's own entry points that the Python
+// driver issued one ctypes call at a time (dimincr.py _detect_stage +
+// _engine), composed here so the ~12 launches of a stage cost microseconds
+// of host time instead of ~0.3 ms of interpreter overhead while the GPU idles
+// between stages.
+#include "common.cuh"
+#include "../../include/sfft_b200.h"
+
+#define SFFTB_TRY(x)                    \
+    do {                                \
+        const int rc_ = (x);            \
+        if (rc_ != SFFTB_OK) return rc_; \
+    } while (0)
+
+extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
+    SFFTB_REQUIRE(a != nullptr, "stage: null descriptor");
+    SFFTB_REQUIRE(a->G >= 1 && a->L >= 1 && a->M >= 1 && a->tdim >= 1 && a->n >= 0,
+                  "stage: bad sizes");
+    SFFTB_REQUIRE(a->d >= a->tdim && a->tail_w >= 1, "stage: bad dimensions");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = a->G, L = a->L, M = a->M, n = a->n, tdim = a->tdim;
+    const int64_t rows = G * L;
+
+    // candidates
+    if (a->prev_J) {
+        SFFTB_TRY(sfftb_gather_rows(a->prev_J, a->t, a->prev_uidx, a->prev_ucount, a->n1,
+                                    a->prefix, stream));
+    }
+    if (a->vals) {
+        SFFTB_REQUIRE(a->n1 * a->n2 == n && a->t + 1 == tdim, "stage: pair sizes");
+        SFFTB_TRY(sfftb_pair_product(a->prefix, a->n1, a->t, a->vals, a->n2, a->J, stream));
+    }
+
+    // generators and tails drawn on the host
+    SFFTB_CUDA(cudaMemcpyAsync(a->zmat, a->zmat_host, (size_t)(rows * tdim) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, st));
+    SFFTB_CUDA(cudaMemcpyAsync(a->tails, a->tails_host,
+                               (size_t)(G * a->tail_w) * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+
+    // structured sampler: anchored coefficients -> residue bins
+    if (a->s > 0)
+        SFFTB_TRY(sfftb_anchor_coeffs(a->support, a->s, a->d, tdim, a->coeffs, a->tails, G,
+                                      a->anchored, stream));
+    SFFTB_TRY(sfftb_scatter_bins(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L, M,
+                                 a->bins, nullptr, stream));
+
+    // samples -> zero test, spectra, bitmaps
+    if (a->fused) {
+        SFFTB_TRY(sfftb_sample_detect_dft(a->bins, G, L, M, a->noise_seed, a->call0, a->sigma,
+                                          a->ghat, a->theta0, a->bits, a->ws_dft, stream));
+    } else {
+        const int64_t step = 65535;
+        for (int64_t b0 = 0; b0 < rows; b0 += step) {
+            const int64_t nb = rows - b0 < step ? rows - b0 : step;
+            SFFTB_TRY(sfftb_dft(a->bins + 2 * b0 * M, M, a->samples + 2 * b0 * M, M, nb, M, 1,
+                                1.0, a->ws_dft, stream));
+        }
+        if (a->sigma > 0)
+            SFFTB_TRY(sfftb_add_noise(a->samples, rows, M, a->noise_seed, a->call0, a->sigma,
+                                      stream));
+        SFFTB_TRY(sfftb_sumsq(a->samples, M, rows, M, a->sumsq, stream));
+        SFFTB_TRY(sfftb_zero_thresholds(a->sumsq, G, L, M, a->theta0, stream));
+        for (int64_t b0 = 0; b0 < rows; b0 += step) {
+            const int64_t nb = rows - b0 < step ? rows - b0 : step;
+            SFFTB_TRY(sfftb_dft(a->samples + 2 * b0 * M, M, a->ghat + 2 * b0 * M, M, nb, M, 0,
+                                1.0 / (double)M, a->ws_dft, stream));
+        }
+        SFFTB_TRY(sfftb_nonzero_bitmap(a->ghat, G, L, M, a->theta0, a->bits, stream));
+    }
+
+    // hashing, compaction, medians, top-s
+    if (n > 0) {
+        SFFTB_TRY(sfftb_hash_hits(a->J, n, tdim, a->zmat, G, L, M, a->bits, a->kbound,
+                                  a->min_hits, nullptr, a->detmask, stream));
+        SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
+                                     stream));
+        SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts, n,
+                                a->med, stream));
+    } else {
+        SFFTB_CUDA(cudaMemsetAsync(a->counts, 0, (size_t)G * sizeof(int64_t), st));
+    }
+    const int64_t cap = n > 0 ? n : 1;
+    SFFTB_TRY(sfftb_topk(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde, a->kidx,
+                         a->kco, a->kcounts, a->ws_topk, stream));
+    SFFTB_CUDA(cudaMemcpyAsync(a->host_counts, a->kcounts, (size_t)G * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+
+    // union of the kept indices (ascending)
+    if (a->umask) {
+        const int64_t nwords = (n + 31) / 32 > 0 ? (n + 31) / 32 : 1;
+        SFFTB_CUDA(cudaMemsetAsync(a->umask, 0, (size_t)nwords * sizeof(uint32_t), st));
+        SFFTB_TRY(sfftb_mark_indices(a->kidx, a->kcounts, G, cap, a->umask, n, stream));
+        if (n > 0) {
+            SFFTB_TRY(sfftb_compact_mask(a->umask, 1, n, a->uidx, a->ucount, a->ws_compact,
+                                         stream));
+        } else {
+            SFFTB_CUDA(cudaMemsetAsync(a->ucount, 0, sizeof(int64_t), st));
+        }
+        SFFTB_CUDA(cudaMemcpyAsync(a->host_counts + G, a->ucount, sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, st));
+    }
+    return SFFTB_OK;
+}

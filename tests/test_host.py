@@ -94,3 +94,34 @@ def test_next_valid_prime_shortcut_is_exact_on_host():
     # expansion shortcut already certifies every p > 5 on the host
     assert pkg.lattice._injective_mod(S, 7)
     assert pkg.next_valid_prime(pkg.full_grid(3, 10), 10.33 * 1000) == 10331
+
+
+def test_native_seed_streams_match_numpy():
+    """hostrng.Streams draws exactly what default_rng(SeedSequence(e)) draws:
+    uniform nodes/tails, 32-bit and 64-bit Lemire integers, interleaved, and
+    the numpy hand-over for other draws."""
+    from paper_2006_13053_b200 import hostrng
+
+    ents = [(2006, t % 3, t, i) for t in range(6) for i in range(4)]
+    ents += [(0, 0, 0, 0), (2**63 + 5, 1, 2, 3), (2**70 + 3, 2, 0, 0)]
+    S = hostrng.Streams(ents)
+    for r, e in enumerate(ents):
+        g = np.random.default_rng(np.random.SeedSequence(e))
+        s = S[r]
+        assert np.array_equal(s.uniform(size=5), g.uniform(size=5))
+        for M in (1, 2, 211, 20663, 103307, 2**31 - 1, 2**32 - 1, 2**32, 2**40 + 7, 2**62):
+            assert np.array_equal(s.integers(0, M, size=(3, 4), dtype=np.int64),
+                                  g.integers(0, M, size=(3, 4), dtype=np.int64))
+            assert np.array_equal(s.uniform(size=1), g.uniform(size=1))
+        assert np.array_equal(s.uniform(-1, 1, size=(2, 2)), g.uniform(-1, 1, size=(2, 2)))
+        assert np.array_equal(s.integers(-7, 9, size=13), g.integers(-7, 9, size=13))
+        assert s.numpy().integers(2**20) == g.integers(2**20)
+    batch = hostrng.streams(11, 1, 4, range(5))
+    tails = batch.uniform_each(3)
+    z = batch.integers_each(0, 1031, (7, 2))
+    for i in range(5):
+        g = np.random.default_rng(np.random.SeedSequence((11, 1, 4, i)))
+        assert np.array_equal(tails[i], g.uniform(size=3))
+        assert np.array_equal(z[i], g.integers(0, 1031, size=(7, 2), dtype=np.int64))
+    with pytest.raises(ValueError):
+        hostrng.streams(-1, 0, 0, [0])

@@ -39,3 +39,5 @@ ms = [ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps)]
 bytes_ = n * 8 * d + n * 8 + L * W * 4 + n // 8
 print(f"hash n=2^{lg}: ms={ms} -> {bytes_ / (min(ms) * 1e-3) / 1e9:.0f} GB/s, "
       f"{n / (min(ms) * 1e-3):.3e} cand/s, mean hits {hits.float().mean().item():.3f}")
+chk = int((hits * torch.arange(n, device="cuda", dtype=torch.int64).remainder(1000003)).sum())
+print(f"checksum {chk} mask {int(mask.to(torch.int64).sum())}")
