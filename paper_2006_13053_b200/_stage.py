@@ -58,8 +58,15 @@ class Arena:
             self._bufs[name] = buf
         return buf[:numel]
 
+    def ptr(self, name, numel, dtype=torch.int64):
+        """Device address of a buffer of >= numel elements (no view built)."""
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = self.get(name, numel, dtype)
+        return buf.data_ptr()
+
     def bytes(self, name, nbytes):
-        return self.get(name, (int(nbytes) + 7) // 8, torch.int64)
+        return self.ptr(name, (int(nbytes) + 7) // 8)
 
 
 def run(desc):
@@ -69,43 +76,44 @@ def run(desc):
 
 
 def buffers(A, desc, G, L, M, n, s, fused, slot):
-    """Point desc's work buffers at arena storage sized for this stage."""
+    """Point desc's work buffers at arena storage sized for this stage;
+    returns the tensors the driver reads afterwards."""
     lib = _native.lib()
+    f64 = torch.float64
     rows = G * L
     W = int(lib.sfftb_bitmap_words(M))
     nw = max((n + 31) // 32, 1)
     cap = max(n, 1)
-    ptr = _dev.ptr
-    desc.anchored = ptr(A.get("anchored", 2 * G * max(s, 1), torch.float64))
-    desc.bins = ptr(A.get("bins", 2 * rows * M, torch.float64))
-    desc.ghat = ptr(A.get("ghat", 2 * rows * M, torch.float64))
-    desc.theta0 = ptr(A.get("theta0", G, torch.float64))
-    desc.bits = ptr(A.get("bits", rows * W, torch.int32))
+    P = A.ptr
+    desc.anchored = P("anchored", 2 * G * max(s, 1), f64)
+    desc.bins = P("bins", 2 * rows * M, f64)
+    desc.ghat = P("ghat", 2 * rows * M, f64)
+    desc.theta0 = P("theta0", G, f64)
+    desc.bits = P("bits", rows * W, torch.int32)
     if fused:
-        desc.samples = None
-        desc.sumsq = None
-        desc.ws_dft = ptr(A.bytes("ws_dft", lib.sfftb_sample_detect_workspace_bytes(rows, M)))
+        desc.samples = desc.sumsq = None
+        desc.ws_dft = A.bytes("ws_dft", lib.sfftb_sample_detect_workspace_bytes(rows, M))
     else:
-        desc.samples = ptr(A.get("samples", 2 * rows * M, torch.float64))
-        desc.sumsq = ptr(A.get("sumsq", rows, torch.float64))
-        desc.ws_dft = ptr(A.bytes("ws_dft", lib.sfftb_dft_workspace_bytes(min(rows, 65535), M)))
-    desc.detmask = ptr(A.get("detmask", G * nw, torch.int32))
-    desc.idx = ptr(A.get("idx", G * cap))
-    desc.counts = ptr(A.get("counts", G))
-    desc.med = ptr(A.get("med", 2 * G * cap, torch.float64))
-    desc.ws_compact = ptr(A.bytes("ws_compact", max(lib.sfftb_compact_workspace_bytes(G, n),
-                                                    lib.sfftb_compact_workspace_bytes(1, n))))
+        desc.samples = P("samples", 2 * rows * M, f64)
+        desc.sumsq = P("sumsq", rows, f64)
+        desc.ws_dft = A.bytes("ws_dft", lib.sfftb_dft_workspace_bytes(min(rows, 65535), M))
+    desc.detmask = P("detmask", G * nw, torch.int32)
+    desc.idx = P("idx", G * cap)
+    desc.counts = P("counts", G)
+    desc.med = P("med", 2 * G * cap, f64)
+    desc.ws_compact = A.bytes("ws_compact", max(lib.sfftb_compact_workspace_bytes(G, n),
+                                                lib.sfftb_compact_workspace_bytes(1, n)))
     kidx = A.get("kidx", G * cap)
-    kco = A.get("kco", 2 * G * cap, torch.float64)
-    desc.kidx, desc.kco = ptr(kidx), ptr(kco)
-    desc.kcounts = ptr(A.get("kcounts", G))
-    desc.ws_topk = ptr(A.bytes("ws_topk", lib.sfftb_topk_workspace_bytes(G, cap)))
-    desc.umask = ptr(A.get("umask", nw, torch.int32))
+    kco = A.get("kco", 2 * G * cap, f64)
+    desc.kidx, desc.kco = kidx.data_ptr(), kco.data_ptr()
+    desc.kcounts = P("kcounts", G)
+    desc.ws_topk = A.bytes("ws_topk", lib.sfftb_topk_workspace_bytes(G, cap))
+    desc.umask = P("umask", nw, torch.int32)
     uidx = A.get(f"uidx{slot}", cap)
     ucount = A.get(f"ucount{slot}", 1)
-    desc.uidx, desc.ucount = ptr(uidx), ptr(ucount)
+    desc.uidx, desc.ucount = uidx.data_ptr(), ucount.data_ptr()
     hc = A.get("host_counts", G + 1, torch.int64, pinned=True)
-    desc.host_counts = ptr(hc)
+    desc.host_counts = hc.data_ptr()
     return kidx, kco, uidx, ucount, hc
 
 

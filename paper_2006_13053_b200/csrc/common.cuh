@@ -53,6 +53,22 @@ inline int num_sms() {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel)
+// and size: launch paths call this every time, the driver call is skipped
+// when an equal or larger opt-in is already recorded.
+cudaError_t smem_opt_in_raw(const void* kernel, size_t bytes);
+template <typename K>
+inline cudaError_t smem_opt_in(K kernel, size_t bytes) {
+    return smem_opt_in_raw(reinterpret_cast<const void*>(kernel), bytes);
+}
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor, memoised per (device,
+// kernel, threads, smem).
+cudaError_t occupancy_raw(int* out, const void* kernel, int threads, size_t smem);
+template <typename K>
+inline cudaError_t occupancy(int* out, K kernel, int threads, size_t smem) {
+    return occupancy_raw(out, reinterpret_cast<const void*>(kernel), threads, smem);
+}
+
 // complex double helpers (interleaved re, im == numpy complex128 layout)
 struct cplx {
     double x, y;

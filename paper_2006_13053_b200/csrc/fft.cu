@@ -718,8 +718,7 @@ __global__ void partial_sumsq_reduce(const double* __restrict__ part, int64_t ro
 
 template <typename K>
 static cudaError_t allow_smem(K kernel, size_t bytes) {
-    if (bytes <= 48 * 1024) return cudaSuccess;
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return smem_opt_in(kernel, bytes);
 }
 
 template <int N, bool INV>

@@ -49,16 +49,9 @@ struct HashArgs {
     int variant;         // tuning-table entry (d = 10)
 };
 
-// FP64/IMAD split of the 32-bit dot product (see hash_rows)
-constexpr int hash_fp64_coords(int D) { return D >= 4 ? D / 2 : 0; }
-
+// FP64/IMAD split of the 32-bit dot product (see hash_rows): opt-in only
 static int hash_x_for(int d, int variant) {
-    if (variant < 0) return 0;
-    if (d == 10) {
-        static const int xs[6] = {5, 4, 5, 6, 5, 4};
-        return xs[variant >= 0 && variant < 6 ? variant : 0];
-    }
-    return hash_fp64_coords(d);
+    return (d == 10 && (variant == 1 || variant == 2)) ? 5 : 0;
 }
 
 // r = u mod M for u < 2^32: q = umulhi(u, floor((2^32-1)/M)) is floor(u/M)
@@ -691,10 +684,9 @@ static int grid_for(int64_t work, int threads) {
 template <int D, int R, bool WIDE, int NT, bool SLOT, int X>
 static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
     auto kern = hash_rows<D, R, WIDE, NT, SLOT, X>;
-    SFFTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+    SFFTB_CUDA(smem_opt_in(kern, smem));
     int per_sm = 0;
-    SFFTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    SFFTB_CUDA(occupancy(&per_sm, kern, NT, smem));
     per_sm = std::max(per_sm, 1);
     constexpr int TILE = (NT / 32) * 32 * R;
     const int64_t ntiles = ceil_div(a.n, TILE);
@@ -719,20 +711,13 @@ template <int D, bool WIDE>
 static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
     constexpr int R = D <= 5 ? 12 : (D <= 7 ? 8 : (D <= 10 ? 6 : (D <= 15 ? 4 : 3)));
     constexpr int RW = R / 2 > 0 ? R / 2 : 1;  // the 64-bit path needs wider temporaries
-    if (!WIDE && a.xsplit > 0) {
-        if (D == 10) {  // tuning table (SFFTB_HASH_VARIANT), default first
-            switch (a.variant) {
-                case 1: return launch_hash_t<D, 4, false, 640, 4>(a, smem, st);
-                case 2: return launch_hash_t<D, 5, false, 640, 5>(a, smem, st);
-                case 3: return launch_hash_t<D, 4, false, 640, 6>(a, smem, st);
-                case 4: return launch_hash_t<D, 3, false, 640, 5>(a, smem, st);
-                case 5: return launch_hash_t<D, 6, false, 640, 4>(a, smem, st);
-                default: return launch_hash_t<D, 4, false, 640, 5>(a, smem, st);
-            }
+    if constexpr (D == 10 && !WIDE) {
+        // opt-in FP64/IMAD split (SFFTB_HASH_VARIANT=1|2); measured slower
+        // than the all-IMAD default on B200 (profiles/r01/SUMMARY.md)
+        if (a.xsplit > 0) {
+            if (a.variant == 2) return launch_hash_t<D, 3, false, 640, 5>(a, smem, st);
+            return launch_hash_t<D, 4, false, 640, 5>(a, smem, st);
         }
-        constexpr int XS = hash_fp64_coords(D);
-        constexpr int RS = 60 / (D + XS) < 1 ? 1 : (60 / (D + XS) < R ? 60 / (D + XS) : R);
-        return launch_hash_t<D, RS, false, 640, XS>(a, smem, st);
     }
     return launch_hash_t<D, (WIDE ? RW : R), WIDE, 640>(a, smem, st);
 }
@@ -812,7 +797,7 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     }
     {
         const char* v = getenv("SFFTB_HASH_VARIANT");
-        a.variant = v ? atoi(v) : 0;
+        a.variant = v ? atoi(v) : 0;  // 0: all-IMAD default
     }
     a.xsplit = fast ? hash_x_for((int)d, a.variant) : 0;
     const int64_t zbytes = ((L * std::max<int64_t>(d, 1) + 3) & ~int64_t(3)) * 4 + 16 +
@@ -855,8 +840,7 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
         1, std::min<int64_t>(std::max<int64_t>(L, 1),
                              ((int64_t)kBitmapSmemBudget - 16) / lat_bytes));
     const size_t smem_g = (size_t)((int64_t)a.Lc * lat_bytes);
-    SFFTB_CUDA(cudaFuncSetAttribute(hash_rows_generic,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+    SFFTB_CUDA(smem_opt_in(hash_rows_generic, smem_g));
     const int64_t ntiles = ceil_div(n, kHashThreads);
     const int gx = (int)std::max<int64_t>(
         1, std::min<int64_t>(ntiles, ceil_div((int64_t)num_sms(), G)));

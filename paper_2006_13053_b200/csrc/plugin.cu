@@ -13,6 +13,9 @@
 #include <math.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -25,6 +28,39 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static std::mutex g_attr_mu;
+static std::map<std::pair<int, const void*>, size_t> g_smem_set;
+static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+
+cudaError_t smem_opt_in_raw(const void* kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto key = std::make_pair(dev, kernel);
+    auto it = g_smem_set.find(key);
+    if (it != g_smem_set.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e =
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) g_smem_set[key] = bytes;
+    return e;
+}
+
+cudaError_t occupancy_raw(int* out, const void* kernel, int threads, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto key = std::make_tuple(dev, kernel, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, smem);
+    if (e == cudaSuccess) g_occ[key] = *out;
+    return e;
+}
 
 __global__ void scatter_medians_kernel(const int64_t* __restrict__ idx,
                                        const int64_t* __restrict__ count,

@@ -195,8 +195,7 @@ extern "C" int sfftb_scatter_bins(const int64_t* support, int64_t s, int64_t d, 
     if (lat == 0) return SFFTB_OK;
     SFFTB_REQUIRE(lat <= 0x7fffffff, "scatter: too many lattices");
     const size_t sm = sizeof(uint64_t) * kScatterChunk;
-    SFFTB_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sm));
+    SFFTB_CUDA(smem_opt_in(scatter_kernel, sm));
     scatter_kernel<<<(unsigned)lat, kScatterThreads, sm, (cudaStream_t)stream>>>(
         support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M,
         (double2*)bins);

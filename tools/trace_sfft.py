@@ -44,8 +44,36 @@ def download(t):
     return r
 
 
+from paper_2006_13053_b200 import _stage, dimincr  # noqa: E402
+
+orig_run = _stage.run
+
+
+def run(desc):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    h = time.perf_counter()
+    e0.record()
+    orig_run(desc)
+    e1.record()
+    log.append((f"<stage G={desc.G} L={desc.L} M={desc.M} n={desc.n}>", h, time.perf_counter(),
+                e0, e1))
+
+
+orig_step1 = dimincr.step1_components
+
+
+def step1(*a, **k):
+    h = time.perf_counter()
+    out = orig_step1(*a, **k)
+    log.append(("<step1_components>", h, time.perf_counter(), None, None))
+    return out
+
+
 _native.call = call
 _dev.download = download
+_stage.run = run
+dimincr.step1_components = step1
 start_ev = torch.cuda.Event(enable_timing=True)
 t0 = time.perf_counter()
 start_ev.record()
