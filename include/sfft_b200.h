@@ -323,6 +323,9 @@ typedef struct {
     int64_t *uidx;              /* (n) */
     int64_t *ucount;            /* (1) */
     int64_t *host_counts;       /* pinned (G + 1) */
+    /* optional: 7 cudaEvent_t recorded at the phase boundaries (candidates |
+     * sampler | transforms | hashing | compaction+medians | top-s+union) */
+    void *const *events;
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);

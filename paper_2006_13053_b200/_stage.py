@@ -36,8 +36,12 @@ class StageDesc(ctypes.Structure):
         ("sumsq", _p), ("bits", _p), ("ws_dft", _p), ("detmask", _p), ("idx", _p),
         ("counts", _p), ("med", _p), ("ws_compact", _p), ("kidx", _p), ("kco", _p),
         ("kcounts", _p), ("ws_topk", _p), ("umask", _p), ("uidx", _p), ("ucount", _p),
-        ("host_counts", _p),
+        ("host_counts", _p), ("events", _p),
     ]
+
+
+PHASES = ("candidates", "sampler", "transforms", "hashing", "compaction+medians",
+          "top-s+union")
 
 
 class Arena:
@@ -70,9 +74,26 @@ class Arena:
 
 
 def run(desc):
+    """One stage call; under a _native.Timeline the phase boundaries are
+    recorded (CUDA events on the launch stream) as 'stage:<phase>' entries."""
     lib = _native.lib()
-    _native.check(lib.sfftb_sfft_stage(ctypes.addressof(desc), _dev.stream()),
-                  "sfftb_sfft_stage")
+    tl = _native._TIMELINE
+    evs = None
+    if tl is not None:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(PHASES) + 1)]
+        for e in evs:
+            e.record()  # materialise the cudaEvent_t; the stage re-records it
+        arr = (ctypes.c_void_p * len(evs))(*[e.cuda_event for e in evs])
+        desc.events = ctypes.addressof(arr)
+    else:
+        desc.events = None
+    rc = lib.sfftb_sfft_stage(ctypes.addressof(desc), _dev.stream())
+    if evs is not None:
+        for k, ph in enumerate(PHASES):
+            tl.records.append((f"stage:{ph}", evs[k], evs[k + 1]))
+        tl.records.append(("sfftb_sfft_stage", evs[0], evs[-1]))
+        desc.events = None
+    _native.check(rc, "sfftb_sfft_stage")
 
 
 def buffers(A, desc, G, L, M, n, s, fused, slot):

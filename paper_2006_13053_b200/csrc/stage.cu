@@ -22,6 +22,12 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t G = a->G, L = a->L, M = a->M, n = a->n, tdim = a->tdim;
     const int64_t rows = G * L;
+    auto mark = [&](int k) -> int {
+        if (a->events && a->events[k])
+            SFFTB_CUDA(cudaEventRecord((cudaEvent_t)a->events[k], st));
+        return SFFTB_OK;
+    };
+    SFFTB_TRY(mark(0));
 
     // candidates
     if (a->prev_J) {
@@ -34,6 +40,7 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
     }
 
     // generators and tails drawn on the host
+    SFFTB_TRY(mark(1));
     SFFTB_CUDA(cudaMemcpyAsync(a->zmat, a->zmat_host, (size_t)(rows * tdim) * sizeof(int64_t),
                                cudaMemcpyHostToDevice, st));
     SFFTB_CUDA(cudaMemcpyAsync(a->tails, a->tails_host,
@@ -48,6 +55,7 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
                                  a->bins, nullptr, stream));
 
     // samples -> zero test, spectra, bitmaps
+    SFFTB_TRY(mark(2));
     if (a->fused) {
         SFFTB_TRY(sfftb_sample_detect_dft(a->bins, G, L, M, a->noise_seed, a->call0, a->sigma,
                                           a->ghat, a->theta0, a->bits, a->ws_dft, stream));
@@ -72,16 +80,20 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
     }
 
     // hashing, compaction, medians, top-s
+    SFFTB_TRY(mark(3));
     if (n > 0) {
         SFFTB_TRY(sfftb_hash_hits(a->J, n, tdim, a->zmat, G, L, M, a->bits, a->kbound,
                                   a->min_hits, nullptr, a->detmask, stream));
+        SFFTB_TRY(mark(4));
         SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
                                      stream));
         SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts, n,
                                 a->med, stream));
     } else {
+        SFFTB_TRY(mark(4));
         SFFTB_CUDA(cudaMemsetAsync(a->counts, 0, (size_t)G * sizeof(int64_t), st));
     }
+    SFFTB_TRY(mark(5));
     const int64_t cap = n > 0 ? n : 1;
     SFFTB_TRY(sfftb_topk(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde, a->kidx,
                          a->kco, a->kcounts, a->ws_topk, stream));
@@ -102,5 +114,6 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
         SFFTB_CUDA(cudaMemcpyAsync(a->host_counts + G, a->ucount, sizeof(int64_t),
                                    cudaMemcpyDeviceToHost, st));
     }
+    SFFTB_TRY(mark(6));
     return SFFTB_OK;
 }

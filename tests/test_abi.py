@@ -57,3 +57,25 @@ def test_hyperbolic_cross_paper_counts():
 
     # PAPER.md table values quoted in SURVEY section 4
     assert hyperbolic_cross(3, 4, count_only=True) == 225
+
+
+def test_stage_descriptor_layout_matches_header(tmp_path):
+    """_stage.StageDesc mirrors sfftb_stage_t field for field (offsets, size)."""
+    import ctypes
+    import subprocess
+
+    from paper_2006_13053_b200._stage import StageDesc
+
+    names = [f[0] for f in StageDesc._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"sfft_b200.h\"\n"
+                   "int main(void){printf(\"%zu\\n\", sizeof(sfftb_stage_t));\n" +
+                   "".join(f"printf(\"%zu\\n\", offsetof(sfftb_stage_t, {n}));\n" for n in names)
+                   + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    out = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert out[0] == ctypes.sizeof(StageDesc)
+    assert out[1:] == [getattr(StageDesc, n).offset for n in names]
