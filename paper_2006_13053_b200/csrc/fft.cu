@@ -483,15 +483,10 @@ __global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
         }
         __syncthreads();  // previous tile done with the slots
         fft2pass<N2, false>(v, slot, t, tw2);
+        out_twiddle<N2, false>(v, n1, t, hi, lo);
         double2* Tw = a.work + b * (int64_t)N;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int k2 = fft2_out_index<N2>(t, e);
-            const int ex = n1 * k2;
-            double2 w = v[e];
-            if (ex) w = cmul(w, twiddle2<false>(hi, lo, ex));
-            Tw[(int64_t)k2 * N1 + n1] = w;
-        }
+        for (int e = 0; e < 16; ++e) Tw[(int64_t)fft2_out_index<N2>(t, e) * N1 + n1] = v[e];
     }
 }
 
@@ -526,14 +521,9 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB(DftArgs a, int N2) {
         for (int e = 0; e < 16; ++e) v[e] = cmul(v[e], __ldg(bh + fft2_out_index<N1>(t, e)));
         fft2_out_to_in<N1>(v);
         fft2pass<N1, true>(v, slot, t, tw1);
+        out_twiddle<N1, true>(v, k2, t, hi, lo);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int m1 = fft2_out_index<N1>(t, e);
-            const int ex = m1 * k2;
-            double2 w = v[e];
-            if (ex) w = cmul(w, twiddle2<true>(hi, lo, ex));
-            row[m1] = w;
-        }
+        for (int e = 0; e < 16; ++e) row[fft2_out_index<N1>(t, e)] = v[e];
     }
 }
 
@@ -638,14 +628,9 @@ __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
             for (int w8 = 0; w8 < 8; ++w8) s8 += red[w8];
             a.sumsq_part[b * per_b + tile % per_b] = s8;
         }
+        out_twiddle<N2, false>(v, m1, t, hi, lo);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int k2 = fft2_out_index<N2>(t, e);
-            const int ex = m1 * k2;
-            double2 w = v[e];
-            if (ex) w = cmul(w, twiddle2<false>(hi, lo, ex));
-            Tw[(int64_t)k2 * N1 + m1] = w;
-        }
+        for (int e = 0; e < 16; ++e) Tw[(int64_t)fft2_out_index<N2>(t, e) * N1 + m1] = v[e];
     }
 }
 

@@ -222,6 +222,37 @@ __device__ __forceinline__ void fft2_out_to_in(double2 (&v)[16]) {
     }
 }
 
+// p[r] = s^r, r < R (R in {2, 4, 8, 16}), from s, s^2, s^4, s^8 by binary
+// powers: at most three complex products (roundings) per entry.  Replaces R
+// table loads per thread by four -- the twiddle lookups were the largest
+// share of the shared-memory traffic (and of its bank conflicts).
+template <int R>
+__device__ __forceinline__ void pow_table(double2 s1, double2 s2, double2 s4, double2 s8,
+                                          double2 (&p)[R]) {
+    p[0] = make_double2(1.0, 0.0);
+    if constexpr (R > 1) p[1] = s1;
+    if constexpr (R > 2) {
+        p[2] = s2;
+        p[3] = cmul(s1, s2);
+    }
+    if constexpr (R > 4) {
+        p[4] = s4;
+        p[5] = cmul(s1, s4);
+        p[6] = cmul(s2, s4);
+        p[7] = cmul(p[3], s4);
+    }
+    if constexpr (R > 8) {
+        p[8] = s8;
+#pragma unroll
+        for (int r = 9; r < 16; ++r) p[r] = cmul(p[r - 8], s8);
+    }
+}
+
+__device__ __forceinline__ double2 conj_if_b(double2 w, bool c) {
+    if (c) w.y = -w.y;
+    return w;
+}
+
 template <int N, bool INV>
 __device__ __forceinline__ void fft2pass(double2 (&v)[16], double2* __restrict__ slot, int t,
                                          const double2* __restrict__ tw) {
@@ -236,21 +267,50 @@ __device__ __forceinline__ void fft2pass(double2 (&v)[16], double2* __restrict__
         double2 u[R2];
 #pragma unroll
         for (int r = 0; r < R2; ++r) u[r] = slot[pad16(j + 16 * r)];
+        // twiddles e^{-+2 pi i jm r / N}, r < R2, from the powers of tw[jm]
+        // (jm = 0 gives exact ones: the products of (1, 0) are exact)
         const int jm = j & 15;
+        const double2 one = make_double2(1.0, 0.0);
+        const double2 s1 = conj_if_b(tw[jm], INV);
+        const double2 s2 = conj_if_b(tw[2 * jm], INV);
+        const double2 s4 = R2 > 4 ? conj_if_b(tw[4 * jm], INV) : one;
+        const double2 s8 = R2 > 8 ? conj_if_b(tw[8 * jm], INV) : one;
+        double2 p[R2];
+        pow_table<R2>(s1, s2, s4, s8, p);
 #pragma unroll
-        for (int r = 1; r < R2; ++r) {
-            const int m = jm * r;  // exponent of e^{-2 pi i / N}
-            if (m) {
-                double2 w = tw[m];
-                if (INV) w.y = -w.y;
-                u[r] = cmul(u[r], w);
-            }
-        }
+        for (int r = 1; r < R2; ++r) u[r] = cmul(u[r], p[r]);
         dft_reg<R2, INV>(u);
 #pragma unroll
         for (int r = 0; r < R2; ++r) v[q * R2 + r] = u[r];
     }
     __syncthreads();
+}
+
+// Four-step twiddle of pass outputs: v[e] *= w^(a * fft2_out_index<N>(t, e)),
+// w = e^{-+2 pi i / NT} from the two-level tables of the full length NT.
+// Per output group g the base w^(a (t + g T)) times (w^(16 a))^r, the powers
+// by pow_table: 5-6 table lookups per thread instead of 16 pairs.
+template <int N, bool INV>
+__device__ __forceinline__ void out_twiddle(double2 (&v)[16], int a, int t,
+                                            const double2* __restrict__ hi,
+                                            const double2* __restrict__ lo) {
+    constexpr int R2 = N / 16, T = N / 16, BPT = 16 / R2;
+    if (a == 0) return;  // every exponent is 0
+    const double2 one = make_double2(1.0, 0.0);
+    const double2 s1 = twiddle2<INV>(hi, lo, 16 * a);
+    const double2 s2 = twiddle2<INV>(hi, lo, 32 * a);
+    const double2 s4 = R2 > 4 ? twiddle2<INV>(hi, lo, 64 * a) : one;
+    const double2 s8 = R2 > 8 ? twiddle2<INV>(hi, lo, 128 * a) : one;
+    double2 p[R2];
+    pow_table<R2>(s1, s2, s4, s8, p);
+#pragma unroll
+    for (int g = 0; g < BPT; ++g) {
+        const int e0 = a * (t + g * T);
+        const double2 b = twiddle2<INV>(hi, lo, e0);  // e0 == 0: exactly (1, 0)
+        v[g * R2] = cmul(v[g * R2], b);
+#pragma unroll
+        for (int r = 1; r < R2; ++r) v[g * R2 + r] = cmul(v[g * R2 + r], cmul(b, p[r]));
+    }
 }
 
 }  // namespace sfftb
