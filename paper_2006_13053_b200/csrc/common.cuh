@@ -53,6 +53,24 @@ inline int num_sms() {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// u mod M for u < 2^62 (M < 2^31): the FP64 quotient estimate is off by at
+// most a few units, fixed up exactly in integers -- no 64-bit division.
+__device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t M, double invM) {
+    int64_t q = (int64_t)((double)u * invM);
+    int64_t r = (int64_t)u - q * (int64_t)M;
+    while (r < 0) r += M;
+    while (r >= (int64_t)M) r -= M;
+    return (uint64_t)r;
+}
+
+// x mod M in [0, M) for any int64 x, skipping the division when |x| < M.
+__device__ __forceinline__ int64_t reduce_mod(int64_t x, int64_t M) {
+    if (x >= 0 && x < M) return x;
+    if (x < 0 && x > -M) return x + M;
+    x %= M;
+    return x < 0 ? x + M : x;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel)
 // and size: launch paths call this every time, the driver call is skipped
 // when an equal or larger opt-in is already recorded.

@@ -92,14 +92,6 @@ __device__ __forceinline__ uint32_t probe_bit(uint32_t base, uint32_t r) {
     return __funnelshift_r(w, w, r) & 1u;
 }
 
-__device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t M, double invM) {
-    // u < 2^62: the double estimate is off by at most a few units
-    int64_t q = (int64_t)((double)u * invM);
-    int64_t r = (int64_t)u - q * (int64_t)M;
-    while (r < 0) r += M;
-    while (r >= (int64_t)M) r -= M;
-    return (uint64_t)r;
-}
 
 // Synchronous cooperative copy (generic fallback kernel only).
 __device__ __forceinline__ void load_bits(uint32_t* dst, const HashArgs& a, int g, int l0,
@@ -375,6 +367,7 @@ __global__ void nonzero_bitmap_kernel(const double2* __restrict__ ghat, int64_t 
 
 static constexpr int kCompactWordsPerBlock = 4096;
 static constexpr int kCompactThreads = 256;
+static constexpr int64_t kCompactSingleWords = 16384;
 
 __global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
                               int64_t nblk, int64_t* __restrict__ blocksum) {
@@ -406,21 +399,24 @@ __global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts) {
     counts[g] = run;
 }
 
+// SINGLE: one CTA per group walks all words with a running carry and writes
+// counts[g] itself -- one launch instead of count/scan/write for the small
+// masks of the sfft stages (nwords <= kCompactSingleWords).
+template <bool SINGLE>
 __global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords, int64_t n,
                               int64_t nblk, const int64_t* __restrict__ blocksum,
-                              int64_t* __restrict__ idx) {
+                              int64_t* __restrict__ idx, int64_t* __restrict__ counts) {
     const int g = blockIdx.y;
-    const int64_t w0 = blockIdx.x * (int64_t)kCompactWordsPerBlock;
+    const int64_t w0 = SINGLE ? 0 : blockIdx.x * (int64_t)kCompactWordsPerBlock;
+    const int64_t wend = SINGLE ? nwords : min(nwords, w0 + kCompactWordsPerBlock);
     __shared__ int64_t warp_tot[kCompactThreads / 32];
     __shared__ int64_t carry;
-    if (threadIdx.x == 0) carry = blocksum[(int64_t)g * nblk + blockIdx.x];
+    if (threadIdx.x == 0) carry = SINGLE ? 0 : blocksum[(int64_t)g * nblk + blockIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t c0 = w0; c0 < min(nwords, w0 + kCompactWordsPerBlock); c0 += blockDim.x) {
+    for (int64_t c0 = w0; c0 < wend; c0 += blockDim.x) {
         const int64_t w = c0 + threadIdx.x;
-        const uint32_t bitsw = (w < nwords && w < w0 + kCompactWordsPerBlock)
-                                   ? mask[(int64_t)g * nwords + w]
-                                   : 0u;
+        const uint32_t bitsw = w < wend ? mask[(int64_t)g * nwords + w] : 0u;
         int cnt = __popc(bitsw);
         int incl = cnt;
 #pragma unroll
@@ -448,6 +444,7 @@ __global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords,
         }
         __syncthreads();
     }
+    if (SINGLE && threadIdx.x == 0) counts[g] = carry;
 }
 
 // ---------------------------------------------------------------------------
@@ -458,18 +455,13 @@ __device__ __forceinline__ int64_t residue_exact(const int64_t* row, const int64
                                                  int64_t M) {
     // sum_j (row_j mod M)(z_j mod M) < d (M-1)^2 < 2^62 (the caller's bound,
     // detect.py:128-129), so one 64-bit accumulation and a final mod suffice
+    // (the 64-bit divisions are skipped for entries already in (-M, M), the
+    // common case, and the final reduction uses the FP64 quotient estimate)
     uint64_t acc = 0;
     for (int j = 0; j < d; ++j) {
-        int64_t e = row[j] % M;
-        if (e < 0) e += M;
-        int64_t zz = z[j];
-        if (zz < 0 || zz >= M) {
-            zz %= M;
-            if (zz < 0) zz += M;
-        }
-        acc += (uint64_t)e * (uint64_t)zz;
+        acc += (uint64_t)reduce_mod(row[j], M) * (uint64_t)reduce_mod(z[j], M);
     }
-    return (int64_t)(acc % (uint64_t)M);
+    return (int64_t)mod_u64(acc, (uint64_t)M, 1.0 / (double)M);
 }
 
 template <int S>
@@ -484,9 +476,15 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int target = L >> 1;
-    for (int g = 0; g < G; ++g) {
-        const int64_t cnt = counts[g];
-        for (int64_t k = gwarp; k < cnt; k += nwarps) {
+    // one flat work list over the groups' detected rows (g, k), so small
+    // groups do not serialise one latency-bound round per group
+    int64_t total = 0;
+    for (int g = 0; g < G; ++g) total += counts[g];
+    for (int64_t w = gwarp; w < total; w += nwarps) {
+        int g = 0;
+        int64_t k = w;
+        while (k >= counts[g]) k -= counts[g++];
+        {
             const int64_t row = idx[(int64_t)g * cap + k];
             double re[S], im[S];
 #pragma unroll
@@ -572,40 +570,31 @@ __global__ void sumsq_kernel(const double2* __restrict__ x, int64_t stride, int6
 
 // One warp per group: lane l owns rms of lattices l, l+32, ...; the median
 // is found by stable ranking (L <= 256).
+// One CTA per group: the L per-lattice RMS values in shared memory, each
+// thread ranks its values against all L (stable rank: #{v_j < v_i} +
+// #{j < i : v_j == v_i}), the holders of ranks (L-1)/2 and L/2 publish them.
 __global__ void zero_threshold_kernel(const double* __restrict__ sumsq, int G, int L, int64_t M,
                                       double* __restrict__ theta) {
-    const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (g >= G) return;
-    double v[8];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        const int l = lane + 32 * s;
-        v[s] = l < L ? sqrt(sumsq[(int64_t)g * L + l] / (double)M) : 0.0;
-    }
+    extern __shared__ double zt_v[];
+    __shared__ double mids[2];
+    const int g = blockIdx.x;
+    for (int l = threadIdx.x; l < L; l += blockDim.x)
+        zt_v[l] = sqrt(sumsq[(int64_t)g * L + l] / (double)M);
+    __syncthreads();
     const int lo = (L - 1) / 2, hi = L / 2;  // middle pair (equal when L is odd)
-    double a = 0.0, b = 0.0;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        const int i = lane + 32 * s;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const double vi = zt_v[i];
         int rank = 0;
-        for (int so = 0; so < 8; ++so) {
-            if (32 * so >= L) break;
-            for (int src = 0; src < 32; ++src) {
-                const double o = __shfl_sync(0xffffffffu, v[so], src);
-                const int j = src + 32 * so;
-                rank += (j < L) && ((o < v[s]) || (o == v[s] && j < i));
-            }
+        for (int j = 0; j < L; ++j) {
+            const double o = zt_v[j];
+            rank += (o < vi) || (o == vi && j < i);
         }
-        if (i < L && rank == lo) a = v[s];
-        if (i < L && rank == hi) b = v[s];
+        if (rank == lo) mids[0] = vi;
+        if (rank == hi) mids[1] = vi;
     }
-    for (int o = 16; o > 0; o >>= 1) {  // exactly one lane holds each value
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    if (lane == 0) {
-        const double mid = (L % 2 == 1) ? a : 0.5 * (a + b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double mid = (L % 2 == 1) ? mids[0] : 0.5 * (mids[0] + mids[1]);
         theta[g] = fmax(1e-12, 1e-10 * mid);
     }
 }
@@ -862,13 +851,19 @@ extern "C" int sfftb_compact_mask(const uint32_t* mask, int64_t G, int64_t n, in
     const int64_t nwords = (n + 31) / 32;
     const int64_t nblk = std::max<int64_t>(1, ceil_div(nwords, kCompactWordsPerBlock));
     int64_t* bs = (int64_t*)ws;
+    if (nwords <= kCompactSingleWords) {
+        compact_write<true><<<dim3(1, (unsigned)G), kCompactThreads, 0, st>>>(
+            mask, nwords, n, 1, nullptr, idx, counts);
+        SFFTB_CHECK_LAUNCH();
+        return SFFTB_OK;
+    }
     compact_count<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(mask, nwords,
                                                                                  nblk, bs);
     SFFTB_CHECK_LAUNCH();
     compact_scan<<<(unsigned)G, 32, 0, st>>>(bs, nblk, counts);
     SFFTB_CHECK_LAUNCH();
-    compact_write<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(
-        mask, nwords, n, nblk, bs, idx);
+    compact_write<false><<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(
+        mask, nwords, n, nblk, bs, idx, counts);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
@@ -919,8 +914,10 @@ extern "C" int sfftb_sumsq(const double* x, int64_t stride, int64_t batch, int64
 extern "C" int sfftb_zero_thresholds(const double* sumsq, int64_t G, int64_t L, int64_t M,
                                      double* theta, void* stream) {
     SFFTB_REQUIRE(L >= 1 && L <= 256, "zero test: 1 <= L <= 256");
-    zero_threshold_kernel<<<(unsigned)ceil_div(G, 4), 128, 0, (cudaStream_t)stream>>>(
-        sumsq, (int)G, (int)L, M, theta);
+    const size_t zsm = sizeof(double) * (size_t)L;
+    SFFTB_CUDA(smem_opt_in(zero_threshold_kernel, zsm));
+    zero_threshold_kernel<<<(unsigned)G, 128, zsm, (cudaStream_t)stream>>>(sumsq, (int)G, (int)L,
+                                                                         M, theta);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }

@@ -41,10 +41,6 @@ __global__ void anchor_kernel(const int64_t* __restrict__ support, int64_t s, in
     }
 }
 
-__device__ __forceinline__ uint64_t mulmod_u64(uint64_t a, uint64_t b, uint64_t M) {
-    return (uint64_t)(((unsigned __int128)a * b) % M);
-}
-
 // One CTA per lattice; bins summed in ascending coefficient order.
 __global__ void __launch_bounds__(kScatterThreads)
     scatter_kernel(const int64_t* __restrict__ support, int64_t s, int d, int t_dim,
@@ -54,6 +50,7 @@ __global__ void __launch_bounds__(kScatterThreads)
     __shared__ uint64_t zs[64];
     const int64_t lat = blockIdx.x;
     const int64_t g = lat / L;
+    const double invM = 1.0 / (double)M;
     for (int j = threadIdx.x; j < t_dim; j += blockDim.x) {
         int64_t z = zmat[lat * t_dim + j] % M;
         zs[j] = (uint64_t)(z < 0 ? z + M : z);
@@ -70,12 +67,9 @@ __global__ void __launch_bounds__(kScatterThreads)
             uint64_t key = ~0ull;
             if (i < cnt) {
                 const int64_t* row = support + (c0 + i) * d;
-                uint64_t r = 0;
-                for (int j = 0; j < t_dim; ++j) {
-                    int64_t e = row[j] % M;
-                    if (e < 0) e += M;
-                    r = (r + mulmod_u64((uint64_t)e, zs[j], (uint64_t)M)) % (uint64_t)M;
-                }
+                uint64_t r = 0;  // r + e z < M + M^2 < 2^62
+                for (int j = 0; j < t_dim; ++j)
+                    r = mod_u64(r + (uint64_t)reduce_mod(row[j], M) * zs[j], (uint64_t)M, invM);
                 key = (r << 32) | (uint64_t)i;
             }
             keys[i] = key;
