@@ -256,6 +256,24 @@ int sfftb_add_noise(double *x, int64_t rows, int64_t M, uint64_t seed,
 int sfftb_injective_mod_dev(const int64_t *elems, int64_t n, int64_t d,
                             int64_t p, int *injective, void *stream);
 
+/*
+ * K9 rank-1-lattice refinement (postprocess_r1l, detect.py:198-228) of n
+ * detected rows (rows (n, d) int64): lattice l has generator zmat[l] and
+ * size offs[l+1] - offs[l] (offs: L+1 prefix sums on the device, Msum =
+ * offs[L]); vals (L, n) complex128 are the per-lattice estimates
+ * ghat_l[r_l(row)] (lattice-major), medians (n) the median estimates.
+ * refined[i] = mean of vals[l, i] over the lattices where row i's residue is
+ * unique among the n rows (lattice order; numpy's complex/int division), else
+ * medians[i]; keep bit i = |refined[i]| > theta0.
+ * ws: sfftb_r1l_workspace_bytes(n, L, Msum).
+ */
+int64_t sfftb_r1l_workspace_bytes(int64_t n, int64_t L, int64_t Msum);
+int sfftb_postprocess_r1l(const int64_t *rows, int64_t n, int64_t d,
+                          const int64_t *zmat, const int64_t *offs, int64_t L,
+                          int64_t Msum, const double *vals, const double *medians,
+                          double theta0, double *refined, uint32_t *keep,
+                          void *ws, void *stream);
+
 /* ---------------------------------------------------------------------
  * One dimension-incremental detection stage (dimincr.py:178-192 + the union
  * of :239-240) as ONE host call: the r iterations of coordinate t share M and

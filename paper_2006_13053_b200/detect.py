@@ -272,8 +272,8 @@ def detect_topk(samples, config, gamma, s_tilde, theta, zero=None):
     return DetectionResult(res.candidates, res._hits, kidx[:k], kco[:k], res.theta_zero)
 
 
-def per_lattice_coefficients(samples, config, gamma):
-    """(n, L) per-lattice estimates ghat_l[r_l(k)] (detect.py:112-119)."""
+def _per_lattice_values_dev(samples, config, gamma):
+    """(L, n) complex128 device tensor of ghat_l[r_l(k)] (detect.py:112-119)."""
     t = _stack_samples(samples, config)
     n, L = len(gamma), config.L
     out = _dev.empty((L, max(n, 1)), torch.complex128)
@@ -282,9 +282,10 @@ def per_lattice_coefficients(samples, config, gamma):
         for col, (s, lat) in enumerate(zip(t, config.lattices)):
             g = dft_batch(s, lat.M)
             z = _dev.upload(lat.z.reshape(1, -1))
-            _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z), 1,
-                         lat.M, _dev.ptr(g), None, n, _dev.ptr(out[col]), _dev.stream())
-        return _dev.download(out[:, :n].T.contiguous())
+            if n:
+                _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z), 1,
+                             lat.M, _dev.ptr(g), None, n, _dev.ptr(out[col]), _dev.stream())
+        return out
     M = config.shared_M
     g = dft_batch(t, M)
     z = config.zmat_device()
@@ -292,36 +293,57 @@ def per_lattice_coefficients(samples, config, gamma):
         if n:
             _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z[col]), 1,
                          M, _dev.ptr(g[col]), None, n, _dev.ptr(out[col]), _dev.stream())
-    return _dev.download(out[:, :n].T.contiguous())
+    return out
+
+
+def per_lattice_coefficients(samples, config, gamma):
+    """(n, L) per-lattice estimates ghat_l[r_l(k)] (detect.py:112-119)."""
+    n = len(gamma)
+    return _dev.download(_per_lattice_values_dev(samples, config, gamma)[:, :n].T.contiguous())
 
 
 def postprocess_r1l(result, samples, config, zero=None):
     """Average the estimates of lattices on which a detected frequency's
     residue is unique within the detected set; keep the median otherwise;
-    drop |value| <= theta_zero (detect.py:198-228)."""
+    drop |value| <= theta_zero (detect.py:198-228).  One K9 call
+    (csrc/postprocess.cu) plus the compaction of the kept rows."""
     if zero is None:
         zero = ZeroTest(result.theta_zero)
     n = len(result.detected)
     if n == 0:
         return result
-    vals = torch.as_tensor(per_lattice_coefficients(samples, config, result.detected),
-                           device=_dev.device())
+    L = config.L
+    vals = _per_lattice_values_dev(samples, config, result.detected)
+    if vals.shape[1] != n:
+        vals = vals[:, :n].contiguous()
     rows = result.detected.device()
-    refined = _dev.as_c128(result.coeffs).clone()
-    cnt = torch.zeros((n,), dtype=torch.int64, device=_dev.device())
-    acc = torch.zeros((n,), dtype=torch.complex128, device=_dev.device())
-    for col, lat in enumerate(config.lattices):
-        z = torch.as_tensor(lat.z, device=_dev.device())
-        res = ((rows % lat.M) * z).sum(dim=1) % lat.M
-        uniq = torch.bincount(res, minlength=lat.M)[res] == 1
-        cnt += uniq
-        acc[uniq] += vals[uniq, col]
-    has = cnt > 0
-    refined[has] = acc[has] / cnt[has]
-    keep = torch.abs(refined) > zero.theta_zero
-    idx = _dev.as_i64(result.detected_idx)[keep]
-    return DetectionResult(result.candidates, result._hits, idx, refined[keep],
-                           result.theta_zero)
+    Ms = np.array([lat.M for lat in config.lattices], dtype=np.int64)
+    offs_h = np.concatenate([[0], np.cumsum(Ms)]).astype(np.int64)
+    offs = _dev.upload(offs_h)
+    med = _dev.as_c128(result.coeffs).contiguous()
+    refined = _dev.empty((n,), torch.complex128)
+    keep = _dev.empty(((n + 31) // 32,), torch.int32)
+    lib = _native.lib()
+    ws = _dev.workspace(lib.sfftb_r1l_workspace_bytes(n, L, int(offs_h[-1])))
+    _native.call("sfftb_postprocess_r1l", _dev.ptr(rows), n, result.detected.dim,
+                 _dev.ptr(config.zmat_device()), _dev.ptr(offs), L, int(offs_h[-1]),
+                 _dev.ptr(vals), _dev.ptr(med), float(zero.theta_zero), _dev.ptr(refined),
+                 _dev.ptr(keep), _dev.ptr(ws), _dev.stream())
+    pos = _dev.empty((n,), torch.int64)
+    cnt = _dev.zeros((1,), torch.int64)
+    cws = _dev.workspace(lib.sfftb_compact_workspace_bytes(1, n))
+    _native.call("sfftb_compact_mask", _dev.ptr(keep), 1, n, _dev.ptr(pos), _dev.ptr(cnt),
+                 _dev.ptr(cws), _dev.stream())
+    k = int(_dev.download(cnt)[0])
+    det = _dev.as_i64(result.detected_idx).contiguous()
+    idx = _dev.empty((max(k, 1),), torch.int64)
+    co = _dev.empty((max(k, 1),), torch.complex128)
+    if k:
+        _native.call("sfftb_gather_rows", _dev.ptr(det), 1, _dev.ptr(pos), _dev.ptr(cnt), k,
+                     _dev.ptr(idx), _dev.stream())
+        _native.call("sfftb_gather_rows", _dev.ptr(refined.view(torch.int64).view(n, 2)), 2,
+                     _dev.ptr(pos), _dev.ptr(cnt), k, _dev.ptr(co), _dev.stream())
+    return DetectionResult(result.candidates, result._hits, idx[:k], co[:k], result.theta_zero)
 
 
 def format_detection(result):

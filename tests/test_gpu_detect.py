@@ -166,3 +166,31 @@ def test_per_lattice_coefficients(cuda):
     got = np.zeros(len(S), complex)
     got[g["t0_idx"]] = g["t0_coeffs"]
     assert np.max(np.abs(med[g["t0_idx"]] - g["t0_coeffs"])) < 1e-10
+
+
+@pytest.mark.parametrize("M,L,n,s", [(211, 9, 3000, 40), (1031, 7, 4000, 300), (97, 5, 500, 60)])
+def test_postprocess_r1l_kernel_vs_oracle(cuda, oracle_lib, M, L, n, s):
+    """K9 on crowded residues (many collisions, rows with and without a
+    collision-free lattice, kept and dropped rows) against the numpy
+    restatement: identical kept indices, refined values to roundoff."""
+    pkg, port = cuda, oracle_lib
+    rng = np.random.default_rng(M * 7 + L)
+    d = 3
+    gamma = np.unique(rng.integers(-40, 41, size=(n, d)), axis=0)
+    S = pkg.FreqSet(d, gamma, _sorted=True)
+    sup = np.sort(rng.choice(len(gamma), size=s, replace=False))
+    coeffs = rng.normal(size=s) + 1j * rng.normal(size=s)
+    coeffs[: s // 4] *= 1e-13  # some refine below the zero threshold
+    zmat = rng.integers(0, M, size=(L, d))
+    cfg = _config(pkg, zmat, M)
+    p = pkg.SparsePoly(S.take(sup), coeffs)
+    orc = pkg.oracle_from_poly(p)
+    smp = [orc.sample_lattice(lat) for lat in cfg.lattices]
+    res = pkg.detect_and_compute(smp, cfg, S)
+    post = pkg.postprocess_r1l(res, smp, cfg)
+    want_idx, want_co = port.postprocess_r1l(gamma[res.detected_idx], res.coeffs,
+                                             res.detected_idx, smp, M, zmat, res.theta_zero)
+    assert len(res.detected_idx) > s // 2
+    assert np.array_equal(post.detected_idx, want_idx)
+    assert np.max(np.abs(post.coeffs - want_co), initial=0.0) <= 1e-13 * max(
+        1.0, np.max(np.abs(want_co), initial=0.0))
