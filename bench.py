@@ -261,26 +261,22 @@ def run_sfft_arm(args, world, rank):
 
 
 def device_gamma(n, d, N, seed):
-    """2^26-scale candidate set generated in HBM: uniform rows of
-    [-N, N]^d, lexicographically sorted, duplicate-free (seeded)."""
+    """2^26-scale candidate set generated in HBM by the package's own
+    kernels: uniform rows of [-N, N]^d (Philox stream), canonicalised
+    (lexicographic radix sort + de-dup, csrc/canon.cu).  Returns (FreqSet,
+    generation ms)."""
     import torch
 
-    g = torch.Generator(device="cuda")
-    g.manual_seed(seed)
-    rows = torch.randint(-N, N + 1, (n, d), generator=g, device="cuda", dtype=torch.int64)
-    span = 2 * N + 1
-    # LSD lexicographic sort on packed keys of <= 4 coordinates (< 2^53)
-    groups = [list(range(i, min(i + 4, d))) for i in range(0, d, 4)]
-    for grp in reversed(groups):
-        key = torch.zeros(n, dtype=torch.int64, device="cuda")
-        for j in grp:
-            key = key * span + (rows[:, j] + N)
-        order = torch.sort(key, stable=True).indices
-        rows = rows.index_select(0, order)
-        del key, order
-    dup = (rows[1:] == rows[:-1]).all(dim=1).any()
-    assert not bool(dup), "duplicate rows drawn (probability ~1e-23): change the seed"
-    return rows.contiguous()
+    import paper_2006_13053_b200 as pkg
+
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    G = pkg.random_box_device(pkg.Box(d, -N, N), n, seed)
+    b.record()
+    torch.cuda.synchronize()
+    return G, a.elapsed_time(b)
 
 
 def run_hash_arm(args, world, rank):
@@ -291,8 +287,8 @@ def run_hash_arm(args, world, rank):
     from paper_2006_13053_b200 import _dev, _native
 
     n, d, N, s = args.hash_rows, 10, 4096, 10_000
-    rows = device_gamma(n, d, N, 4242 + rank)
-    G = pkg.FreqSet.from_device(d, rows)
+    G, gen_ms = device_gamma(n, d, N, 4242 + rank)
+    rows = G.device()
     G.memo("bounds", lambda: np.array([[-N, N]] * d, dtype=np.int64))  # known by construction
     rng = np.random.default_rng(2026 + rank)
     sup_idx = np.sort(rng.choice(n, size=s, replace=False))
@@ -373,7 +369,7 @@ def run_hash_arm(args, world, rank):
             "ms": max_over_ranks(statistics.mean(times), world),
             "hash_ms": max_over_ranks(statistics.mean(hash_ms), world),
             "path_ms": max_over_ranks(statistics.mean(path_ms), world),
-            "clocks": clocks, "parity": parity,
+            "clocks": clocks, "parity": parity, "gamma_generation_ms": gen_ms,
             "e2e_ms": max_over_ranks(statistics.mean(e2e), world), "h2d": n * d * 8,
             "d2h": d2h, "rows_host_sample": rows_h[:1 << 20], "ghat": ghat,
             "zmat": cfg.zmat(), "theta0": res.theta_zero}
@@ -591,6 +587,9 @@ def main():
                 (h["n"] * 8 * h["d"] + h["n"] * 8 + h["L"] * h["M"] * 16 + h["n_det"] * 24)
                 / (h["path_ms"] * 1e-3) / 1e9, 1),
             "parity": h["parity"], "clocks": h["clocks"],
+            "gamma_generation_ms": round(h["gamma_generation_ms"], 2),
+            "gamma_generation_note": "device Philox rows + canonicalisation (csrc/canon.cu); "
+                                     "reference host Gamma generation 432.6 s (SURVEY 8(d))",
             "e2e": {"value": round(h["n"] / (h["e2e_ms"] * 1e-3), 1), "unit": "candidates/s",
                     "ms": round(h["e2e_ms"], 2), "h2d_bytes_per_step": h["h2d"],
                     "d2h_bytes_per_step": h["d2h"]},

@@ -274,6 +274,25 @@ int sfftb_postprocess_r1l(const int64_t *rows, int64_t n, int64_t d,
                           double theta0, double *refined, uint32_t *keep,
                           void *ws, void *stream);
 
+/*
+ * Device canonicalisation of a candidate set (FreqSet, freqset.py:48-67):
+ * rows (n, d) int64 in any order, with duplicates -> out (first *count rows,
+ * *count on the device) lexicographically sorted and duplicate-free.
+ * Synchronises the stream once per key group (the packing plan needs the
+ * per-coordinate spans).  ws: sfftb_canonicalize_workspace_bytes(n, d).
+ */
+int64_t sfftb_canonicalize_workspace_bytes(int64_t n, int64_t d);
+int sfftb_canonicalize_rows(const int64_t *rows, int64_t n, int64_t d,
+                            int64_t *out, int64_t *count, void *ws, void *stream);
+
+/*
+ * Seeded synthetic candidate rows: out (n, d) uniform on [lo, hi]^d from a
+ * counter-based Philox4x32-10 stream (entry e = i*d + j, key = seed).  Not
+ * numpy's stream: the reference-identical _random_from_box stays on the host.
+ */
+int sfftb_random_box_rows(int64_t n, int64_t d, int64_t lo, int64_t hi,
+                          uint64_t seed, int64_t *out, void *stream);
+
 /* ---------------------------------------------------------------------
  * One dimension-incremental detection stage (dimincr.py:178-192 + the union
  * of :239-240) as ONE host call: the r iterations of coordinate t share M and

@@ -65,6 +65,9 @@ _SIGS = {
     "sfftb_add_noise": (_int, [_p, _i64, _i64, _u64, _i64, _dbl, _p]),
     "sfftb_injective_mod_dev": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int), _p]),
     "sfftb_sfft_stage": (_int, [_p, _p]),
+    "sfftb_canonicalize_workspace_bytes": (_i64, [_i64, _i64]),
+    "sfftb_canonicalize_rows": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
+    "sfftb_random_box_rows": (_int, [_i64, _i64, _i64, _i64, _u64, _p, _p]),
     "sfftb_r1l_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "sfftb_postprocess_r1l": (_int, [_p, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _dbl, _p, _p,
                                      _p, _p]),

@@ -222,3 +222,43 @@ def test_fused_sample_detect_matches_unfused(cuda, M, G, L, sigma):
     assert np.array_equal(_dev.download(bits_f), _dev.download(bits_u))
     if sigma == 0:
         assert np.max(np.abs(_dev.download(ghat_f) - bins)) < 1e-12
+
+
+@pytest.mark.parametrize("case", ["dups_small_box", "wide_multi_group", "extremes", "tiny"])
+def test_device_canonicalisation_matches_host(cuda, case):
+    """csrc/canon.cu sort + de-dup == the host canonical() (freqset.py:48-67)."""
+    import torch
+
+    pkg = cuda
+    from paper_2006_13053_b200 import _dev
+    from paper_2006_13053_b200.freqset import canonical
+
+    rng = np.random.default_rng(len(case))
+    if case == "dups_small_box":
+        rows = rng.integers(-3, 4, size=(100_003, 4))
+    elif case == "wide_multi_group":  # 10 x 21-bit spans: four 64-bit key groups
+        rows = rng.integers(-(1 << 20), 1 << 20, size=(300_001, 10))
+        rows = np.vstack([rows, rows[:5000]])  # exact duplicates across the set
+    elif case == "extremes":
+        rows = rng.integers(-(1 << 62), 1 << 62, size=(20_000, 3))
+        rows[:, 1] = 7  # a constant coordinate
+        rows = np.vstack([rows, rows[::3]])
+    else:
+        rows = np.array([[5, -1], [5, -1], [-2, 3]])
+    got = _dev.download(pkg.canonicalize_device(_dev.upload(rows), rows.shape[1]))
+    assert np.array_equal(got, canonical(np.ascontiguousarray(rows)))
+    S = pkg.FreqSet.from_device(rows.shape[1], _dev.upload(rows), canonical=False)
+    assert len(S) == got.shape[0]
+
+
+def test_random_box_device(cuda):
+    pkg = cuda
+    box = pkg.Box(3, -2, 2)  # 125 points: forces re-draws and a random drop
+    S = pkg.random_box_device(box, 100, seed=5)
+    e = S.elems
+    assert e.shape == (100, 3) and np.all(e >= -2) and np.all(e <= 2)
+    assert np.array_equal(e, np.unique(e, axis=0))
+    big = pkg.random_box_device(pkg.Box(10, -4096, 4096), 1 << 16, seed=9)
+    assert len(big) == 1 << 16
+    b = big.elems
+    assert np.array_equal(b, np.unique(b, axis=0)) and b.min() >= -4096 and b.max() <= 4096
