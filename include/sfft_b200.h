@@ -363,6 +363,9 @@ typedef struct {
     /* optional: 7 cudaEvent_t recorded at the phase boundaries (candidates |
      * sampler | transforms | hashing | compaction+medians | top-s+union) */
     void *const *events;
+    /* elements between consecutive groups in zmat_host (0: dense G*L*tdim);
+     * lets the host pre-draw L_cap >= L generators per group before L is known */
+    int64_t zmat_host_ld;
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);

@@ -11,6 +11,7 @@ because stage t+1 gathers its prefix from stage t's J).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import torch
 
@@ -36,7 +37,7 @@ class StageDesc(ctypes.Structure):
         ("sumsq", _p), ("bits", _p), ("ws_dft", _p), ("detmask", _p), ("idx", _p),
         ("counts", _p), ("med", _p), ("ws_compact", _p), ("kidx", _p), ("kco", _p),
         ("kcounts", _p), ("ws_topk", _p), ("umask", _p), ("uidx", _p), ("ucount", _p),
-        ("host_counts", _p), ("events", _p),
+        ("host_counts", _p), ("events", _p), ("zmat_host_ld", _i64),
     ]
 
 
@@ -71,6 +72,24 @@ class Arena:
 
     def bytes(self, name, nbytes):
         return self.ptr(name, (int(nbytes) + 7) // 8)
+
+
+_LOCAL = threading.local()
+
+
+def arena():
+    """The calling thread's stage arena, kept across reconstructions (like a
+    cached FFT plan): a repeated sfft allocates nothing.  Nothing returned to
+    the caller aliases it -- results are copied to the host before sfft
+    returns.  ``release()`` frees it."""
+    a = getattr(_LOCAL, "arena", None)
+    if a is None:
+        a = _LOCAL.arena = Arena()
+    return a
+
+
+def release():
+    _LOCAL.arena = None
 
 
 def run(desc):
@@ -133,17 +152,18 @@ def buffers(A, desc, G, L, M, n, s, fused, slot):
     uidx = A.get(f"uidx{slot}", cap)
     ucount = A.get(f"ucount{slot}", 1)
     desc.uidx, desc.ucount = uidx.data_ptr(), ucount.data_ptr()
-    hc = A.get("host_counts", G + 1, torch.int64, pinned=True)
+    hc = A.get(f"host_counts{slot}", G + 1, torch.int64, pinned=True)
     desc.host_counts = hc.data_ptr()
     return kidx, kco, uidx, ucount, hc
 
 
-def host_inputs(A, zs, tails, tail_w):
-    """Copy generators/tails into pinned staging buffers; returns the tensors."""
+def host_inputs(A, zs, tails, tail_w, slot=0):
+    """Copy generators/tails into pinned staging buffers (one pair per slot,
+    so the next stage's draws never overwrite a pending copy)."""
     G, L, tdim = zs.shape
-    zh = A.get("zmat_host", G * L * tdim, torch.int64, pinned=True)
+    zh = A.get(f"zmat_host{slot}", G * L * tdim, torch.int64, pinned=True)
     zh.numpy()[:] = zs.reshape(-1)
-    th = A.get("tails_host", G * tail_w, torch.float64, pinned=True)
+    th = A.get(f"tails_host{slot}", G * tail_w, torch.float64, pinned=True)
     tn = th.numpy().reshape(G, tail_w)
     tn[:] = 0.0
     for g, tl in enumerate(tails):

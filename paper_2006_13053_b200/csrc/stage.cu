@@ -41,8 +41,17 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
 
     // generators and tails drawn on the host
     SFFTB_TRY(mark(1));
-    SFFTB_CUDA(cudaMemcpyAsync(a->zmat, a->zmat_host, (size_t)(rows * tdim) * sizeof(int64_t),
-                               cudaMemcpyHostToDevice, st));
+    if (a->zmat_host_ld > 0 && a->zmat_host_ld != L * tdim) {
+        SFFTB_REQUIRE(a->zmat_host_ld >= L * tdim, "stage: zmat_host_ld < L*tdim");
+        SFFTB_CUDA(cudaMemcpy2DAsync(a->zmat, (size_t)(L * tdim) * sizeof(int64_t), a->zmat_host,
+                                     (size_t)a->zmat_host_ld * sizeof(int64_t),
+                                     (size_t)(L * tdim) * sizeof(int64_t), (size_t)G,
+                                     cudaMemcpyHostToDevice, st));
+    } else {
+        SFFTB_CUDA(cudaMemcpyAsync(a->zmat, a->zmat_host,
+                                   (size_t)(rows * tdim) * sizeof(int64_t),
+                                   cudaMemcpyHostToDevice, st));
+    }
     SFFTB_CUDA(cudaMemcpyAsync(a->tails, a->tails_host,
                                (size_t)(G * a->tail_w) * sizeof(double),
                                cudaMemcpyHostToDevice, st));
