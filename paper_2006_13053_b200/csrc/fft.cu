@@ -54,6 +54,19 @@ static int bluestein_log(int64_t M) {
     return lg;
 }
 
+// Convolution length: the smallest N >= 2M-1 among the powers of two (>= 256)
+// and, above the single-CTA sizes, the mixed-radix 192 * {128, 256} of the
+// register four-step kernels (N = 3 * 2^k: 25% fewer bytes per pass than the
+// next power of two for M in (8192, 12288] and (16384, 24576]).
+static int64_t bluestein_N(int64_t M) {
+    const int64_t pow2 = int64_t(1) << bluestein_log(M);
+    if (pow2 > (int64_t(1) << kSmallMaxLog)) {
+        for (int64_t c : {int64_t(24576), int64_t(49152)})
+            if (c >= 2 * M - 1 && c < pow2) return c;
+    }
+    return pow2;
+}
+
 // iterative radix-2 FFT in long double (plan construction only)
 static void host_fft_ld(std::vector<long double>& re, std::vector<long double>& im) {
     const size_t n = re.size();
@@ -88,15 +101,48 @@ static void host_fft_ld(std::vector<long double>& re, std::vector<long double>& 
     }
 }
 
+// B^ of a mixed-radix length N = 3 * 2^k: three decimated power-of-two FFTs
+// combined by one radix-3 step, all in long double.
+static void host_fft3_ld(std::vector<long double>& re, std::vector<long double>& im) {
+    const size_t n = re.size(), m = n / 3;
+    std::vector<long double> r[3], i[3];
+    for (int q = 0; q < 3; ++q) {
+        r[q].resize(m);
+        i[q].resize(m);
+        for (size_t j = 0; j < m; ++j) {
+            r[q][j] = re[3 * j + q];
+            i[q][j] = im[3 * j + q];
+        }
+        host_fft_ld(r[q], i[q]);
+    }
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (size_t k = 0; k < n; ++k) {
+        long double sr = 0.0L, si = 0.0L;
+        for (int q = 0; q < 3; ++q) {
+            const long double a = -2.0L * PI * (long double)((q * k) % n) / (long double)n;
+            const long double c = cosl(a), sn = sinl(a);
+            const long double xr = r[q][k % m], xi = i[q][k % m];
+            sr += xr * c - xi * sn;
+            si += xr * sn + xi * c;
+        }
+        re[k] = sr;
+        im[k] = si;
+    }
+}
+
 static int build_plan(int64_t M, BluesteinPlan** out) {
     SFFTB_REQUIRE(M >= 1, "DFT length must be >= 1");
     const int lg = bluestein_log(M);
     SFFTB_REQUIRE(lg <= kMaxLog, "DFT length too large for the Bluestein plan (M <= 524288)");
     BluesteinPlan* p = new BluesteinPlan();
     p->M = M;
-    p->logN = lg;
-    p->N = 1 << lg;
-    if (lg > kSmallMaxLog) {
+    p->N = (int)bluestein_N(M);
+    const bool mixed = (p->N & (p->N - 1)) != 0;
+    p->logN = mixed ? 0 : lg;
+    if (mixed) {
+        p->N1 = 192;
+        p->N2 = p->N / 192;
+    } else if (lg > kSmallMaxLog) {
         p->N1 = 1 << (lg / 2);
         p->N2 = 1 << (lg - lg / 2);
     }
@@ -133,7 +179,10 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
         long double a = -2.0L * PI * (64.0L * k) / N;
         thi[k] = make_double2((double)cosl(a), (double)sinl(a));
     }
-    host_fft_ld(br, bi);
+    if (mixed)
+        host_fft3_ld(br, bi);
+    else
+        host_fft_ld(br, bi);
     for (int k = 0; k < N; ++k) {
         int dst = k;
         if (p->N1) {  // B^[k2 + N2 k1] stored at [k2][k1]
@@ -527,6 +576,92 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB(DftArgs a, int N2) {
     }
 }
 
+// Row pass for the mixed-radix length N = 192 * N2 (N1 = 192 = 16 x 12):
+// forward 192-point FFT (radix 12 on 16 threads, one transpose, radix 16 on
+// 12 threads), x B^, inverse 192-point FFT (radix 16 on the same 12 threads
+// straight from registers, one transpose, radix 12 on 16 threads), four-step
+// twiddle.  Index maps: j = t + 16 r (t < 16, r < 12), k = s + 12 q
+// (s < 12, q < 16); w192^{jk} = w192^{ts} w16^{tq} w12^{rs}.
+// Per-row shared slots: 16 x 13 (pass-1 layout [t][s]) and 12 x 17 (inverse
+// layout [s][t]) in 212 double2 -- the +4 pad puts neighbouring rows in the
+// other half of the banks for the remapped middle pass.
+static constexpr int kR192Slot = 212;
+__global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2) {
+    constexpr int N1 = 192, F = 16;
+    extern __shared__ double2 smem[];
+    double2* tw1 = smem + F * kR192Slot;  // e^{-2 pi i m/192}
+    double2* lo = tw1 + N1;
+    double2* hi_s = lo + 64;
+    const int tid = threadIdx.x;
+    const int f = tid >> 4, t = tid & 15;
+    // middle passes: 192 (row, column) pairs on threads 0..191 (6 full warps)
+    const bool mid = tid < F * 12;
+    const int f2 = tid / 12, sc = tid % 12;
+    const int N = N1 * N2;
+    stage(tw1, a.tw_n1, N1);
+    stage(lo, a.tw_lo, 64);
+    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    double2* slot = smem + f * kR192Slot;
+    double2* slot2 = smem + f2 * kR192Slot;
+    const int per_b = N2 / F;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const int64_t b = tile / per_b;
+        const int kbase = (int)(tile % per_b) * F;
+        const int k2 = kbase + f;
+        double2* row = a.work + b * (int64_t)N + (int64_t)k2 * N1;
+        double2 x[12];
+#pragma unroll
+        for (int r = 0; r < 12; ++r) x[r] = row[t + 16 * r];
+        __syncthreads();  // previous tile done with the slots
+        // forward pass 1: radix 12 over r, twiddle w192^{t s} (powers of w^t)
+        dft12<false>(x);
+        {
+            const Pow16 p(tw1[t], tw1[2 * t], tw1[4 * t], tw1[8 * t]);
+#pragma unroll
+            for (int sI = 0; sI < 12; ++sI) slot[t * 13 + sI] = sI ? cmul(x[sI], p(sI)) : x[sI];
+        }
+        __syncthreads();
+        double2 u[16];
+        if (mid) {
+            // forward pass 2: radix 16 over t' for column sc of row f2
+#pragma unroll
+            for (int tp = 0; tp < 16; ++tp) u[tp] = slot2[tp * 13 + sc];
+            dft_reg<16, false>(u);  // u[q] = X[sc + 12 q]
+            const double2* bh = a.bhat + (int64_t)(kbase + f2) * N1;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) u[q] = cmul(u[q], __ldg(bh + sc + 12 * q));
+            // inverse pass A: radix 16 over q
+            dft_reg<16, true>(u);  // u[t'] = sum_q X w16^{-t' q}
+        }
+        __syncthreads();  // pass-2 loads done before the slots are rewritten
+        if (mid) {
+            // twiddle w192^{-t' s} from the powers of conj(w^s)
+            const Pow16 p(conj_if_b(tw1[sc], true), conj_if_b(tw1[2 * sc], true),
+                          conj_if_b(tw1[4 * sc], true), conj_if_b(tw1[8 * sc], true));
+#pragma unroll
+            for (int tp = 0; tp < 16; ++tp)
+                slot2[sc * 17 + tp] = tp ? cmul(u[tp], p(tp)) : u[tp];
+        }
+        __syncthreads();
+        // inverse pass B: radix 12 over s for t' = t
+#pragma unroll
+        for (int sI = 0; sI < 12; ++sI) x[sI] = slot[sI * 17 + t];
+        dft12<true>(x);  // x[r] = y[t + 16 r]
+        // four-step twiddle w^{-(t + 16 r) k2}: base w^{-t k2} x (w^{-16 k2})^r
+        if (k2) {
+            const Pow16 p(twiddle2<true>(hi, lo, 16 * k2), twiddle2<true>(hi, lo, 32 * k2),
+                          twiddle2<true>(hi, lo, 64 * k2), twiddle2<true>(hi, lo, 128 * k2));
+            const double2 base = twiddle2<true>(hi, lo, t * k2);
+            x[0] = cmul(x[0], base);
+#pragma unroll
+            for (int r = 1; r < 12; ++r) x[r] = cmul(x[r], cmul(base, p(r)));
+        }
+#pragma unroll
+        for (int r = 0; r < 12; ++r) row[t + 16 * r] = x[r];
+    }
+}
+
 template <int N2, bool INV>
 __global__ void __launch_bounds__(256, 2) fs2_colC(DftArgs a, int N1) {
     using Lay = Fs2Layout<N2>;
@@ -569,7 +704,7 @@ __global__ void __launch_bounds__(256, 2) fs2_colC(DftArgs a, int N1) {
 // four-step twiddle.  Samples never reach HBM.  colC_bits = detection colC
 // that also emits the nonzero bitmap (|ghat| > theta, _core.pyx:195).
 // ---------------------------------------------------------------------------
-template <int N2>
+template <int N2, bool NOISE>
 __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
     using Lay = Fs2Layout<N2>;
     constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
@@ -605,7 +740,7 @@ __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
                 const double2 w = __ldg(a.chirp + h);
                 double2 y = cmul(w, v[e]);
                 y.y = -y.y;  // sample: conj(w c), the M*ifft of the bins
-                if (a.noise_sigma > 0.0) {
+                if (NOISE) {
                     const double2 nz = harness_noise(a.noise_seed,
                                                      (uint64_t)(a.noise_call0 + b), h,
                                                      a.noise_sigma);
@@ -807,8 +942,23 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
     return SFFTB_OK;
 }
 
+static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
+    const size_t hi = a.hi_in_smem ? (size_t)(192 * N2 / 64) : 0;
+    const size_t sm = sizeof(double2) * (16 * kR192Slot + 192 + 64 + hi);
+    DftArgs c = a;
+    c.ntiles = (int64_t)(N2 / 16) * batch;
+    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    SFFTB_CUDA(allow_smem(fs2_rowB192, sm));
+    fs2_rowB192<<<grid, 256, sm, st>>>(c, N2);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
 template <int N1>
 static int fs2_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
+    if constexpr (N1 == 192) {
+        return fs2_rows192(a, batch, N2, st);
+    } else {
     using Lay = Fs2Layout<N1>;
     const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
     const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
@@ -819,6 +969,18 @@ static int fs2_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
     fs2_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
+    }
+}
+
+// the row pass for any supported N1 (128, 192, 256)
+static int fs2_rows_any(const DftArgs& a, int64_t batch, int N1, int N2, cudaStream_t st) {
+    if (N1 == 256) return fs2_rows<256>(a, batch, N2, st);
+    if (N1 == 192) return fs2_rows<192>(a, batch, N2, st);
+    return fs2_rows<128>(a, batch, N2, st);
+}
+
+static bool fs2_supported(const BluesteinPlan* p) {
+    return (p->N1 == 128 || p->N1 == 192 || p->N1 == 256) && (p->N2 == 128 || p->N2 == 256);
 }
 
 template <bool INV>
@@ -826,7 +988,7 @@ static int fs2_all(const BluesteinPlan* p, const DftArgs& a, int64_t batch, cuda
     int rc = p->N2 == 256 ? fs2_cols<256, INV>(a, batch, p->N1, st, true)
                           : fs2_cols<128, INV>(a, batch, p->N1, st, true);
     if (rc) return rc;
-    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    rc = fs2_rows_any(a, batch, p->N1, p->N2, st);
     if (rc) return rc;
     return p->N2 == 256 ? fs2_cols<256, INV>(a, batch, p->N1, st, false)
                         : fs2_cols<128, INV>(a, batch, p->N1, st, false);
@@ -843,9 +1005,9 @@ using namespace sfftb;
 
 extern "C" int64_t sfftb_dft_workspace_bytes(int64_t batch, int64_t M) {
     if (batch <= 0 || M <= 0) return 0;
-    const int lg = bluestein_log(M);
-    if (lg <= kSmallMaxLog) return 0;
-    return batch * (int64_t(1) << lg) * (int64_t)sizeof(double2);
+    const int64_t N = bluestein_N(M);
+    if (N <= (int64_t(1) << kSmallMaxLog)) return 0;
+    return batch * N * (int64_t)sizeof(double2);
 }
 
 extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y_stride,
@@ -853,7 +1015,7 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
                          void* stream) {
     SFFTB_REQUIRE(batch >= 0 && M >= 1, "dft: bad sizes");
     if (batch == 0) return SFFTB_OK;
-    SFFTB_REQUIRE(batch <= 65535 || bluestein_log(M) <= kSmallMaxLog,
+    SFFTB_REQUIRE(batch <= 65535 || bluestein_N(M) <= (int64_t(1) << kSmallMaxLog),
                   "dft: batch too large for one launch");
     BluesteinPlan* p = nullptr;
     int rc = get_plan(M, &p);
@@ -874,12 +1036,11 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
     a.tw_n2 = p->tw_n2;
     a.work = (double2*)ws;
     a.hi_in_smem = p->N / 64 <= 2048;  // <= 32 KB of shared memory
-    if (p->logN <= kSmallMaxLog)
+    if (p->N <= (1 << kSmallMaxLog))
         return inverse ? small_dispatch<true>(p->logN, a, batch, st)
                        : small_dispatch<false>(p->logN, a, batch, st);
     SFFTB_REQUIRE(ws != nullptr, "dft: workspace required");
-    if ((p->N1 == 128 || p->N1 == 256) && (p->N2 == 128 || p->N2 == 256))
-        return fs2_dispatch(p, a, batch, inverse != 0, st);
+    if (fs2_supported(p)) return fs2_dispatch(p, a, batch, inverse != 0, st);
     // Run the three passes over L2-sized slices of the batch so the
     // four-step intermediate (16*N bytes per transform) is re-read from L2,
     // not HBM: <= 48 MiB of workspace live per slice (L2 is ~126 MB).
@@ -906,9 +1067,8 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
 
 extern "C" int64_t sfftb_sample_detect_workspace_bytes(int64_t batch, int64_t M) {
     if (batch <= 0 || M <= 0) return 0;
-    const int lg = bluestein_log(M);
-    if (lg <= kSmallMaxLog) return 0;
-    const int64_t N = int64_t(1) << lg;
+    const int64_t N = bluestein_N(M);
+    if (N <= (int64_t(1) << kSmallMaxLog)) return 0;
     return batch * N * (int64_t)sizeof(double2) + batch * 64 * (int64_t)sizeof(double) +
            batch * (int64_t)sizeof(double);
 }
@@ -921,8 +1081,8 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
     BluesteinPlan* p = nullptr;
     int rc = get_plan(M, &p);
     if (rc != SFFTB_OK) return rc;
-    if (!((p->N1 == 128 || p->N1 == 256) && (p->N2 == 128 || p->N2 == 256))) {
-        set_error("sample_detect: fused path needs N1, N2 in {128, 256}");
+    if (!fs2_supported(p)) {
+        set_error("sample_detect: fused path needs N1 in {128, 192, 256}, N2 in {128, 256}");
         return SFFTB_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -957,7 +1117,7 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
     rc = p->N2 == 256 ? fs2_cols<256, true>(a, batch, p->N1, st, true)
                       : fs2_cols<128, true>(a, batch, p->N1, st, true);
     if (rc) return rc;
-    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    rc = fs2_rows_any(a, batch, p->N1, p->N2, st);
     if (rc) return rc;
     // fused colC(sampler) + colA(detection)
     {
@@ -968,12 +1128,22 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
         const size_t hi = a.hi_in_smem ? (size_t)(N / 64) : 0;
         if (p->N2 == 256) {
             const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256 + 64 + hi);
-            SFFTB_CUDA(allow_smem(fs2_colCA<256>, sm));
-            fs2_colCA<256><<<grid, 256, sm, st>>>(c, p->N1);
+            if (sigma > 0.0) {
+                SFFTB_CUDA(allow_smem(fs2_colCA<256, true>, sm));
+                fs2_colCA<256, true><<<grid, 256, sm, st>>>(c, p->N1);
+            } else {
+                SFFTB_CUDA(allow_smem(fs2_colCA<256, false>, sm));
+                fs2_colCA<256, false><<<grid, 256, sm, st>>>(c, p->N1);
+            }
         } else {
             const size_t sm = sizeof(double2) * (Fs2Layout<128>::DATA + 128 + 64 + hi);
-            SFFTB_CUDA(allow_smem(fs2_colCA<128>, sm));
-            fs2_colCA<128><<<grid, 256, sm, st>>>(c, p->N1);
+            if (sigma > 0.0) {
+                SFFTB_CUDA(allow_smem(fs2_colCA<128, true>, sm));
+                fs2_colCA<128, true><<<grid, 256, sm, st>>>(c, p->N1);
+            } else {
+                SFFTB_CUDA(allow_smem(fs2_colCA<128, false>, sm));
+                fs2_colCA<128, false><<<grid, 256, sm, st>>>(c, p->N1);
+            }
         }
         SFFTB_CHECK_LAUNCH();
         const int per_b = p->N1 / F;
@@ -984,7 +1154,7 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
     rc = sfftb_zero_thresholds(sumsq, G, L, M, theta, st);
     if (rc) return rc;
     // detection: rowB, then colC emitting ghat (scale 1/M) and the bitmap
-    rc = p->N1 == 256 ? fs2_rows<256>(a, batch, p->N2, st) : fs2_rows<128>(a, batch, p->N2, st);
+    rc = fs2_rows_any(a, batch, p->N1, p->N2, st);
     if (rc) return rc;
     SFFTB_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * batch * a.W, st));
     {

@@ -248,6 +248,26 @@ __device__ __forceinline__ void pow_table(double2 s1, double2 s2, double2 s4, do
     }
 }
 
+// s^r, r < 16, as q4[r >> 2] * q1[r & 3] with q1 = {1, s, s^2, s^3} and
+// q4 = {1, s^4, s^8, s^12}: 8 live values instead of pow_table's 16, at most
+// three roundings per power.
+struct Pow16 {
+    double2 q1[4], q4[4];
+    __device__ __forceinline__ Pow16(double2 s1, double2 s2, double2 s4, double2 s8) {
+        q1[0] = q4[0] = make_double2(1.0, 0.0);
+        q1[1] = s1;
+        q1[2] = s2;
+        q1[3] = cmul(s1, s2);
+        q4[1] = s4;
+        q4[2] = s8;
+        q4[3] = cmul(s4, s8);
+    }
+    __device__ __forceinline__ double2 operator()(int r) const {
+        const int a = r >> 2, c = r & 3;
+        return a ? (c ? cmul(q4[a], q1[c]) : q4[a]) : q1[c];
+    }
+};
+
 __device__ __forceinline__ double2 conj_if_b(double2 w, bool c) {
     if (c) w.y = -w.y;
     return w;
@@ -275,15 +295,70 @@ __device__ __forceinline__ void fft2pass(double2 (&v)[16], double2* __restrict__
         const double2 s2 = conj_if_b(tw[2 * jm], INV);
         const double2 s4 = R2 > 4 ? conj_if_b(tw[4 * jm], INV) : one;
         const double2 s8 = R2 > 8 ? conj_if_b(tw[8 * jm], INV) : one;
-        double2 p[R2];
-        pow_table<R2>(s1, s2, s4, s8, p);
+        const Pow16 p(s1, s2, s4, s8);
 #pragma unroll
-        for (int r = 1; r < R2; ++r) u[r] = cmul(u[r], p[r]);
+        for (int r = 1; r < R2; ++r) u[r] = cmul(u[r], p(r));
         dft_reg<R2, INV>(u);
 #pragma unroll
         for (int r = 0; r < R2; ++r) v[q * R2 + r] = u[r];
     }
     __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Radix-3 and radix-12 register DFTs (natural order in and out), for the
+// mixed-radix four-step length N = 3 * 2^k (row FFTs of length 192).
+// ---------------------------------------------------------------------------
+template <bool INV>
+__device__ __forceinline__ void dft3(double2& a, double2& b, double2& c) {
+    constexpr double h = 0.86602540378443864676;  // sqrt(3)/2
+    const double2 s = cadd(b, c), d = csub(b, c);
+    const double2 m = make_double2(a.x - 0.5 * s.x, a.y - 0.5 * s.y);
+    // forward: X1 = m - i h d, X2 = m + i h d (e^{-2 pi i/3} = -1/2 - i h)
+    const double2 rot = INV ? make_double2(-h * d.y, h * d.x) : make_double2(h * d.y, -h * d.x);
+    a = cadd(a, s);
+    b = cadd(m, rot);
+    c = csub(m, rot);
+}
+
+// e^{-+2 pi i k/12}, k in [0, 12)
+template <bool INV>
+__device__ __forceinline__ double2 w12(int k) {
+    constexpr double h = 0.86602540378443864676;
+    double2 w;
+    switch (k) {
+        case 0: w = make_double2(1.0, 0.0); break;
+        case 1: w = make_double2(h, -0.5); break;
+        case 2: w = make_double2(0.5, -h); break;
+        case 3: w = make_double2(0.0, -1.0); break;
+        case 4: w = make_double2(-0.5, -h); break;
+        case 5: w = make_double2(-h, -0.5); break;
+        default: w = make_double2(-1.0, 0.0); break;  // 6
+    }
+    if (INV) w.y = -w.y;
+    return w;
+}
+
+// 12-point DFT: n = 4a + b, k = c + 3d (a, c < 3; b, d < 4):
+// X[c + 3d] = sum_b w4^{bd} w12^{bc} (sum_a x[4a + b] w3^{ac}).
+template <bool INV>
+__device__ __forceinline__ void dft12(double2 (&v)[12]) {
+    double2 y[4][3];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        double2 p = v[b], q = v[4 + b], r = v[8 + b];
+        dft3<INV>(p, q, r);
+        y[b][0] = p;
+        y[b][1] = b ? cmul(q, w12<INV>(b)) : q;
+        y[b][2] = b ? cmul(r, w12<INV>(2 * b)) : r;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double2 u[4] = {y[0][c], y[1][c], y[2][c], y[3][c]};
+        dft_reg<4, INV>(u);
+#pragma unroll
+        for (int d = 0; d < 4; ++d) v[c + 3 * d] = u[d];
+    }
 }
 
 // Four-step twiddle of pass outputs: v[e] *= w^(a * fft2_out_index<N>(t, e)),
@@ -301,15 +376,14 @@ __device__ __forceinline__ void out_twiddle(double2 (&v)[16], int a, int t,
     const double2 s2 = twiddle2<INV>(hi, lo, 32 * a);
     const double2 s4 = R2 > 4 ? twiddle2<INV>(hi, lo, 64 * a) : one;
     const double2 s8 = R2 > 8 ? twiddle2<INV>(hi, lo, 128 * a) : one;
-    double2 p[R2];
-    pow_table<R2>(s1, s2, s4, s8, p);
+    const Pow16 p(s1, s2, s4, s8);
 #pragma unroll
     for (int g = 0; g < BPT; ++g) {
         const int e0 = a * (t + g * T);
         const double2 b = twiddle2<INV>(hi, lo, e0);  // e0 == 0: exactly (1, 0)
         v[g * R2] = cmul(v[g * R2], b);
 #pragma unroll
-        for (int r = 1; r < R2; ++r) v[g * R2 + r] = cmul(v[g * R2 + r], cmul(b, p[r]));
+        for (int r = 1; r < R2; ++r) v[g * R2 + r] = cmul(v[g * R2 + r], cmul(b, p(r)));
     }
 }
 

@@ -101,8 +101,11 @@ def test_dft_vs_reference_and_naive(cuda):
         assert np.max(np.abs(y - g[f"y{M}"])) < 1e-12, M
 
 
+# 8209 / 12281 / 10331: N = 24576 = 192 x 128 (mixed radix); 16411 / 24571 / 20663:
+# N = 49152 = 192 x 256; 12289 / 24593: the power-of-two neighbours
 @pytest.mark.parametrize("M", [2, 3, 5, 7, 31, 127, 211, 509, 1009, 1039, 2069, 4099,
-                               10331, 20663, 40009, 103307])
+                               8209, 10331, 12281, 12289, 16411, 20663, 24571, 24593,
+                               40009, 103307])
 def test_dft_primes_vs_naive_and_parseval(cuda, M):
     import paper_2006_13053_b200 as pkg
 
@@ -195,7 +198,8 @@ def test_noise_stream_matches_oracle(cuda, oracle_lib):
     assert abs(np.std(got.real) - sigma) < 0.05 * sigma
 
 
-@pytest.mark.parametrize("M,G,L,sigma", [(20663, 2, 5, 0.0), (10331, 3, 3, 1e-3), (4099, 1, 7, 0.0)])
+@pytest.mark.parametrize("M,G,L,sigma", [(20663, 2, 5, 0.0), (10331, 3, 3, 1e-3), (4099, 1, 7, 0.0),
+                                         (30011, 2, 3, 1e-3), (14009, 1, 5, 0.0)])
 def test_fused_sample_detect_matches_unfused(cuda, M, G, L, sigma):
     """sfftb_sample_detect_dft (samples kept on chip) == inverse DFT + noise +
     zero test + forward DFT + bitmap run as separate kernels."""

@@ -26,9 +26,10 @@ with _native.Timeline() as tl:
     for _ in range(reps):
         _engine.sample_spectra_fused(b, M, G, L, 1, 0, 0.0)
 ms = tl.ms()["sfftb_sample_detect_dft"]
-N = 256
-while N < 2 * M - 1:
-    N *= 2
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import bluestein_N  # noqa: E402
+
+N = bluestein_N(M)
 rows = G * L
 print(f"fused M={M} N={N} rows={rows}: ms={[round(v, 4) for v in ms]}; "
       f"5-pass traffic {rows * (2 * M + 8 * N) * 16 / (min(ms) * 1e-3) / 1e9:.0f} GB/s")
