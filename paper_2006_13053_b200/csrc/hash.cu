@@ -464,6 +464,59 @@ __device__ __forceinline__ int64_t residue_exact(const int64_t* row, const int64
     return (int64_t)mod_u64(acc, (uint64_t)M, 1.0 / (double)M);
 }
 
+// Median of one component (re or im) of the L values a warp holds (lane +
+// 32 s).  Fast path: with ranks lt = #{v_j < v_i} (shared-memory broadcast
+// reads, one compare per pair), the stable-sort position floor(L/2) is held
+// by the lowest-index element with lt == floor(L/2) -- unless that position
+// falls strictly inside a run of equal values, which no lane can then claim;
+// the warp then falls back to full stable ranks #{v_j < v_i} + #{j < i: v_j
+// == v_i} (bit-identical to the reference's insertion-sort median,
+// _core.pyx:151-161, including the order of +0.0 and -0.0).
+template <int S>
+__device__ __forceinline__ double warp_median(const double (&v)[S], const double* sv, int L,
+                                              int lane) {
+    const int target = L >> 1;
+    int lt[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) lt[s] = 0;
+    for (int j = 0; j < L; ++j) {
+        const double o = sv[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) lt[s] += o < v[s];
+    }
+    int owner = -1;
+    double val = 0.0;
+#pragma unroll
+    for (int s = S - 1; s >= 0; --s) {  // lowest claiming index wins
+        const int i = lane + 32 * s;
+        const unsigned b = __ballot_sync(0xffffffffu, i < L && lt[s] == target);
+        if (b) {
+            const int src = __ffs(b) - 1;
+            owner = src + 32 * s;
+            val = __shfl_sync(0xffffffffu, v[s], src);
+        }
+    }
+    if (owner >= 0) return val;
+    int rk[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) rk[s] = 0;
+    for (int j = 0; j < L; ++j) {
+        const double o = sv[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int i = lane + 32 * s;
+            rk[s] += (o < v[s]) || (o == v[s] && j < i);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        const unsigned b = __ballot_sync(0xffffffffu, i < L && rk[s] == target);
+        if (b) val = __shfl_sync(0xffffffffu, v[s], __ffs(b) - 1);
+    }
+    return val;
+}
+
 template <int S>
 __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict__ elems, int d,
                                                       const int64_t* __restrict__ zmat, int G,
@@ -472,10 +525,10 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                                                       const int64_t* __restrict__ idx,
                                                       const int64_t* __restrict__ counts,
                                                       int64_t cap, double2* __restrict__ coeffs) {
-    const int lane = threadIdx.x & 31;
+    __shared__ double sre[8][32 * S], sim[8][32 * S];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int target = L >> 1;
     // one flat work list over the groups' detected rows (g, k), so small
     // groups do not serialise one latency-bound round per group
     int64_t total = 0;
@@ -484,49 +537,28 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
         int g = 0;
         int64_t k = w;
         while (k >= counts[g]) k -= counts[g++];
-        {
-            const int64_t row = idx[(int64_t)g * cap + k];
-            double re[S], im[S];
+        const int64_t row = idx[(int64_t)g * cap + k];
+        double re[S], im[S];
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int l = lane + 32 * s;
-                re[s] = 0.0;
-                im[s] = 0.0;
-                if (l < L) {
-                    const int64_t r = residue_exact(elems + row * d,
-                                                    zmat + ((int64_t)g * L + l) * d, d, M);
-                    const double2 v = ghat[((int64_t)g * L + l) * M + r];
-                    re[s] = v.x;
-                    im[s] = v.y;
-                }
+        for (int s = 0; s < S; ++s) {
+            const int l = lane + 32 * s;
+            re[s] = 0.0;
+            im[s] = 0.0;
+            if (l < L) {
+                const int64_t r = residue_exact(elems + row * d,
+                                                zmat + ((int64_t)g * L + l) * d, d, M);
+                const double2 v = ghat[((int64_t)g * L + l) * M + r];
+                re[s] = v.x;
+                im[s] = v.y;
             }
-            // stable rank of each owned value: #{j: v_j < v_i} + #{j < i: v_j == v_i}
-            int rk_re[S], rk_im[S];
-#pragma unroll
-            for (int s = 0; s < S; ++s) rk_re[s] = rk_im[s] = 0;
-#pragma unroll
-            for (int so = 0; so < S; ++so) {
-                for (int src = 0; src < 32; ++src) {
-                    const int j = src + 32 * so;
-                    const double ore = __shfl_sync(0xffffffffu, re[so], src);
-                    const double oim = __shfl_sync(0xffffffffu, im[so], src);
-                    if (j >= L) continue;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int i = lane + 32 * s;
-                        rk_re[s] += (ore < re[s]) || (ore == re[s] && j < i);
-                        rk_im[s] += (oim < im[s]) || (oim == im[s] && j < i);
-                    }
-                }
-            }
-            double2* out = coeffs + (int64_t)g * cap + k;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int i = lane + 32 * s;
-                if (i < L && rk_re[s] == target) out->x = re[s];
-                if (i < L && rk_im[s] == target) out->y = im[s];
-            }
+            sre[wib][l] = re[s];
+            sim[wib][l] = im[s];
         }
+        __syncwarp();
+        const double mre = warp_median<S>(re, sre[wib], L, lane);
+        const double mim = warp_median<S>(im, sim[wib], L, lane);
+        if (lane == 0) coeffs[(int64_t)g * cap + k] = make_double2(mre, mim);
+        __syncwarp();  // the next row's stores wait for these reads
     }
 }
 

@@ -266,3 +266,22 @@ def test_random_box_device(cuda):
     assert len(big) == 1 << 16
     b = big.elems
     assert np.array_equal(b, np.unique(b, axis=0)) and b.min() >= -4096 and b.max() <= 4096
+
+
+@pytest.mark.parametrize("L", [1, 7, 31, 33, 47, 63, 65])
+def test_medians_ties_and_signed_zeros_bitexact(cuda, oracle_lib, L):
+    """Median selection with heavy ties, +0.0/-0.0 mixes and runs straddling
+    the middle position (the fast path's fallback) -- bitwise against the C
+    restatement of the reference's insertion-sort median."""
+    from paper_2006_13053_b200 import _kernels
+
+    rng = np.random.default_rng(L)
+    M, d, n = 13, 2, 4000
+    e = rng.integers(0, M, size=(n, d))
+    z = rng.integers(0, M, size=(L, d))
+    vals = np.array([0.0, -0.0, 1.0, -1.0, 2.5, 0.0, -0.0])
+    gh = (rng.choice(vals, size=(L, M)) + 1j * rng.choice(vals, size=(L, M))).astype(np.complex128)
+    hits, med = _kernels.detect_gather(e, z, M, gh, -1.0, 0.0, True)  # every row detected
+    want_h, want_m = oracle_lib.gather_c(e, z, M, gh, -1.0, 0.0, True)
+    assert np.array_equal(hits, want_h)
+    assert np.array_equal(med.view(np.int64), want_m.view(np.int64))

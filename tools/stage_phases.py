@@ -11,17 +11,21 @@ import paper_2006_13053_b200 as pkg  # noqa: E402
 from paper_2006_13053_b200 import _native  # noqa: E402
 import workloads  # noqa: E402
 
-w = workloads.metric_config()
+w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "metric_config")()
 box = pkg.Box(w.d, w.lo, w.hi)
 params = pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
 poly = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+def oracle():
+    return pkg.oracle_from_poly(poly, noise_sigma=w.sigma, noise_seed=w.noise_seed)
+
+
 for _ in range(3):
-    pkg.sfft(pkg.oracle_from_poly(poly), box, params, seed=w.seed)
+    pkg.sfft(oracle(), box, params, seed=w.seed)
 torch.cuda.synchronize()
 for rep in range(2):
     t0 = time.perf_counter()
     with _native.Timeline() as tl:
-        pkg.sfft(pkg.oracle_from_poly(poly), box, params, seed=w.seed)
+        pkg.sfft(oracle(), box, params, seed=w.seed)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
     ms = tl.ms()
