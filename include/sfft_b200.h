@@ -162,6 +162,30 @@ int sfftb_compact_mask(const uint32_t *mask, int64_t G, int64_t n, int64_t *idx,
                        int64_t *counts, void *ws, void *stream);
 
 /*
+ * Residue tables of a Cartesian candidate set J = prefix (n1 x t) x vals (n2)
+ * (pair_candidates, dimincr.py:155-175; row i = i1*n2 + i2) for GL lattices
+ * with generators zmat (GL x (t+1)):  P[l*n1 + i1] = prefix[i1] . z_l[0:t]
+ * mod M,  V[l*n2 + i2] = vals[i2] * z_l[t] mod M;  r_l(i) = (P + V) mod M.
+ */
+int sfftb_pair_residues(const int64_t *prefix, int64_t n1, int64_t t,
+                        const int64_t *vals, int64_t n2, const int64_t *zmat,
+                        int64_t GL, int64_t M, int32_t *P, int32_t *V, void *stream);
+
+/* sfftb_hash_hits on a Cartesian J from its residue tables (same outputs):
+ * bitmaps + tables in shared memory, sfftb_hash_pairs_smem_bytes(L, M, n2)
+ * <= 200 KB. */
+int64_t sfftb_hash_pairs_smem_bytes(int64_t L, int64_t M, int64_t n2);
+int sfftb_hash_pairs(const int32_t *P, const int32_t *V, int64_t n1, int64_t n2,
+                     int64_t G, int64_t L, int64_t M, const uint32_t *bits,
+                     int64_t min_hits, int64_t *hits64, uint32_t *detmask, void *stream);
+
+/* sfftb_medians on a Cartesian J from its residue tables (same outputs). */
+int sfftb_medians_pairs(const int32_t *P, const int32_t *V, int64_t n1, int64_t n2,
+                        int64_t G, int64_t L, int64_t M, const double *ghat,
+                        const int64_t *idx, const int64_t *counts, int64_t cap,
+                        double *coeffs, void *stream);
+
+/*
  * Odd-L componentwise medians of the L per-lattice values of the compacted
  * rows: coeffs[g*cap + k] for row idx[g*cap + k], k < counts[g] (device).
  * The middle element of a stable sort, i.e. the reference's insertion-sort
@@ -366,6 +390,10 @@ typedef struct {
     /* elements between consecutive groups in zmat_host (0: dense G*L*tdim);
      * lets the host pre-draw L_cap >= L generators per group before L is known */
     int64_t zmat_host_ld;
+    /* optional residue tables of the Cartesian J (pair stages): ptab
+     * (G*L x n1) and vtab (G*L x n2) int32; NULL: generic hashing/medians */
+    int32_t *ptab;
+    int32_t *vtab;
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);

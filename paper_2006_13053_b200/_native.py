@@ -65,6 +65,11 @@ _SIGS = {
     "sfftb_add_noise": (_int, [_p, _i64, _i64, _u64, _i64, _dbl, _p]),
     "sfftb_injective_mod_dev": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int), _p]),
     "sfftb_sfft_stage": (_int, [_p, _p]),
+    "sfftb_pair_residues": (_int, [_p, _i64, _i64, _p, _i64, _p, _i64, _i64, _p, _p, _p]),
+    "sfftb_hash_pairs_smem_bytes": (_i64, [_i64, _i64, _i64]),
+    "sfftb_hash_pairs": (_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),
+    "sfftb_medians_pairs": (_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _i64, _p,
+                                   _p]),
     "sfftb_canonicalize_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_canonicalize_rows": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
     "sfftb_random_box_rows": (_int, [_i64, _i64, _i64, _i64, _u64, _p, _p]),

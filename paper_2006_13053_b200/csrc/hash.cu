@@ -517,14 +517,24 @@ __device__ __forceinline__ double warp_median(const double (&v)[S], const double
     return val;
 }
 
-template <int S>
+// Residue tables of a Cartesian candidate set J = prefix x vals (the
+// dimension-incremental pairing, dimincr.py:155-175): row i = i1 * n2 + i2
+// has residue (P[l][i1] + V[l][i2]) mod M on lattice l.
+struct PairTables {
+    const int32_t* P;  // [G*L][n1]
+    const int32_t* V;  // [G*L][n2]
+    int64_t n1, n2;
+};
+
+template <int S, bool PAIRS = false>
 __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict__ elems, int d,
                                                       const int64_t* __restrict__ zmat, int G,
                                                       int L, int64_t M,
                                                       const double2* __restrict__ ghat,
                                                       const int64_t* __restrict__ idx,
                                                       const int64_t* __restrict__ counts,
-                                                      int64_t cap, double2* __restrict__ coeffs) {
+                                                      int64_t cap, double2* __restrict__ coeffs,
+                                                      PairTables pt = PairTables{}) {
     __shared__ double sre[8][32 * S], sim[8][32 * S];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -545,8 +555,15 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
             re[s] = 0.0;
             im[s] = 0.0;
             if (l < L) {
-                const int64_t r = residue_exact(elems + row * d,
-                                                zmat + ((int64_t)g * L + l) * d, d, M);
+                int64_t r;
+                if (PAIRS) {
+                    const int64_t gl = (int64_t)g * L + l;
+                    const int64_t i1 = row / pt.n2, i2 = row - i1 * pt.n2;
+                    r = (int64_t)pt.P[gl * pt.n1 + i1] + pt.V[gl * pt.n2 + i2];
+                    if (r >= M) r -= M;
+                } else {
+                    r = residue_exact(elems + row * d, zmat + ((int64_t)g * L + l) * d, d, M);
+                }
                 const double2 v = ghat[((int64_t)g * L + l) * M + r];
                 re[s] = v.x;
                 im[s] = v.y;
@@ -576,6 +593,118 @@ __global__ void lattice_values_kernel(const int64_t* __restrict__ elems, int d,
         const int64_t r = residue_exact(elems + row * d, zmat + (int64_t)l * d, d, M);
         out[e] = ghat[(int64_t)l * M + r];
     }
+}
+
+// P[gl][i1] = prefix[i1] . z_gl[0:t] mod M;  V[gl][i2] = vals[i2] * z_gl[t] mod M
+__global__ void pair_residues_kernel(const int64_t* __restrict__ prefix, int64_t n1, int t,
+                                     const int64_t* __restrict__ vals, int64_t n2,
+                                     const int64_t* __restrict__ zmat, int64_t GL, int64_t M,
+                                     int32_t* __restrict__ P, int32_t* __restrict__ V) {
+    const int td = t + 1;
+    const int64_t np = GL * n1, total = np + GL * n2;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < np) {
+            const int64_t gl = e / n1, i1 = e % n1;
+            P[e] = (int32_t)residue_exact(prefix + i1 * t, zmat + gl * td, t, M);
+        } else {
+            const int64_t f = e - np, gl = f / n2, i2 = f % n2;
+            const uint64_t a = (uint64_t)reduce_mod(vals[i2], M);
+            const uint64_t b = (uint64_t)reduce_mod(zmat[gl * td + t], M);
+            V[f] = (int32_t)mod_u64(a * b, (uint64_t)M, 1.0 / (double)M);
+        }
+    }
+}
+
+// Hashing of a Cartesian J from its residue tables.  The group's bitmaps
+// arrive in shared memory by one bulk copy (TMA engine, mbarrier), the V table
+// by an unrolled loop; per tile of kPairRows * 256 rows the P entries of the
+// tile's i1 range are staged too.  Each thread owns kPairRows rows
+// (independent chains); per (row, lattice): two shared loads (P broadcast, V
+// contiguous), an add, an unsigned-min reduction and the bit probe -- no dot
+// product, no multiply-high.  (Probing the bitmaps from L1 instead: ~16
+// wavefronts per random warp probe vs ~4 in shared memory, measured slower.)
+static constexpr int kPairRows = 8;
+static constexpr int kPairThreads = 256;
+static constexpr int kPairTile = kPairRows * kPairThreads;
+
+__global__ void __launch_bounds__(kPairThreads)
+    hash_pairs_kernel(const int32_t* __restrict__ P, const int32_t* __restrict__ V, int64_t n1,
+                      int64_t n2, int L, int64_t M, const uint32_t* __restrict__ bits, int64_t W,
+                      int64_t min_hits, int64_t* __restrict__ hits64,
+                      uint32_t* __restrict__ detmask, int span) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ uint64_t bar;
+    const int g = blockIdx.y;
+    const int64_t n = n1 * n2, nwords = (n + 31) / 32;
+    uint32_t* bm = sm;                                     // L * W words
+    uint32_t* vs = sm + (int64_t)L * W;                    // L * n2
+    uint32_t* ps = vs + (((int64_t)L * n2 + 3) & ~int64_t(3));  // L * span
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)((int64_t)L * W * 4);
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(bm, bits + (int64_t)g * L * W, bytes, &bar);
+    }
+    const uint32_t* gV = (const uint32_t*)V + (int64_t)g * L * n2;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < (int64_t)L * n2; i += blockDim.x) vs[i] = __ldg(gV + i);
+    const uint32_t* gP = (const uint32_t*)P + (int64_t)g * L * n1;
+    const uint32_t M32 = (uint32_t)M;
+    const int64_t ntiles = (n + kPairTile - 1) / kPairTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bool waited = false;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t t0 = tile * kPairTile;
+        const int64_t i1lo = t0 / n2;
+        __syncthreads();  // previous tile done with ps
+#pragma unroll 4
+        for (int64_t e = threadIdx.x; e < (int64_t)L * span; e += blockDim.x) {
+            const int l = (int)(e / span);
+            const int64_t i1 = i1lo + e % span;
+            ps[e] = i1 < n1 ? __ldg(gP + (int64_t)l * n1 + i1) : 0u;
+        }
+        if (!waited) {
+            mbar_wait(&bar, 0);
+            waited = true;
+        }
+        __syncthreads();
+        int pi[kPairRows], vi[kPairRows], hits[kPairRows];
+        bool valid[kPairRows];
+#pragma unroll
+        for (int q = 0; q < kPairRows; ++q) {
+            const int64_t i = t0 + (int64_t)warp * 32 * kPairRows + q * 32 + lane;
+            valid[q] = i < n;
+            const int64_t ii = valid[q] ? i : t0;
+            const int64_t i1 = ii / n2;
+            pi[q] = (int)(i1 - i1lo);
+            vi[q] = (int)(ii - i1 * n2);
+            hits[q] = 0;
+        }
+        for (int l = 0; l < L; ++l) {
+            const uint32_t* pl = ps + (int64_t)l * span;
+            const uint32_t* vl = vs + (int64_t)l * n2;
+            const uint32_t* bl = bm + (int64_t)l * W;
+#pragma unroll
+            for (int q = 0; q < kPairRows; ++q) {
+                uint32_t r = pl[pi[q]] + vl[vi[q]];
+                r = min(r, r - M32);  // r < 2M: one unsigned min reduces it
+                hits[q] += (bl[r >> 5] >> (r & 31)) & 1u;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kPairRows; ++q) {
+            const int64_t i = t0 + (int64_t)warp * 32 * kPairRows + q * 32 + lane;
+            const unsigned det = __ballot_sync(0xffffffffu, valid[q] && hits[q] >= min_hits);
+            if (valid[q] && hits64) hits64[(int64_t)g * n + i] = hits[q];
+            if (lane == 0 && i < n) detmask[(int64_t)g * nwords + (i >> 5)] = det;
+        }
+    }
+    if (!waited) mbar_wait(&bar, 0);  // never leave a bulk copy in flight
 }
 
 // ---------------------------------------------------------------------------
@@ -919,6 +1048,75 @@ extern "C" int sfftb_medians(const int64_t* elems, int64_t d, const int64_t* zma
         medians_kernel<4><<<blocks, 256, 0, st>>>(elems, (int)d, zmat, (int)G, (int)L, M,
                                                   (const double2*)ghat, idx, counts, cap,
                                                   (double2*)coeffs);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_pair_residues(const int64_t* prefix, int64_t n1, int64_t t,
+                                   const int64_t* vals, int64_t n2, const int64_t* zmat,
+                                   int64_t GL, int64_t M, int32_t* P, int32_t* V,
+                                   void* stream) {
+    SFFTB_REQUIRE(n1 >= 0 && n2 >= 0 && t >= 1 && GL >= 1, "pair_residues: bad sizes");
+    SFFTB_REQUIRE(M >= 1 && M < (int64_t(1) << 30), "pair_residues: M must be < 2^30");
+    const int64_t total = GL * (n1 + n2);
+    if (total == 0) return SFFTB_OK;
+    pair_residues_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+        prefix, n1, (int)t, vals, n2, zmat, GL, M, P, V);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+static int64_t pair_span(int64_t n2) { return kPairTile / n2 + 2; }
+
+extern "C" int64_t sfftb_hash_pairs_smem_bytes(int64_t L, int64_t M, int64_t n2) {
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    return 4 * (L * W + ((L * n2 + 3) & ~int64_t(3)) + L * pair_span(n2));
+}
+
+extern "C" int sfftb_hash_pairs(const int32_t* P, const int32_t* V, int64_t n1, int64_t n2,
+                                int64_t G, int64_t L, int64_t M, const uint32_t* bits,
+                                int64_t min_hits, int64_t* hits64, uint32_t* detmask,
+                                void* stream) {
+    SFFTB_REQUIRE(n1 >= 0 && n2 >= 1 && G >= 1 && G <= 65535 && L >= 1, "hash_pairs: bad sizes");
+    SFFTB_REQUIRE(M >= 1 && M < (int64_t(1) << 30), "hash_pairs: M must be < 2^30");
+    const int64_t n = n1 * n2;
+    if (n == 0) return SFFTB_OK;
+    const size_t sm = (size_t)sfftb_hash_pairs_smem_bytes(L, M, n2);
+    SFFTB_REQUIRE(sm <= 200 * 1024, "hash_pairs: bitmaps + tables exceed shared memory");
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    SFFTB_CUDA(smem_opt_in(hash_pairs_kernel, sm));
+    int per_sm = 1;
+    SFFTB_CUDA(occupancy(&per_sm, hash_pairs_kernel, kPairThreads, sm));
+    const int64_t want =
+        std::max<int64_t>(1, ceil_div((int64_t)num_sms() * std::max(per_sm, 1), G));
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kPairTile), want));
+    hash_pairs_kernel<<<dim3(gx, (unsigned)G), kPairThreads, sm, (cudaStream_t)stream>>>(
+        P, V, n1, n2, (int)L, M, bits, W, min_hits, hits64, detmask, (int)pair_span(n2));
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_medians_pairs(const int32_t* P, const int32_t* V, int64_t n1, int64_t n2,
+                                   int64_t G, int64_t L, int64_t M, const double* ghat,
+                                   const int64_t* idx, const int64_t* counts, int64_t cap,
+                                   double* coeffs, void* stream) {
+    SFFTB_REQUIRE(L >= 1 && L <= 128 && (L % 2) == 1, "medians require odd L <= 128");
+    SFFTB_REQUIRE(G >= 1 && M >= 1 && n2 >= 1, "medians_pairs: bad sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = num_sms() * 8;
+    const PairTables pt{P, V, n1, n2};
+    if (L <= 32)
+        medians_kernel<1, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
+                                                        (const double2*)ghat, idx, counts, cap,
+                                                        (double2*)coeffs, pt);
+    else if (L <= 64)
+        medians_kernel<2, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
+                                                        (const double2*)ghat, idx, counts, cap,
+                                                        (double2*)coeffs, pt);
+    else
+        medians_kernel<4, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
+                                                        (const double2*)ghat, idx, counts, cap,
+                                                        (double2*)coeffs, pt);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }

@@ -90,14 +90,33 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
 
     // hashing, compaction, medians, top-s
     SFFTB_TRY(mark(3));
+    // Cartesian J (pair stages): residues from per-lattice tables of the
+    // prefix and value parts -- n1 + n2 dot products per lattice, not n1*n2
+    // (table hashing beats the resident dot-product kernel from ~8 coordinates
+    // on: measured 23+7 vs 29 us at 7, 48+11 vs 117 us at 19; tools/prof_pairs.py)
+    const bool pairs = a->vals && a->ptab && a->vtab && a->n2 >= 1;
+    const bool hash_pairs =
+        pairs && tdim >= 8 && sfftb_hash_pairs_smem_bytes(L, M, a->n2) <= 200 * 1024;
     if (n > 0) {
-        SFFTB_TRY(sfftb_hash_hits(a->J, n, tdim, a->zmat, G, L, M, a->bits, a->kbound,
-                                  a->min_hits, nullptr, a->detmask, stream));
+        if (pairs)
+            SFFTB_TRY(sfftb_pair_residues(a->prefix, a->n1, a->t, a->vals, a->n2, a->zmat, rows,
+                                          M, a->ptab, a->vtab, stream));
+        if (hash_pairs) {
+            SFFTB_TRY(sfftb_hash_pairs(a->ptab, a->vtab, a->n1, a->n2, G, L, M, a->bits,
+                                       a->min_hits, nullptr, a->detmask, stream));
+        } else {
+            SFFTB_TRY(sfftb_hash_hits(a->J, n, tdim, a->zmat, G, L, M, a->bits, a->kbound,
+                                      a->min_hits, nullptr, a->detmask, stream));
+        }
         SFFTB_TRY(mark(4));
         SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
                                      stream));
-        SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts, n,
-                                a->med, stream));
+        if (pairs)
+            SFFTB_TRY(sfftb_medians_pairs(a->ptab, a->vtab, a->n1, a->n2, G, L, M, a->ghat,
+                                          a->idx, a->counts, n, a->med, stream));
+        else
+            SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts,
+                                    n, a->med, stream));
     } else {
         SFFTB_TRY(mark(4));
         SFFTB_CUDA(cudaMemsetAsync(a->counts, 0, (size_t)G * sizeof(int64_t), st));

@@ -285,3 +285,51 @@ def test_medians_ties_and_signed_zeros_bitexact(cuda, oracle_lib, L):
     want_h, want_m = oracle_lib.gather_c(e, z, M, gh, -1.0, 0.0, True)
     assert np.array_equal(hits, want_h)
     assert np.array_equal(med.view(np.int64), want_m.view(np.int64))
+
+
+@pytest.mark.parametrize("t,n1,n2,G,L,M", [(1, 65, 65, 5, 31, 20663), (4, 1000, 65, 5, 37, 20663),
+                                           (9, 2000, 129, 2, 41, 10331), (2, 37, 3, 1, 7, 97)])
+def test_pair_tables_match_generic_hashing_and_medians(cuda, t, n1, n2, G, L, M):
+    """Residue tables of a Cartesian J reproduce sfftb_hash_hits / sfftb_medians
+    on the materialised J bit for bit."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine, _native
+
+    rng = np.random.default_rng(n1 + t)
+    prefix = np.unique(rng.integers(-64, 65, size=(n1, t)), axis=0)
+    n1 = prefix.shape[0]
+    vals = np.unique(rng.integers(-64, 65, size=n2))
+    n2 = vals.size
+    pre_d, vals_d = _dev.upload(prefix), _dev.upload(vals)
+    J = _engine.pair_product(pre_d, vals_d)
+    z = _dev.upload(rng.integers(0, M, size=(G * L, t + 1)))
+    W = int(_native.lib().sfftb_bitmap_words(M))
+    bits = _dev.upload((rng.integers(0, 1 << 31, size=(G * L * W,)) & 0x22222222).astype(np.int32))
+    n = n1 * n2
+    st = _dev.stream()
+    P = _dev.empty((G * L * n1,), torch.int32)
+    V = _dev.empty((G * L * n2,), torch.int32)
+    _native.call("sfftb_pair_residues", _dev.ptr(pre_d), n1, t, _dev.ptr(vals_d), n2, _dev.ptr(z),
+                 G * L, M, _dev.ptr(P), _dev.ptr(V), st)
+    nw = (n + 31) // 32
+    h1, h2 = _dev.empty((G * n,), torch.int64), _dev.empty((G * n,), torch.int64)
+    m1, m2 = _dev.empty((G * nw,), torch.int32), _dev.empty((G * nw,), torch.int32)
+    mh = (L + 1) // 2 - 1
+    _native.call("sfftb_hash_hits", _dev.ptr(J), n, t + 1, _dev.ptr(z), G, L, M, _dev.ptr(bits),
+                 -1, mh, _dev.ptr(h1), _dev.ptr(m1), st)
+    _native.call("sfftb_hash_pairs", _dev.ptr(P), _dev.ptr(V), n1, n2, G, L, M, _dev.ptr(bits),
+                 mh, _dev.ptr(h2), _dev.ptr(m2), st)
+    assert np.array_equal(_dev.download(h1), _dev.download(h2))
+    assert np.array_equal(_dev.download(m1), _dev.download(m2))
+    ghat = _dev.upload(rng.normal(size=(G * L, M)) + 1j * rng.normal(size=(G * L, M)))
+    idx = _dev.upload(np.concatenate([np.sort(rng.choice(n, size=min(n, 500), replace=False))
+                                      for _ in range(G)]))
+    k = min(n, 500)
+    cnt = _dev.upload(np.full(G, k, dtype=np.int64))
+    o1, o2 = _dev.empty((G * k,), torch.complex128), _dev.empty((G * k,), torch.complex128)
+    _native.call("sfftb_medians", _dev.ptr(J), t + 1, _dev.ptr(z), G, L, M, _dev.ptr(ghat),
+                 _dev.ptr(idx), _dev.ptr(cnt), k, _dev.ptr(o1), st)
+    _native.call("sfftb_medians_pairs", _dev.ptr(P), _dev.ptr(V), n1, n2, G, L, M,
+                 _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(cnt), k, _dev.ptr(o2), st)
+    assert np.array_equal(_dev.download(o1).view(np.int64), _dev.download(o2).view(np.int64))
