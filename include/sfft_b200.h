@@ -218,6 +218,17 @@ int sfftb_topk(const int64_t *idx, const double *coeffs, const int64_t *counts,
                int64_t *kidx, double *kcoeffs, int64_t *kcounts, void *ws,
                void *stream);
 
+/*
+ * sfftb_topk for large groups (10^4 - 10^6 detected rows each, e.g. noisy
+ * data where every candidate passes the zero test): the same selection and
+ * output, spread over the whole GPU (grid-wide key histograms, a 12/12/12/
+ * 12/12/4-bit radix select, tie masks, compaction).  Same workspace size.
+ */
+int sfftb_topk_grid(const int64_t *idx, const double *coeffs, const int64_t *counts,
+                    int64_t G, int64_t cap, double theta, int64_t s_tilde,
+                    int64_t *kidx, double *kcoeffs, int64_t *kcounts, void *ws,
+                    void *stream);
+
 /* Set mask bit i for every listed index (group union, dimincr.py:239-240). */
 int sfftb_mark_indices(const int64_t *idx, const int64_t *counts, int64_t G,
                        int64_t cap, uint32_t *mask, int64_t n, void *stream);
@@ -394,6 +405,9 @@ typedef struct {
      * (G*L x n1) and vtab (G*L x n2) int32; NULL: generic hashing/medians */
     int32_t *ptab;
     int32_t *vtab;
+    /* 1: the top-s selection runs grid-wide (sfftb_topk_grid) -- set when
+     * large detected sets are expected (the previous stage saturated) */
+    int64_t topk_grid;
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);

@@ -127,14 +127,16 @@ def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
     return gather(ghat, theta0, bits, M, zmat, G, L, rows, kbound, nu, want_medians, want_hits)
 
 
-def topk(idx, coeffs, counts, G, cap, theta, s_tilde):
-    """Threshold + top-s per group (detect.py:184-193) on device."""
+def topk(idx, coeffs, counts, G, cap, theta, s_tilde, grid=False):
+    """Threshold + top-s per group (detect.py:184-193) on device; ``grid``
+    spreads each group over the whole GPU (large detected sets)."""
     cap = max(int(cap), 1)
     kidx = _dev.empty((G * cap,), torch.int64)
     kco = _dev.empty((G * cap,), torch.complex128)
     kcounts = _dev.empty((G,), torch.int64)
     ws = _dev.workspace(_native.lib().sfftb_topk_workspace_bytes(G, cap))
-    _native.call("sfftb_topk", _dev.ptr(idx), _dev.ptr(coeffs), _dev.ptr(counts), G, cap,
+    _native.call("sfftb_topk_grid" if grid else "sfftb_topk", _dev.ptr(idx), _dev.ptr(coeffs),
+                 _dev.ptr(counts), G, cap,
                  float(theta), int(s_tilde), _dev.ptr(kidx), _dev.ptr(kco), _dev.ptr(kcounts),
                  _dev.ptr(ws), _dev.stream())
     return kidx, kco, kcounts

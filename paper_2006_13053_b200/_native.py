@@ -53,6 +53,7 @@ _SIGS = {
     "sfftb_lattice_values": (_int, [_p, _i64, _p, _i64, _i64, _p, _p, _i64, _p, _p]),
     "sfftb_topk_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_topk": (_int, [_p, _p, _p, _i64, _i64, _dbl, _i64, _p, _p, _p, _p, _p]),
+    "sfftb_topk_grid": (_int, [_p, _p, _p, _i64, _i64, _dbl, _i64, _p, _p, _p, _p, _p]),
     "sfftb_mark_indices": (_int, [_p, _p, _i64, _i64, _p, _i64, _p]),
     "sfftb_gather_rows": (_int, [_p, _i64, _p, _p, _i64, _p, _p]),
     "sfftb_pair_product": (_int, [_p, _i64, _i64, _p, _i64, _p, _p]),

@@ -38,7 +38,7 @@ class StageDesc(ctypes.Structure):
         ("counts", _p), ("med", _p), ("ws_compact", _p), ("kidx", _p), ("kco", _p),
         ("kcounts", _p), ("ws_topk", _p), ("umask", _p), ("uidx", _p), ("ucount", _p),
         ("host_counts", _p), ("events", _p), ("zmat_host_ld", _i64), ("ptab", _p),
-        ("vtab", _p),
+        ("vtab", _p), ("topk_grid", _i64),
     ]
 
 

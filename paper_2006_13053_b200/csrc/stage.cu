@@ -123,8 +123,12 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
     }
     SFFTB_TRY(mark(5));
     const int64_t cap = n > 0 ? n : 1;
-    SFFTB_TRY(sfftb_topk(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde, a->kidx,
-                         a->kco, a->kcounts, a->ws_topk, stream));
+    if (a->topk_grid && cap >= 16384)
+        SFFTB_TRY(sfftb_topk_grid(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde,
+                                  a->kidx, a->kco, a->kcounts, a->ws_topk, stream));
+    else
+        SFFTB_TRY(sfftb_topk(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde, a->kidx,
+                             a->kco, a->kcounts, a->ws_topk, stream));
     SFFTB_CUDA(cudaMemcpyAsync(a->host_counts, a->kcounts, (size_t)G * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, st));
 

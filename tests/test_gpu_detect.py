@@ -145,8 +145,10 @@ def test_topk_selection_vs_oracle(cuda, oracle_lib):
     co = np.where(rng.random(n) < 0.5, mags + 0j, 1j * mags)
     idx_d, co_d = _dev.upload(idx), _dev.upload(co)
     cnt = torch.tensor([n], device="cuda")
-    for s_tilde, theta in ((2000, 1.3), (n + 5, 0.0), (0, 0.0), (1, 1.9), (70_000, 1.0)):
-        kidx, kco, kc = _engine.topk(idx_d, co_d, cnt, 1, n, theta, s_tilde)
+    for grid, s_tilde, theta in [(g, s, th) for g in (False, True)
+                                 for s, th in ((2000, 1.3), (n + 5, 0.0), (0, 0.0), (1, 1.9),
+                                               (70_000, 1.0))]:
+        kidx, kco, kc = _engine.topk(idx_d, co_d, cnt, 1, n, theta, s_tilde, grid=grid)
         k = int(kc[0])
         want_i, want_c = oracle_lib.topk_filter(idx, co, s_tilde, theta)
         assert k == len(want_i)
@@ -194,3 +196,33 @@ def test_postprocess_r1l_kernel_vs_oracle(cuda, oracle_lib, M, L, n, s):
     assert np.array_equal(post.detected_idx, want_idx)
     assert np.max(np.abs(post.coeffs - want_co), initial=0.0) <= 1e-13 * max(
         1.0, np.max(np.abs(want_co), initial=0.0))
+
+
+def test_topk_grid_path_multi_group_vs_oracle(cuda, oracle_lib):
+    """The grid-wide top-s (caps >= 16384) with several groups of different
+    counts inside one cap-strided batch, exact ties, dropped entries."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine
+
+    rng = np.random.default_rng(5)
+    cap, G = 40_000, 3
+    counts = [40_000, 17_000, 25_001]
+    idx = np.zeros((G, cap), np.int64)
+    co = np.zeros((G, cap), np.complex128)
+    for g, n in enumerate(counts):
+        idx[g, :n] = np.sort(rng.choice(10**6, size=n, replace=False))
+        m = rng.choice(np.linspace(0.5, 2, 300), size=n)
+        co[g, :n] = np.where(rng.random(n) < 0.5, m + 0j, -1j * m)
+    idx_d, co_d = _dev.upload(idx.ravel()), _dev.upload(co.ravel())
+    cnt = torch.tensor(counts, device="cuda")
+    for grid, s_tilde, theta in [(g, s, th) for g in (True, False)
+                                 for s, th in ((2000, 0.9), (30_000, 0.0), (1, 1.99), (0, 0.0))]:
+        kidx, kco, kc = _engine.topk(idx_d, co_d, cnt, G, cap, theta, s_tilde, grid=grid)
+        kc = _dev.download(kc)
+        ki, kk = _dev.download(kidx), _dev.download(kco)
+        for g, n in enumerate(counts):
+            want_i, want_c = oracle_lib.topk_filter(idx[g, :n], co[g, :n], s_tilde, theta)
+            assert kc[g] == len(want_i)
+            assert np.array_equal(ki[g * cap: g * cap + kc[g]], want_i)
+            assert np.array_equal(kk[g * cap: g * cap + kc[g]], want_c)
