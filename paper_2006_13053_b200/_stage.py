@@ -147,7 +147,7 @@ def buffers(A, desc, G, L, M, n, s, fused, slot):
     kidx = A.get("kidx", G * cap)
     kco = A.get("kco", 2 * G * cap, f64)
     desc.kidx, desc.kco = kidx.data_ptr(), kco.data_ptr()
-    desc.kcounts = P("kcounts", G)
+    desc.kcounts = A.get("kcounts", G).data_ptr()
     desc.ws_topk = A.bytes("ws_topk", lib.sfftb_topk_workspace_bytes(G, cap))
     desc.umask = P("umask", nw, torch.int32)
     uidx = A.get(f"uidx{slot}", cap)
@@ -155,7 +155,8 @@ def buffers(A, desc, G, L, M, n, s, fused, slot):
     desc.uidx, desc.ucount = uidx.data_ptr(), ucount.data_ptr()
     hc = A.get(f"host_counts{slot}", G + 1, torch.int64, pinned=True)
     desc.host_counts = hc.data_ptr()
-    return kidx, kco, uidx, ucount, hc
+    kcounts = A.get("kcounts", G)
+    return kidx, kco, uidx, ucount, hc, kcounts
 
 
 def host_inputs(A, zs, tails, tail_w, slot=0):

@@ -135,6 +135,32 @@ class Stream:
         return out
 
 
+def _small(v):
+    return 0 <= v < (1 << 32)
+
+
+def grid(master, tag, ts, indices):
+    """Streams for SeedSequence((master, tag, t, i)) over t in ts (outer), i in
+    indices (inner) -- the entropy words assembled with numpy in one go when
+    tag, t and i are single words (always, for the driver)."""
+    ts, indices = list(ts), list(indices)
+    if not (_small(tag) and all(_small(v) for v in ts) and all(_small(v) for v in indices)):
+        return Streams([(master, tag, t, i) for t in ts for i in indices])
+    mw = _words(master)
+    rows = len(ts) * len(indices)
+    arr = np.empty((rows, len(mw) + 3), dtype=np.uint32)
+    arr[:, :len(mw)] = mw
+    arr[:, len(mw)] = tag
+    arr[:, len(mw) + 1] = np.repeat(np.asarray(ts, dtype=np.uint32), len(indices))
+    arr[:, len(mw) + 2] = np.tile(np.asarray(indices, dtype=np.uint32), len(ts))
+    out = Streams.__new__(Streams)
+    out.state = np.zeros((rows, 6), dtype=np.uint64)
+    if rows:
+        _native.check(_native.lib().sfftb_pcg64_seed(_ptr(arr), rows, arr.shape[1],
+                                                     _ptr(out.state)), "pcg64_seed")
+    return out
+
+
 def streams(master, tag, t, indices):
     """Streams for SeedSequence((master, tag, t, i)), i in indices."""
-    return Streams([(master, tag, t, i) for i in indices])
+    return grid(master, tag, [t], indices)
