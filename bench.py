@@ -543,6 +543,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config entry-point times (configs 1, 2, 3, 5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local = dist_env()
@@ -601,6 +603,8 @@ def main():
                     "ms": round(h["e2e_ms"], 2), "h2d_bytes_per_step": h["h2d"],
                     "d2h_bytes_per_step": h["d2h"]},
         }
+    if rank == 0 and world == 1 and not args.no_configs:
+        out["other_configs"] = all_configs()
     if rank == 0 and world == 1 and not args.no_cpu:
         est, info = cpu_sfft_bounded(r["workload"], args.cpu_budget, workers)
         out["cpu_baseline"] = {
@@ -625,6 +629,56 @@ def main():
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def all_configs(reps=3):
+    """Entry-point device time of the other BASELINE configs on this GPU
+    (median of `reps` after one warm-up; parity = exact support for the
+    exact-sparse configs, planted support for config 1)."""
+    import torch
+
+    import paper_2006_13053_b200 as pkg
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts, out = [], None
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts), out
+
+    out = {}
+    for name in ("config2", "config3", "config5"):
+        w = getattr(workloads, name)()
+        poly = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+        box = pkg.Box(w.d, w.lo, w.hi)
+        params = pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
+        ms, res = timed(lambda: pkg.sfft(pkg.oracle_from_poly(
+            poly, noise_sigma=w.sigma, noise_seed=w.noise_seed), box, params, seed=w.seed))
+        ent = {"entry": "sfft", "ms": round(ms, 3), "samples": res.sample_count,
+               "support": len(res.support)}
+        if w.sigma == 0:
+            ent["exact_support"] = bool(np.array_equal(
+                res.support.elems, w.support[np.lexsort(w.support.T[::-1])]))
+        out[w.name] = ent
+    w = workloads.config1()
+    G = pkg.FreqSet(w.d, w.gamma, _sorted=True)
+    cfg = pkg.draw_config(G, w.s, 0.1, rng=w.rng)
+    orc = pkg.oracle_from_poly(pkg.SparsePoly(G.take(w.support_idx), w.coeffs))
+    smp = orc.sample_lattices_device(cfg.zmat_device(), cfg.shared_M,
+                                     torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
+                                     1, cfg.L, w.d).contiguous()
+    ms, det = timed(lambda: pkg.detect_and_compute(smp, cfg, G).detected_idx)
+    out["cfg1"] = {"entry": "detect_and_compute", "ms": round(ms, 3),
+                   "detected_equals_support": bool(np.array_equal(det,
+                                                                  np.sort(w.support_idx)))}
+    return out
 
 
 def reference_arm(args, rank, world, workers):
