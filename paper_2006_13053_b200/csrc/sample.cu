@@ -108,6 +108,118 @@ __global__ void __launch_bounds__(kScatterThreads)
     }
 }
 
+// Same binning with a stable LSD radix sort of the residues (8-bit digits,
+// ceil(log2 M / 8) passes) in place of the bitonic network: per pass a digit
+// histogram, its scan, and a stable scatter in rounds of 512 items whose
+// in-round ranks come from __match_any_sync peer masks -- ~3 barriers per
+// round instead of log2(P)^2/2 network stages.  Ties stay in coefficient
+// order, so the run heads accumulate exactly like np.bincount.
+static constexpr int kScatterRsThreads = 512;
+static constexpr int kScatterRsChunk = 4096;
+
+__global__ void __launch_bounds__(kScatterRsThreads)
+    scatter_rs_kernel(const int64_t* __restrict__ support, int64_t s, int d, int t_dim,
+                      const double2* __restrict__ anchored, const int64_t* __restrict__ zmat,
+                      int L, int64_t M, int npass, double2* __restrict__ bins) {
+    constexpr int W = kScatterRsThreads / 32;
+    extern __shared__ uint32_t rs_dsm[];
+    uint32_t* ra = rs_dsm;
+    uint32_t* ia = ra + kScatterRsChunk;
+    uint32_t* rb = ia + kScatterRsChunk;
+    uint32_t* ib = rb + kScatterRsChunk;
+    uint32_t(*wcnt)[256] = reinterpret_cast<uint32_t(*)[256]>(ib + kScatterRsChunk);
+    __shared__ uint32_t base[256], running[256];
+    __shared__ uint64_t zs[64];
+    const int64_t lat = blockIdx.x, g = lat / L;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const double invM = 1.0 / (double)M;
+    for (int j = threadIdx.x; j < t_dim; j += blockDim.x)
+        zs[j] = (uint64_t)reduce_mod(zmat[lat * t_dim + j], M);
+    for (int b = threadIdx.x; b < W * 256; b += blockDim.x) wcnt[0][b] = 0;
+    double2* B = bins + lat * M;
+    for (int64_t h = threadIdx.x; h < M; h += blockDim.x) B[h] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const double2* a = anchored + g * s;
+    for (int64_t c0 = 0; c0 < s; c0 += kScatterRsChunk) {
+        const int cnt = (int)(s - c0 < kScatterRsChunk ? s - c0 : kScatterRsChunk);
+        uint32_t *r0 = ra, *i0 = ia, *r1 = rb, *i1 = ib;
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int64_t* row = support + (c0 + i) * d;
+            uint64_t r = 0;  // r + e z < M + M^2 < 2^62
+            for (int j = 0; j < t_dim; ++j)
+                r = mod_u64(r + (uint64_t)reduce_mod(row[j], M) * zs[j], (uint64_t)M, invM);
+            r0[i] = (uint32_t)r;
+            i0[i] = (uint32_t)i;
+        }
+        for (int pass = 0; pass < npass; ++pass) {
+            const int shift = 8 * pass;
+            for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+                base[b] = 0;
+                running[b] = 0;
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+                atomicAdd(&base[(r0[i] >> shift) & 255u], 1u);
+            __syncthreads();
+            if (threadIdx.x == 0) {  // exclusive scan of the 256 digit counts
+                uint32_t run = 0;
+                for (int b = 0; b < 256; ++b) {
+                    const uint32_t v = base[b];
+                    base[b] = run;
+                    run += v;
+                }
+            }
+            __syncthreads();
+            for (int rr = 0; rr < cnt; rr += blockDim.x) {
+                const int i = rr + threadIdx.x;
+                const bool ok = i < cnt;
+                const unsigned dg = ok ? ((r0[i] >> shift) & 255u) : 256u + lane;
+                const unsigned peers = __match_any_sync(0xffffffffu, dg);
+                const int rank = __popc(peers & lt);
+                if (ok && rank == 0) wcnt[warp][dg] = __popc(peers);
+                __syncthreads();
+                if (ok) {
+                    uint32_t pos = base[dg] + running[dg] + rank;
+                    for (int w = 0; w < warp; ++w) pos += wcnt[w][dg];
+                    r1[pos] = r0[i];
+                    i1[pos] = i0[i];
+                }
+                __syncthreads();
+                if (threadIdx.x < 256) {
+                    uint32_t sum = 0;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        sum += wcnt[w][threadIdx.x];
+                        wcnt[w][threadIdx.x] = 0;
+                    }
+                    running[threadIdx.x] += sum;
+                }
+                __syncthreads();
+            }
+            uint32_t* t = r0;
+            r0 = r1;
+            r1 = t;
+            t = i0;
+            i0 = i1;
+            i1 = t;
+        }
+        // run heads accumulate their run in ascending coefficient order
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const uint32_t r = r0[i];
+            if (i > 0 && r0[i - 1] == r) continue;
+            double2 acc = B[r];
+            for (int q = i; q < cnt && r0[q] == r; ++q) {
+                const double2 v = a[c0 + i0[q]];
+                acc.x += v.x;
+                acc.y += v.y;
+            }
+            B[r] = acc;
+        }
+        __syncthreads();
+    }
+}
+
 // One warp per point: lane q accumulates coefficients q, q+32, ... in order,
 // then a fixed shuffle tree adds the 32 partial sums (deterministic).
 static constexpr int kEvalThreads = 256;
@@ -188,6 +300,17 @@ extern "C" int sfftb_scatter_bins(const int64_t* support, int64_t s, int64_t d, 
     const int64_t lat = G * L;
     if (lat == 0) return SFFTB_OK;
     SFFTB_REQUIRE(lat <= 0x7fffffff, "scatter: too many lattices");
+    if (M <= (int64_t(1) << 24)) {  // the radix path: <= 3 digit passes
+        int npass = 1;
+        while (npass < 4 && (int64_t(1) << (8 * npass)) < M) ++npass;
+        const size_t rsm = sizeof(uint32_t) * (4 * kScatterRsChunk + 256 * (kScatterRsThreads / 32));
+        SFFTB_CUDA(smem_opt_in(scatter_rs_kernel, rsm));
+        scatter_rs_kernel<<<(unsigned)lat, kScatterRsThreads, rsm, (cudaStream_t)stream>>>(
+            support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M, npass,
+            (double2*)bins);
+        SFFTB_CHECK_LAUNCH();
+        return SFFTB_OK;
+    }
     const size_t sm = sizeof(uint64_t) * kScatterChunk;
     SFFTB_CUDA(smem_opt_in(scatter_kernel, sm));
     scatter_kernel<<<(unsigned)lat, kScatterThreads, sm, (cudaStream_t)stream>>>(
