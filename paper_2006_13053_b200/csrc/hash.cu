@@ -367,7 +367,7 @@ __global__ void nonzero_bitmap_kernel(const double2* __restrict__ ghat, int64_t 
 
 static constexpr int kCompactWordsPerBlock = 4096;
 static constexpr int kCompactThreads = 256;
-static constexpr int64_t kCompactSingleWords = 16384;
+static constexpr int64_t kCompactSingleWords = 8192;  // one 1024-thread CTA per group
 
 __global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
                               int64_t nblk, int64_t* __restrict__ blocksum) {
@@ -402,14 +402,15 @@ __global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts) {
 // SINGLE: one CTA per group walks all words with a running carry and writes
 // counts[g] itself -- one launch instead of count/scan/write for the small
 // masks of the sfft stages (nwords <= kCompactSingleWords).
-template <bool SINGLE>
-__global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords, int64_t n,
-                              int64_t nblk, const int64_t* __restrict__ blocksum,
-                              int64_t* __restrict__ idx, int64_t* __restrict__ counts) {
+template <bool SINGLE, int NT = kCompactThreads>
+__global__ void __launch_bounds__(NT)
+    compact_write(const uint32_t* __restrict__ mask, int64_t nwords, int64_t n, int64_t nblk,
+                  const int64_t* __restrict__ blocksum, int64_t* __restrict__ idx,
+                  int64_t* __restrict__ counts) {
     const int g = blockIdx.y;
     const int64_t w0 = SINGLE ? 0 : blockIdx.x * (int64_t)kCompactWordsPerBlock;
     const int64_t wend = SINGLE ? nwords : min(nwords, w0 + kCompactWordsPerBlock);
-    __shared__ int64_t warp_tot[kCompactThreads / 32];
+    __shared__ int64_t warp_tot[NT / 32];
     __shared__ int64_t carry;
     if (threadIdx.x == 0) carry = SINGLE ? 0 : blocksum[(int64_t)g * nblk + blockIdx.x];
     __syncthreads();
@@ -439,7 +440,7 @@ __global__ void compact_write(const uint32_t* __restrict__ mask, int64_t nwords,
         __syncthreads();
         if (threadIdx.x == 0) {
             int64_t t = 0;
-            for (int k = 0; k < kCompactThreads / 32; ++k) t += warp_tot[k];
+            for (int k = 0; k < NT / 32; ++k) t += warp_tot[k];
             carry += t;
         }
         __syncthreads();
@@ -1013,7 +1014,7 @@ extern "C" int sfftb_compact_mask(const uint32_t* mask, int64_t G, int64_t n, in
     const int64_t nblk = std::max<int64_t>(1, ceil_div(nwords, kCompactWordsPerBlock));
     int64_t* bs = (int64_t*)ws;
     if (nwords <= kCompactSingleWords) {
-        compact_write<true><<<dim3(1, (unsigned)G), kCompactThreads, 0, st>>>(
+        compact_write<true, 1024><<<dim3(1, (unsigned)G), 1024, 0, st>>>(
             mask, nwords, n, 1, nullptr, idx, counts);
         SFFTB_CHECK_LAUNCH();
         return SFFTB_OK;
