@@ -465,50 +465,49 @@ __device__ __forceinline__ int64_t residue_exact(const int64_t* row, const int64
     return (int64_t)mod_u64(acc, (uint64_t)M, 1.0 / (double)M);
 }
 
-// Median of one component (re or im) of the L values a warp holds (lane +
-// 32 s).  Fast path: with ranks lt = #{v_j < v_i} (shared-memory broadcast
-// reads, one compare per pair), the stable-sort position floor(L/2) is held
-// by the lowest-index element with lt == floor(L/2) -- unless that position
-// falls strictly inside a run of equal values, which no lane can then claim;
-// the warp then falls back to full stable ranks #{v_j < v_i} + #{j < i: v_j
-// == v_i} (bit-identical to the reference's insertion-sort median,
-// _core.pyx:151-161, including the order of +0.0 and -0.0).
+// Componentwise median of the L complex values a warp holds (lane + 32 s).
+// Fast path: ranks lt = #{v_j < v_i} for both components in one pass over the
+// warp's values in shared memory (broadcast double2 reads); the stable-sort
+// position floor(L/2) is held by the lowest-index element with lt ==
+// floor(L/2) -- unless that position falls strictly inside a run of equal
+// values, which no lane can then claim; that component then falls back to
+// full stable ranks #{v_j < v_i} + #{j < i: v_j == v_i} (bit-identical to the
+// reference's insertion-sort median, _core.pyx:151-161, including the order
+// of +0.0 and -0.0).
 template <int S>
-__device__ __forceinline__ double warp_median(const double (&v)[S], const double* sv, int L,
-                                              int lane) {
+__device__ __forceinline__ double median_claim(const double (&v)[S], const int (&lt)[S], int L,
+                                               int lane, bool& found) {
     const int target = L >> 1;
-    int lt[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) lt[s] = 0;
-    for (int j = 0; j < L; ++j) {
-        const double o = sv[j];
-#pragma unroll
-        for (int s = 0; s < S; ++s) lt[s] += o < v[s];
-    }
-    int owner = -1;
     double val = 0.0;
+    found = false;
 #pragma unroll
     for (int s = S - 1; s >= 0; --s) {  // lowest claiming index wins
         const int i = lane + 32 * s;
         const unsigned b = __ballot_sync(0xffffffffu, i < L && lt[s] == target);
         if (b) {
-            const int src = __ffs(b) - 1;
-            owner = src + 32 * s;
-            val = __shfl_sync(0xffffffffu, v[s], src);
+            val = __shfl_sync(0xffffffffu, v[s], __ffs(b) - 1);
+            found = true;
         }
     }
-    if (owner >= 0) return val;
+    return val;
+}
+
+template <int S>
+__device__ __forceinline__ double median_stable(const double (&v)[S], const double2* sv, bool im,
+                                                int L, int lane) {
+    const int target = L >> 1;
     int rk[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) rk[s] = 0;
     for (int j = 0; j < L; ++j) {
-        const double o = sv[j];
+        const double o = im ? sv[j].y : sv[j].x;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int i = lane + 32 * s;
             rk[s] += (o < v[s]) || (o == v[s] && j < i);
         }
     }
+    double val = 0.0;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const int i = lane + 32 * s;
@@ -516,6 +515,28 @@ __device__ __forceinline__ double warp_median(const double (&v)[S], const double
         if (b) val = __shfl_sync(0xffffffffu, v[s], __ffs(b) - 1);
     }
     return val;
+}
+
+template <int S>
+__device__ __forceinline__ double2 warp_median2(const double (&re)[S], const double (&im)[S],
+                                                const double2* sv, int L, int lane) {
+    int lr[S], li[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) lr[s] = li[s] = 0;
+    for (int j = 0; j < L; ++j) {
+        const double2 o = sv[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            lr[s] += o.x < re[s];
+            li[s] += o.y < im[s];
+        }
+    }
+    bool fr, fi;
+    double mr = median_claim<S>(re, lr, L, lane, fr);
+    double mi = median_claim<S>(im, li, L, lane, fi);
+    if (!fr) mr = median_stable<S>(re, sv, false, L, lane);
+    if (!fi) mi = median_stable<S>(im, sv, true, L, lane);
+    return make_double2(mr, mi);
 }
 
 // Residue tables of a Cartesian candidate set J = prefix x vals (the
@@ -536,7 +557,7 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                                                       const int64_t* __restrict__ counts,
                                                       int64_t cap, double2* __restrict__ coeffs,
                                                       PairTables pt = PairTables{}) {
-    __shared__ double sre[8][32 * S], sim[8][32 * S];
+    __shared__ double2 sv[8][32 * S];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -569,13 +590,11 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                 re[s] = v.x;
                 im[s] = v.y;
             }
-            sre[wib][l] = re[s];
-            sim[wib][l] = im[s];
+            sv[wib][l] = make_double2(re[s], im[s]);
         }
         __syncwarp();
-        const double mre = warp_median<S>(re, sre[wib], L, lane);
-        const double mim = warp_median<S>(im, sim[wib], L, lane);
-        if (lane == 0) coeffs[(int64_t)g * cap + k] = make_double2(mre, mim);
+        const double2 m = warp_median2<S>(re, im, sv[wib], L, lane);
+        if (lane == 0) coeffs[(int64_t)g * cap + k] = m;
         __syncwarp();  // the next row's stores wait for these reads
     }
 }
