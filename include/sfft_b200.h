@@ -162,6 +162,20 @@ int sfftb_compact_mask(const uint32_t *mask, int64_t G, int64_t n, int64_t *idx,
                        int64_t *counts, void *ws, void *stream);
 
 /*
+ * Distinct lattice sizes (detect.py:134-145): for each row of vals (n, L)
+ * complex128, hits[i] = #{l: hypot(vals[i, l]) > theta} and, when
+ * want_medians and hits[i] >= thr, medians[i] = np.median of the real and
+ * imaginary parts (mean of the two middle values for even L).
+ */
+int sfftb_rows_hits_medians(const double *vals, int64_t n, int64_t L, double theta,
+                            double thr, int want_medians, int64_t *hits,
+                            double *medians, void *stream);
+
+/* mask bit i = hits[i] >= thr (the detection threshold nu*L, a double). */
+int sfftb_threshold_mask(const int64_t *hits, int64_t n, double thr, uint32_t *mask,
+                         void *stream);
+
+/*
  * Residue tables of a Cartesian candidate set J = prefix (n1 x t) x vals (n2)
  * (pair_candidates, dimincr.py:155-175; row i = i1*n2 + i2) for GL lattices
  * with generators zmat (GL x (t+1)):  P[l*n1 + i1] = prefix[i1] . z_l[0:t]

@@ -435,6 +435,24 @@ def gather(samples, M, zmat, elems, theta0, nu, want_medians,
     return hits, med, thr
 
 
+def gather_mixed(samples, Ms, zmat, elems, theta0, nu, want_medians):
+    """_gather for distinct lattice sizes (detect.py:134-145): hits by np.abs
+    (hypot) > theta, np.median of the real and imaginary parts."""
+    L = len(Ms)
+    vals = np.empty((elems.shape[0], L), dtype=np.complex128)
+    for col, (s, M) in enumerate(zip(samples, Ms)):
+        g = dft_normalized(np.asarray(s, dtype=np.complex128))
+        vals[:, col] = g[residues(elems, zmat[col], M)]
+    hits = np.sum(np.abs(vals) > theta0, axis=1).astype(np.int64)
+    thr = nu * L
+    med = np.zeros(elems.shape[0], dtype=np.complex128)
+    det = hits >= thr
+    if want_medians and np.any(det):
+        sel = vals[det]
+        med[det] = np.median(sel.real, axis=1) + 1j * np.median(sel.imag, axis=1)
+    return hits, med, thr
+
+
 def detect_and_compute(samples, M, zmat, elems, theta0=None, nu=0.5, **kw):
     """Alg. 2 (detect.py:158-169) -> (hits, detected_idx, coeffs, theta0)."""
     if nu != 0.5:

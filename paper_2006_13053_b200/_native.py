@@ -66,6 +66,8 @@ _SIGS = {
     "sfftb_add_noise": (_int, [_p, _i64, _i64, _u64, _i64, _dbl, _p]),
     "sfftb_injective_mod_dev": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int), _p]),
     "sfftb_sfft_stage": (_int, [_p, _p]),
+    "sfftb_rows_hits_medians": (_int, [_p, _i64, _i64, _dbl, _dbl, _int, _p, _p, _p]),
+    "sfftb_threshold_mask": (_int, [_p, _i64, _dbl, _p, _p]),
     "sfftb_pair_residues": (_int, [_p, _i64, _i64, _p, _i64, _p, _i64, _i64, _p, _p, _p]),
     "sfftb_hash_pairs_smem_bytes": (_i64, [_i64, _i64, _i64]),
     "sfftb_hash_pairs": (_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _p]),

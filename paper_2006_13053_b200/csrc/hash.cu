@@ -615,6 +615,62 @@ __global__ void lattice_values_kernel(const int64_t* __restrict__ elems, int d,
     }
 }
 
+// Distinct lattice sizes (reference detect.py:134-145, numpy path): per row of
+// vals (n, L) the hits count #{l: |v_l| > theta} with |.| = hypot (np.abs) and,
+// for rows with hits >= thr, np.median of the real and imaginary parts: the
+// middle element (odd L) or the mean of the two middle elements (even L).
+// One warp per row; values staged in shared memory, stable ranks.
+__global__ void __launch_bounds__(256)
+    rows_hits_medians_kernel(const double2* __restrict__ vals, int64_t n, int L, double theta,
+                             double thr, int want_medians, int64_t* __restrict__ hits,
+                             double2* __restrict__ med) {
+    __shared__ double2 sv[8][128];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < n; i += nw) {
+        int h = 0;
+        for (int l = lane; l < L; l += 32) {
+            const double2 v = vals[i * L + l];
+            sv[wib][l] = v;
+            h += hypot(v.x, v.y) > theta;
+        }
+        for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+        __syncwarp();
+        double2 m = make_double2(0.0, 0.0);
+        if (want_medians && (double)h >= thr) {
+            const int lo = (L - 1) / 2, hi = L / 2;
+            double lo_re = 0.0, hi_re = 0.0, lo_im = 0.0, hi_im = 0.0;
+            for (int l = lane; l < L; l += 32) {
+                const double2 v = sv[wib][l];
+                int rr = 0, ri = 0;
+                for (int j = 0; j < L; ++j) {
+                    const double2 o = sv[wib][j];
+                    rr += (o.x < v.x) || (o.x == v.x && j < l);
+                    ri += (o.y < v.y) || (o.y == v.y && j < l);
+                }
+                if (rr == lo) lo_re = v.x;
+                if (rr == hi) hi_re = v.x;
+                if (ri == lo) lo_im = v.y;
+                if (ri == hi) hi_im = v.y;
+            }
+            for (int o = 16; o > 0; o >>= 1) {  // exactly one lane holds each
+                lo_re += __shfl_xor_sync(0xffffffffu, lo_re, o);
+                hi_re += __shfl_xor_sync(0xffffffffu, hi_re, o);
+                lo_im += __shfl_xor_sync(0xffffffffu, lo_im, o);
+                hi_im += __shfl_xor_sync(0xffffffffu, hi_im, o);
+            }
+            m = (L & 1) ? make_double2(lo_re, lo_im)
+                        : make_double2((lo_re + hi_re) / 2.0, (lo_im + hi_im) / 2.0);
+        }
+        if (lane == 0) {
+            hits[i] = h;
+            if (want_medians) med[i] = m;
+        }
+        __syncwarp();
+    }
+}
+
 // P[gl][i1] = prefix[i1] . z_gl[0:t] mod M;  V[gl][i2] = vals[i2] * z_gl[t] mod M
 __global__ void pair_residues_kernel(const int64_t* __restrict__ prefix, int64_t n1, int t,
                                      const int64_t* __restrict__ vals, int64_t n2,
@@ -1068,6 +1124,37 @@ extern "C" int sfftb_medians(const int64_t* elems, int64_t d, const int64_t* zma
         medians_kernel<4><<<blocks, 256, 0, st>>>(elems, (int)d, zmat, (int)G, (int)L, M,
                                                   (const double2*)ghat, idx, counts, cap,
                                                   (double2*)coeffs);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+__global__ void threshold_mask_kernel(const int64_t* __restrict__ hits, int64_t n, double thr,
+                                      uint32_t* __restrict__ mask) {
+    const int64_t nb = (n + 31) / 32 * 32;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool d = i < n && (double)hits[i] >= thr;
+        const unsigned b = __ballot_sync(0xffffffffu, d);
+        if ((threadIdx.x & 31) == 0) mask[i >> 5] = b;
+    }
+}
+
+extern "C" int sfftb_threshold_mask(const int64_t* hits, int64_t n, double thr, uint32_t* mask,
+                                    void* stream) {
+    if (n <= 0) return SFFTB_OK;
+    threshold_mask_kernel<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        hits, n, thr, mask);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_rows_hits_medians(const double* vals, int64_t n, int64_t L, double theta,
+                                       double thr, int want_medians, int64_t* hits,
+                                       double* medians, void* stream) {
+    SFFTB_REQUIRE(n >= 0 && L >= 1 && L <= 128, "rows_hits_medians: 1 <= L <= 128");
+    if (n == 0) return SFFTB_OK;
+    rows_hits_medians_kernel<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const double2*)vals, n, (int)L, theta, thr, want_medians, hits, (double2*)medians);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }

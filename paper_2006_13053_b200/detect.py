@@ -192,35 +192,50 @@ def _gather(samples, config, gamma, zero, want_medians, want_hits=True):
 
 
 def _gather_mixed(samples, config, gamma, zero, want_medians):
-    """Distinct lattice sizes (detect.py:134-145): one lattice at a time."""
+    """Distinct lattice sizes (detect.py:134-145): each lattice's spectrum and
+    per-row values on the device, then hits by |v| > theta with np.abs's
+    hypot and np.median per row (csrc/hash.cu rows_hits_medians)."""
     rows = gamma.device()
     n = len(gamma)
     L = config.L
-    theta = _theta_tensor(zero.theta_zero)
-    hits = torch.zeros((n,), dtype=torch.int64, device=_dev.device())
-    vals = torch.empty((n, L), dtype=torch.complex128, device=_dev.device())
-    allrows = torch.arange(n, dtype=torch.int64, device=_dev.device())
-    for col, (s, lat) in enumerate(zip(samples, config.lattices)):
+    theta = float(zero.theta_zero)
+    allrows = torch.arange(max(n, 1), dtype=torch.int64, device=_dev.device())
+    vals = torch.empty((max(n, 1), L), dtype=torch.complex128, device=_dev.device())
+    col_buf = torch.empty((max(n, 1),), dtype=torch.complex128, device=_dev.device())
+    for col, (s, lat) in enumerate(zip(samples, config.lattices)):  # staged per lattice
+        g = dft_batch(s.reshape(1, -1), lat.M)
         z = _dev.upload(lat.z.reshape(1, -1))
-        b = _engine.detect_batch(s, lat.M, z, 1, 1, rows, _kbound(gamma), 1.0, theta0=theta,
-                                 want_medians=False, want_hits=True)
-        hits += b.hits
-        out = torch.empty((n,), dtype=torch.complex128, device=_dev.device())
         if n:
             _native.call("sfftb_lattice_values", _dev.ptr(rows), gamma.dim, _dev.ptr(z), 1,
-                         lat.M, _dev.ptr(b.ghat), _dev.ptr(allrows), n, _dev.ptr(out),
+                         lat.M, _dev.ptr(g), _dev.ptr(allrows), n, _dev.ptr(col_buf),
                          _dev.stream())
-        vals[:, col] = out
+            vals[:n, col] = col_buf[:n]
     thr = config.nu * L
-    det = hits.to(torch.float64) >= thr
-    idx = torch.nonzero(det).flatten()
+    hits = _dev.empty((max(n, 1),), torch.int64)
+    med = _dev.zeros((max(n, 1),), torch.complex128)
+    if n:
+        _native.call("sfftb_rows_hits_medians", _dev.ptr(vals), n, L, theta, float(thr),
+                     int(bool(want_medians)), _dev.ptr(hits), _dev.ptr(med), _dev.stream())
+    hits = hits[:n]
+    mask = _dev.empty((max((n + 31) // 32, 1),), torch.int32)
+    idx = _dev.empty((max(n, 1),), torch.int64)
+    cnt = _dev.zeros((1,), torch.int64)
+    if n:
+        _native.call("sfftb_threshold_mask", _dev.ptr(hits), n, float(thr), _dev.ptr(mask),
+                     _dev.stream())
+        ws = _dev.workspace(_native.lib().sfftb_compact_workspace_bytes(1, n))
+        _native.call("sfftb_compact_mask", _dev.ptr(mask), 1, n, _dev.ptr(idx), _dev.ptr(cnt),
+                     _dev.ptr(ws), _dev.stream())
+    k = int(_dev.download(cnt)[0])
+    idx = idx[:k]
     coeffs = None
     if want_medians:
-        sel = vals[idx]
-        coeffs = torch.complex(torch.median(sel.real, dim=1).values,
-                               torch.median(sel.imag, dim=1).values)
-    return _engine.Batch(1, L, 0, n, None, theta, hits, idx,
-                         torch.tensor([idx.numel()], device=_dev.device()), coeffs)
+        coeffs = _dev.empty((max(k, 1),), torch.complex128)
+        if k:
+            _native.call("sfftb_gather_rows", _dev.ptr(med.view(torch.int64).view(-1, 2)), 2,
+                         _dev.ptr(idx), _dev.ptr(cnt), k, _dev.ptr(coeffs), _dev.stream())
+        coeffs = coeffs[:k]
+    return _engine.Batch(1, L, 0, n, None, _theta_tensor(theta), hits, idx, cnt, coeffs)
 
 
 def _result_from_batch(gamma, b, theta0, with_coeffs):

@@ -226,3 +226,32 @@ def test_topk_grid_path_multi_group_vs_oracle(cuda, oracle_lib):
             assert kc[g] == len(want_i)
             assert np.array_equal(ki[g * cap: g * cap + kc[g]], want_i)
             assert np.array_equal(kk[g * cap: g * cap + kc[g]], want_c)
+
+
+@pytest.mark.parametrize("Ms", [(211, 223, 227, 229, 233), (97, 101, 103, 107)])
+def test_distinct_lattice_sizes_vs_oracle(cuda, oracle_lib, Ms):
+    """Configurations whose lattices have different sizes (the reference's
+    numpy path, detect.py:134-145): hits by hypot, np.median coefficients."""
+    pkg, port = cuda, oracle_lib
+    rng = np.random.default_rng(len(Ms))
+    d = 3
+    gamma = np.unique(rng.integers(-20, 21, size=(3000, d)), axis=0)
+    S = pkg.FreqSet(d, gamma, _sorted=True)
+    sup = np.sort(rng.choice(len(gamma), size=15, replace=False))
+    p = pkg.SparsePoly(S.take(sup), rng.normal(size=15) + 1j * rng.normal(size=15))
+    zmat = np.vstack([rng.integers(0, M, size=d) for M in Ms])
+    cfg = pkg.MultiLatticeConfig([pkg.Rank1Lattice(z, M) for z, M in zip(zmat, Ms)], 0.5, 10.33,
+                                 0.5)
+    assert cfg.shared_M is None
+    orc = pkg.oracle_from_poly(p)
+    smp = [orc.sample_lattice(lat) for lat in cfg.lattices]
+    fr = pkg.detect_frequencies(smp, cfg, S)
+    theta0 = fr.theta_zero
+    hits, med, thr = port.gather_mixed(smp, Ms, zmat, gamma, theta0, 0.5, len(Ms) % 2 == 1)
+    assert np.array_equal(fr.hits, hits)
+    assert np.array_equal(fr.detected_idx, np.flatnonzero(hits >= thr))
+    if len(Ms) % 2 == 1:
+        res = pkg.detect_and_compute(smp, cfg, S)
+        idx = np.flatnonzero(hits >= thr)
+        assert np.array_equal(res.detected_idx, idx)
+        assert np.max(np.abs(res.coeffs - med[idx]), initial=0.0) < 1e-12
