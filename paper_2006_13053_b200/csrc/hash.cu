@@ -79,6 +79,39 @@ __device__ __forceinline__ uint32_t probe_slot(uint32_t slot, uint32_t r) {
     return __funnelshift_r(w, w, r) & 1u;
 }
 
+// The probed words themselves (bit r & 31 is the answer): the caller shifts
+// that bit into a per-row bit accumulator instead of adding it.
+__device__ __forceinline__ uint32_t word_slot(uint32_t slot, uint32_t r) {
+    uint32_t w;
+    asm volatile("{\n\t.reg .u32 a;\n\t"
+                 "shr.u32 a, %1, 3;\n\t"
+                 "lop3.b32 a, a, 0xFFFFFFFC, %2, 0xEA;\n\t"
+                 "ld.shared.u32 %0, [a];\n\t}"
+                 : "=r"(w)
+                 : "r"(r), "r"(slot));
+    return w;
+}
+
+__device__ __forceinline__ uint32_t word_bit(uint32_t base, uint32_t r) {
+    uint32_t w;
+    asm volatile("{\n\t.reg .u32 a;\n\t"
+                 "shr.u32 a, %1, 5;\n\t"
+                 "shl.b32 a, a, 2;\n\t"
+                 "add.u32 a, a, %2;\n\t"
+                 "ld.shared.u32 %0, [a];\n\t}"
+                 : "=r"(w)
+                 : "r"(r), "r"(base));
+    return w;
+}
+
+// acc' = (acc << 1) | bit r of w: rotate bit r to position 31, funnel it in --
+// two shifts on the ALU pipe (the per-lattice hit add would otherwise be an
+// IMAD on the already saturated FMA-heavy pipe); popc every 32 lattices.
+__device__ __forceinline__ uint32_t shift_in_bit(uint32_t acc, uint32_t w, uint32_t r) {
+    const uint32_t rot = __funnelshift_l(w, w, ~r);  // rotate left by 31 - (r & 31)
+    return __funnelshift_l(rot, acc, 1);
+}
+
 // Bit r of the bitmap at shared address `base`: word (r >> 5), bit r & 31.
 __device__ __forceinline__ uint32_t probe_bit(uint32_t base, uint32_t r) {
     uint32_t w;
@@ -232,8 +265,13 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
             }
         }
         int hits[R];
+        uint32_t bacc[R];
+        int nbits = 0;
 #pragma unroll
-        for (int q = 0; q < R; ++q) hits[q] = 0;
+        for (int q = 0; q < R; ++q) {
+            hits[q] = 0;
+            bacc[q] = 0;
+        }
 
         for (int c = 0; c < nchunks; ++c) {
             const int64_t qq = resident ? 0 : qc;
@@ -270,7 +308,16 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
                             acc += (uint64_t)ku[WIDE ? q : 0][WIDE ? j : 0] * (uint32_t)zr[j];
                         r = (uint32_t)mod_u64(acc, (uint64_t)a.M, invM);
                     }
-                    hits[q] += SLOT ? probe_slot(lb, r) : probe_bit(lb, r);
+                    const uint32_t w = SLOT ? word_slot(lb, r) : word_bit(lb, r);
+                    bacc[q] = shift_in_bit(bacc[q], w, r);
+                }
+                if (++nbits == 32) {
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        hits[q] += __popc(bacc[q]);
+                        bacc[q] = 0;
+                    }
+                    nbits = 0;
                 }
             }
             if (!resident) {
@@ -279,6 +326,8 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
                 ++qc;
             }
         }
+#pragma unroll
+        for (int q = 0; q < R; ++q) hits[q] += __popc(bacc[q]);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             const int64_t i = base + q * 32 + lane;
