@@ -104,12 +104,13 @@ __device__ __forceinline__ uint32_t word_bit(uint32_t base, uint32_t r) {
     return w;
 }
 
-// acc' = (acc << 1) | bit r of w: rotate bit r to position 31, funnel it in --
-// two shifts on the ALU pipe (the per-lattice hit add would otherwise be an
-// IMAD on the already saturated FMA-heavy pipe); popc every 32 lattices.
+// acc' = (acc >> 1) | (bit r of w) << 31: rotate bit r down to position 0,
+// funnel it in from the top -- two shifts on the ALU pipe (the per-lattice hit
+// add would otherwise be an IMAD on the already saturated FMA-heavy pipe);
+// popc every 32 lattices.
 __device__ __forceinline__ uint32_t shift_in_bit(uint32_t acc, uint32_t w, uint32_t r) {
-    const uint32_t rot = __funnelshift_l(w, w, ~r);  // rotate left by 31 - (r & 31)
-    return __funnelshift_l(rot, acc, 1);
+    const uint32_t rot = __funnelshift_r(w, w, r);  // bit r & 31 -> bit 0
+    return __funnelshift_r(acc, rot, 1);            // (rot:acc) >> 1
 }
 
 // Bit r of the bitmap at shared address `base`: word (r >> 5), bit r & 31.
