@@ -462,13 +462,30 @@ def cpu_hash_bounded(rows_host, zmat, M, ghat, theta0, workers, budget_s=8.0):
 
 # ---------------------------------------------------------------------------
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch from the committed ncu capture
+    (profiles/r01/traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                        "traffic.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f)[kernel]
+        return ent
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_hash(h, peak, src):
     """Algorithmic bytes of one hashing launch: rows (n*8d) + int64 hits
     (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8)."""
     bytes_ = h["n"] * 8 * h["d"] + h["n"] * 8 + h["L"] * h["W"] * 4 + h["n"] // 8
     ach = bytes_ / (h["hash_ms"] * 1e-3) / 1e9
+    tr = measured_traffic("hash_rows")
+    traffic = None
+    if tr and tr.get("rows") == h["n"] and tr.get("L") == h["L"] and tr.get("M") == h["M"]:
+        traffic = tr["dram_read"] + tr["dram_write"]
     return {"bound": "hbm", "kernel": "hash_rows (sfftb_hash_hits)", "achieved": round(ach, 1),
-            "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+            "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
             "algorithmic_bytes": bytes_, "peak_source": src,
             "launch_ms": round(h["hash_ms"], 4)}
 
@@ -523,6 +540,10 @@ def roofline_sfft(r, peak, src):
         flops += rows * 2 * (2 * fft_flops(N) + 3 * 6 * 2 * N)
     t = sum(tms)
     ach = bytes_ / (t * 1e-3) / 1e9
+    tr = measured_traffic("sample_detect_dft")
+    if tr:  # per call at the dominant stage shape (185 lattices, M = 20663)
+        out["traffic"] = tr["dram_read"] + tr["dram_write"]
+        out["traffic_shape"] = f"{tr['lattices']} lattices, M={tr['M']}, N={tr['N']}"
     out.update({"kernel": "sfftb_sample_detect_dft (fs2_colA/rowB/colCA/rowB/colC_bits)",
                 "calls": len(tms), "ms_total": round(t, 3),
                 "share_of_step": round(t / r["ms"], 3),
