@@ -54,22 +54,24 @@ class Arena:
 
     def get(self, name, numel, dtype=torch.int64, pinned=False):
         numel = max(int(numel), 1)
-        buf = self._bufs.get(name)
+        ent = self._bufs.get(name)
+        # a name is one buffer kind: never reinterpret another dtype / memory
+        buf = ent[0] if ent is not None and ent[1] == dtype and ent[2] == pinned else None
         if buf is None or buf.numel() < numel:
             grow = numel if buf is None else max(numel, buf.numel() * 5 // 4)
             if pinned:
                 buf = torch.empty(grow, dtype=dtype, pin_memory=True)
             else:
                 buf = torch.empty(grow, dtype=dtype, device=_dev.device())
-            self._bufs[name] = buf
+            self._bufs[name] = (buf, dtype, pinned)
         return buf[:numel]
 
     def ptr(self, name, numel, dtype=torch.int64):
         """Device address of a buffer of >= numel elements (no view built)."""
-        buf = self._bufs.get(name)
-        if buf is None or buf.numel() < numel or buf.dtype != dtype:
-            buf = self.get(name, numel, dtype)
-        return buf.data_ptr()
+        ent = self._bufs.get(name)
+        if ent is None or ent[1] != dtype or ent[2] or ent[0].numel() < numel:
+            return self.get(name, numel, dtype).data_ptr()
+        return ent[0].data_ptr()
 
     def bytes(self, name, nbytes):
         return self.ptr(name, (int(nbytes) + 7) // 8)
