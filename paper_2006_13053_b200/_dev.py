@@ -85,7 +85,15 @@ def upload(arr, dtype=None):
 
 
 def download(t):
-    return t.detach().cpu().numpy()
+    """Device tensor -> numpy.  Large results go through a pinned staging
+    buffer (the numpy array views it): a pageable D2H copy runs at ~2 GB/s on
+    the B200 boxes, a pinned one at ~55 GB/s (tools/micro/h2d_bw.py)."""
+    t = t.detach()
+    if t.is_cuda and t.numel() * t.element_size() >= (1 << 20):
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t)
+        return out.numpy()
+    return t.cpu().numpy()
 
 
 def empty(shape, dtype):
