@@ -116,6 +116,55 @@ def gather(ghat, theta0, bits, M, zmat, G, L, rows, kbound, nu, want_medians=Tru
     return Batch(G, L, M, n, ghat, theta0, hits, idx, counts, coeffs)
 
 
+def gather_streamed(ghat, theta0, bits, M, zmat, L, host_rows, kbound, nu, want_medians=True,
+                    want_hits=False, chunk_rows=1 << 22):
+    """gather() for one group whose candidate rows are still on the host:
+    the rows go up in chunks on a copy stream while each landed chunk is
+    hashed on the compute stream (PCIe and hashing overlap); compaction and
+    medians follow on the whole set.  Returns (Batch, device rows)."""
+    n, d = int(host_rows.shape[0]), int(host_rows.shape[1])
+    st = _dev.stream()
+    dev = _dev.device()
+    rows = torch.empty((max(n, 1), d), dtype=torch.int64, device=dev)
+    src = torch.from_numpy(host_rows)
+    nwords = (n + 31) // 32
+    detmask = _dev.empty((max(nwords, 1),), torch.int32)
+    hits = _dev.empty((max(n, 1),), torch.int64) if want_hits else None
+    min_hits = min_hits_for(nu, L)
+    copy = torch.cuda.Stream(device=dev)
+    main = torch.cuda.current_stream(dev)
+    copy.wait_stream(main)  # the buffers above were allocated on the main stream
+    for c0 in range(0, n, chunk_rows):
+        c1 = min(n, c0 + chunk_rows)
+        with torch.cuda.stream(copy):
+            rows[c0:c1].copy_(src[c0:c1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        main.wait_event(ev)
+        _native.call("sfftb_hash_hits", rows[c0:c1].data_ptr(), c1 - c0, d, _dev.ptr(zmat), 1, L,
+                     M, _dev.ptr(bits), int(kbound), min_hits,
+                     None if hits is None else hits[c0:c1].data_ptr(),
+                     detmask[c0 // 32:].data_ptr(), st)
+    rows.record_stream(copy)
+    src_keep = src  # the host rows must outlive the async copies: synchronise below
+    idx = _dev.empty((max(n, 1),), torch.int64)
+    counts = _dev.zeros((1,), torch.int64)
+    if n:
+        ws = _dev.workspace(_native.lib().sfftb_compact_workspace_bytes(1, n))
+        _native.call("sfftb_compact_mask", _dev.ptr(detmask), 1, n, _dev.ptr(idx),
+                     _dev.ptr(counts), _dev.ptr(ws), st)
+    coeffs = None
+    if want_medians:
+        coeffs = _dev.empty((max(n, 1),), torch.complex128)
+        if n:
+            _native.call("sfftb_medians", _dev.ptr(rows), d, _dev.ptr(zmat), 1, L, M,
+                         _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(counts), n, _dev.ptr(coeffs),
+                         st)
+    copy.synchronize()
+    del src_keep
+    return Batch(1, L, M, n, ghat, theta0, hits, idx, counts, coeffs), rows[:n]
+
+
 def detect_batch(samples, M, zmat, G, L, rows, kbound, nu, theta0=None,
                  want_medians=True, want_hits=False):
     """Run the full detection chain on device tensors.

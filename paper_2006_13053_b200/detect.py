@@ -168,6 +168,11 @@ def default_zero_test(samples):
     return _zero_from_device([_dev.upload(r).reshape(1, -1) for r in rows])
 
 
+# host-resident candidate sets at least this large are uploaded in chunks
+# overlapped with hashing (_engine.gather_streamed)
+STREAM_UPLOAD_BYTES = 256 << 20
+
+
 def _kbound(gamma):
     return gamma.memo("kbound", gamma.kbound)
 
@@ -185,6 +190,17 @@ def _gather(samples, config, gamma, zero, want_medians, want_hits=True):
         raise ParameterError("lattice size too large for int64 residues")
     if config.dim != gamma.dim:
         raise ParameterError("candidate set/lattice dimension mismatch")
+    host = gamma._host if gamma._dev is None else None
+    if host is not None and host.nbytes >= STREAM_UPLOAD_BYTES:
+        # large host-resident candidate set: upload in chunks, overlapped with
+        # the hashing of the chunks already on the device
+        ghat, theta0, bits = _engine.spectra(samples, M, 1, config.L,
+                                             _theta_tensor(zero.theta_zero))
+        b, rows = _engine.gather_streamed(ghat, theta0, bits, M, config.zmat_device(),
+                                          config.L, host, _kbound(gamma), config.nu,
+                                          want_medians=want_medians, want_hits=want_hits)
+        gamma._dev = rows  # cached like FreqSet.device()
+        return b
     return _engine.detect_batch(samples, M, config.zmat_device(), 1, config.L,
                                 gamma.device(), _kbound(gamma), config.nu,
                                 theta0=_theta_tensor(zero.theta_zero),

@@ -255,3 +255,32 @@ def test_distinct_lattice_sizes_vs_oracle(cuda, oracle_lib, Ms):
         idx = np.flatnonzero(hits >= thr)
         assert np.array_equal(res.detected_idx, idx)
         assert np.max(np.abs(res.coeffs - med[idx]), initial=0.0) < 1e-12
+
+
+def test_streamed_upload_matches_resident(cuda, monkeypatch):
+    """Host-resident candidate sets above the streaming threshold are uploaded
+    in chunks overlapped with hashing; results equal the resident path."""
+    import paper_2006_13053_b200.detect as det
+
+    pkg = cuda
+    rng = np.random.default_rng(21)
+    d, n = 6, 300_000
+    gamma = np.unique(rng.integers(-500, 501, size=(n, d)), axis=0)
+    sup = np.sort(rng.choice(len(gamma), size=200, replace=False))
+    S_dev = pkg.FreqSet(d, gamma, _sorted=True)
+    S_dev.device()
+    p = pkg.SparsePoly(S_dev.take(sup), rng.normal(size=200) + 1j * rng.normal(size=200) + 2)
+    cfg = pkg.draw_config(S_dev, 200, 0.1, rng=np.random.default_rng(3))
+    smp = [pkg.oracle_from_poly(p).sample_lattice(lat) for lat in cfg.lattices]
+    want = pkg.detect_and_compute(smp, cfg, S_dev)
+    monkeypatch.setattr(det, "STREAM_UPLOAD_BYTES", 1 << 20)
+    from paper_2006_13053_b200 import _engine
+    monkeypatch.setattr(_engine.gather_streamed, "__defaults__",
+                        (True, False, 1 << 15))  # many chunks
+    S_host = pkg.FreqSet(d, gamma, _sorted=True)
+    got = pkg.detect_and_compute(smp, cfg, S_host)
+    assert S_host._dev is not None  # cached by the streamed path
+    assert np.array_equal(got.hits, want.hits)
+    assert np.array_equal(got.detected_idx, want.detected_idx)
+    assert np.array_equal(got.coeffs, want.coeffs)
+    assert np.array_equal(got.detected_idx, sup)
