@@ -162,6 +162,16 @@ int sfftb_compact_mask(const uint32_t *mask, int64_t G, int64_t n, int64_t *idx,
                        int64_t *counts, void *ws, void *stream);
 
 /*
+ * sfftb_compact_mask with at most cap indices kept per group: idx[g*cap + k],
+ * counts[g] = min(set bits, cap), totals[g] = set bits (totals may be NULL).
+ * Same workspace.  Used by batched trials whose detected sets are far
+ * smaller than the candidate set (analysis.py:218-250).
+ */
+int sfftb_compact_mask_cap(const uint32_t *mask, int64_t G, int64_t n,
+                           int64_t cap, int64_t *idx, int64_t *counts,
+                           int64_t *totals, void *ws, void *stream);
+
+/*
  * Distinct lattice sizes (detect.py:134-145): for each row of vals (n, L)
  * complex128, hits[i] = #{l: hypot(vals[i, l]) > theta} and, when
  * want_medians and hits[i] >= thr, medians[i] = np.median of the real and
@@ -425,6 +435,53 @@ typedef struct {
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Experiment harness (csrc/analysis.cu; reference latfft/analysis.py and
+ * the f10 test function of polyeval.py:216-277).
+ * ------------------------------------------------------------------- */
+
+/*
+ * mask bit i = (rows[i] is a row of pool), pool lexicographically sorted and
+ * duplicate-free (FreqSet.contains_rows, freqset.py:139-142).  Device.
+ */
+int sfftb_rows_in_sorted(const int64_t *rows, int64_t n, int64_t d,
+                         const int64_t *pool, int64_t m, uint32_t *mask,
+                         void *stream);
+
+/*
+ * Alias classification of pfp_pfn_count (analysis.py:67-104) for G groups of
+ * detected rows idx/med[g*cap + k], k < counts[g], against in_mask (bit per
+ * candidate: member of I).  rounded = rint(Re), integral = |Re - rounded| <=
+ * tol and |Im| <= tol.  tallies[g*5 + c]: c = 0 detected & in_I, 1 not
+ * integral, 2 integral & rounded < 1, 3 pfn (in_I & rounded >= 2), 4 pfp
+ * (not in_I & rounded >= 1).  cls[g*cap + k] (may be NULL): bit 0 = in_I,
+ * bits 1-3 = 0 clean, 1 not integral, 2 rounded < 1, 3 pfn, 4 pfp.
+ */
+int sfftb_alias_classify(const int64_t *idx, const double *med,
+                         const int64_t *counts, int64_t G, int64_t cap,
+                         const uint32_t *in_mask, double tol, uint8_t *cls,
+                         int64_t *tallies, void *stream);
+
+/*
+ * Sum over groups of products of periodised B-splines (f10_values,
+ * polyeval.py:261-272): value(x) = sum_g prod_{a: axis_group[a] == g}
+ * scale[g] * N_{order[g]}(x_a), N_m the centred cardinal B-spline of
+ * bspline_values (polyeval.py:216-225) without its prefactor scale = C_m * m.
+ * axis_group[a] = -1 leaves axis a out.  d <= 32, ngroups <= 8.
+ * _lattice: out (G*L, M) complex128 at the nodes [(j z mod M)/M | tail_g]
+ * (zmat (G*L, t_dim), tails (G, max(d - t_dim, 1))).  _points: out (m,) at X
+ * (m, d).  Device.
+ */
+int sfftb_spline_sum_lattice(int64_t d, const int32_t *axis_group,
+                             int64_t ngroups, const int32_t *order,
+                             const double *scale, const int64_t *zmat,
+                             int64_t G, int64_t L, int64_t M, int64_t t_dim,
+                             const double *tails, double *out, void *stream);
+int sfftb_spline_sum_points(int64_t d, const int32_t *axis_group,
+                            int64_t ngroups, const int32_t *order,
+                            const double *scale, const double *X, int64_t m,
+                            double *out, void *stream);
 
 /* ---------------------------------------------------------------------
  * Host seed streams (csrc/hostrng.cpp): numpy Generator(PCG64(SeedSequence(

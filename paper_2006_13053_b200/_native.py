@@ -79,6 +79,12 @@ _SIGS = {
     "sfftb_r1l_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "sfftb_postprocess_r1l": (_int, [_p, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _dbl, _p, _p,
                                      _p, _p]),
+    "sfftb_compact_mask_cap": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
+    "sfftb_rows_in_sorted": (_int, [_p, _i64, _i64, _p, _i64, _p, _p]),
+    "sfftb_alias_classify": (_int, [_p, _p, _p, _i64, _i64, _p, _dbl, _p, _p, _p]),
+    "sfftb_spline_sum_lattice": (_int, [_i64, _p, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _p,
+                                        _p, _p]),
+    "sfftb_spline_sum_points": (_int, [_i64, _p, _i64, _p, _p, _p, _i64, _p, _p]),
     "sfftb_pcg64_seed": (_int, [_p, _i64, _i64, _p]),
     "sfftb_pcg64_random": (_int, [_p, _i64, _i64, _p]),
     "sfftb_pcg64_integers": (_int, [_p, _i64, _i64, _i64, _i64, _p]),

@@ -437,7 +437,8 @@ __global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
     if (threadIdx.x == 0) blocksum[(int64_t)g * nblk + blockIdx.x] = red[0];
 }
 
-__global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts) {
+__global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts, int64_t cap,
+                             int64_t* totals) {
     const int g = blockIdx.x;
     if (threadIdx.x != 0) return;
     int64_t run = 0;
@@ -446,7 +447,8 @@ __global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts) {
         blocksum[(int64_t)g * nblk + b] = run;
         run += v;
     }
-    counts[g] = run;
+    counts[g] = min(run, cap);
+    if (totals) totals[g] = run;
 }
 
 // SINGLE: one CTA per group walks all words with a running carry and writes
@@ -456,7 +458,7 @@ template <bool SINGLE, int NT = kCompactThreads>
 __global__ void __launch_bounds__(NT)
     compact_write(const uint32_t* __restrict__ mask, int64_t nwords, int64_t n, int64_t nblk,
                   const int64_t* __restrict__ blocksum, int64_t* __restrict__ idx,
-                  int64_t* __restrict__ counts) {
+                  int64_t* __restrict__ counts, int64_t cap, int64_t* __restrict__ totals) {
     const int g = blockIdx.y;
     const int64_t w0 = SINGLE ? 0 : blockIdx.x * (int64_t)kCompactWordsPerBlock;
     const int64_t wend = SINGLE ? nwords : min(nwords, w0 + kCompactWordsPerBlock);
@@ -485,7 +487,10 @@ __global__ void __launch_bounds__(NT)
             const int bit = __ffs(b) - 1;
             b &= b - 1;
             const int64_t row = w * 32 + bit;
-            if (row < n) idx[(int64_t)g * n + pos++] = row;
+            if (row < n) {
+                if (pos < cap) idx[(int64_t)g * cap + pos] = row;
+                ++pos;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -495,7 +500,10 @@ __global__ void __launch_bounds__(NT)
         }
         __syncthreads();
     }
-    if (SINGLE && threadIdx.x == 0) counts[g] = carry;
+    if (SINGLE && threadIdx.x == 0) {
+        counts[g] = min(carry, cap);
+        if (totals) totals[g] = carry;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1131,28 +1139,34 @@ extern "C" int64_t sfftb_compact_workspace_bytes(int64_t G, int64_t n) {
     return G * nblk * (int64_t)sizeof(int64_t);
 }
 
-extern "C" int sfftb_compact_mask(const uint32_t* mask, int64_t G, int64_t n, int64_t* idx,
-                                  int64_t* counts, void* ws, void* stream) {
-    SFFTB_REQUIRE(G >= 1 && n >= 0 && G <= 65535, "compact: bad sizes");
+extern "C" int sfftb_compact_mask_cap(const uint32_t* mask, int64_t G, int64_t n, int64_t cap,
+                                      int64_t* idx, int64_t* counts, int64_t* totals, void* ws,
+                                      void* stream) {
+    SFFTB_REQUIRE(G >= 1 && n >= 0 && G <= 65535 && cap >= 0, "compact: bad sizes");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nwords = (n + 31) / 32;
     const int64_t nblk = std::max<int64_t>(1, ceil_div(nwords, kCompactWordsPerBlock));
     int64_t* bs = (int64_t*)ws;
     if (nwords <= kCompactSingleWords) {
         compact_write<true, 1024><<<dim3(1, (unsigned)G), 1024, 0, st>>>(
-            mask, nwords, n, 1, nullptr, idx, counts);
+            mask, nwords, n, 1, nullptr, idx, counts, cap, totals);
         SFFTB_CHECK_LAUNCH();
         return SFFTB_OK;
     }
     compact_count<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(mask, nwords,
                                                                                  nblk, bs);
     SFFTB_CHECK_LAUNCH();
-    compact_scan<<<(unsigned)G, 32, 0, st>>>(bs, nblk, counts);
+    compact_scan<<<(unsigned)G, 32, 0, st>>>(bs, nblk, counts, cap, totals);
     SFFTB_CHECK_LAUNCH();
     compact_write<false><<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(
-        mask, nwords, n, nblk, bs, idx, counts);
+        mask, nwords, n, nblk, bs, idx, counts, cap, totals);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
+}
+
+extern "C" int sfftb_compact_mask(const uint32_t* mask, int64_t G, int64_t n, int64_t* idx,
+                                  int64_t* counts, void* ws, void* stream) {
+    return sfftb_compact_mask_cap(mask, G, n, n, idx, counts, nullptr, ws, stream);
 }
 
 extern "C" int sfftb_medians(const int64_t* elems, int64_t d, const int64_t* zmat, int64_t G,

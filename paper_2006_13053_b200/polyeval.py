@@ -267,3 +267,212 @@ def random_poly(I, rng, min_mag=1e-6):
         coeffs[todo] = vals
         todo = todo[np.abs(vals) < min_mag]
     return SparsePoly(I, coeffs)
+
+
+# ---------------------------------------------------------------------------
+# periodised B-splines and the ten-variate test function f10
+# (polyeval.py:160-350).  Function values are computed on the device
+# (csrc/analysis.cu, sfftb_spline_sum_*); the closed-form Fourier
+# coefficients and norms below are scalar host formulas of the error metric.
+# ---------------------------------------------------------------------------
+
+import math as _math
+
+_BSPLINE_NORM_CACHE = {}
+
+#: (axes, spline order) of the three tensor-product summands (0-based axes)
+F10_GROUPS = (((0, 2, 7), 2), ((1, 4, 5, 9), 4), ((3, 6, 8), 6))
+F10_DIM = 10
+
+
+def _sinc(t):
+    out = np.ones_like(t)
+    nz = t != 0
+    out[nz] = np.sin(t[nz]) / t[nz]
+    return out
+
+
+def bspline_norm_constant(m):
+    """C_m = (sum_k sinc(pi k / m)^(2m))^(-1/2), truncated at |k| <=
+    max(1e5, 1000 m) and summed smallest-first (polyeval.py:175-190)."""
+    m = int(m)
+    if m < 1:
+        raise ParameterError("spline order must be >= 1")
+    if m not in _BSPLINE_NORM_CACHE:
+        horizon = max(100_000, 1000 * m)
+        k = np.arange(1, horizon + 1, dtype=np.float64)
+        s = _sinc(np.pi * k / m) ** (2 * m)
+        total = 1.0 + 2.0 * float(np.sum(s[::-1]))
+        _BSPLINE_NORM_CACHE[m] = total ** -0.5
+    return _BSPLINE_NORM_CACHE[m]
+
+
+def bspline_coeffs(m, ks):
+    """Fourier coefficients C_m sinc(pi k / m)^m (-1)^k (polyeval.py:198-203)."""
+    ks = np.asarray(ks, dtype=np.int64)
+    c = bspline_norm_constant(m)
+    vals = c * _sinc(np.pi * ks / m) ** m
+    vals[ks % 2 == 1] *= -1.0
+    return vals
+
+
+def bspline_coeff(m, k):
+    return float(bspline_coeffs(m, np.asarray([k]))[0])
+
+
+class SplineSum:
+    """sum over groups of tensor products of periodised unit-norm B-splines,
+    evaluated on the device (one kernel over all points / lattice nodes)."""
+
+    __slots__ = ("dim", "groups", "_axis", "_order", "_scale")
+
+    def __init__(self, dim, groups):
+        self.dim = int(dim)
+        self.groups = tuple((tuple(int(a) for a in axes), int(m)) for axes, m in groups)
+        axis = np.full(self.dim, -1, dtype=np.int32)
+        for g, (axes, _) in enumerate(self.groups):
+            for a in axes:
+                if not 0 <= a < self.dim or axis[a] != -1:
+                    raise ParameterError("spline groups must be disjoint axes of the domain")
+                axis[a] = g
+            if list(axes) != sorted(axes):
+                raise ParameterError("spline group axes must be ascending")
+        self._axis = axis
+        self._order = np.array([m for _, m in self.groups], dtype=np.int32)
+        self._scale = np.array([bspline_norm_constant(m) * m for _, m in self.groups],
+                               dtype=np.float64)
+
+    def _args(self):
+        return (self.dim, self._axis.ctypes.data, len(self.groups), self._order.ctypes.data,
+                self._scale.ctypes.data)
+
+    def points_device(self, X_dev):
+        """(m,) complex128 device values at the rows of a (m, dim) device tensor."""
+        X_dev = X_dev.to(torch.float64).contiguous()
+        m = int(X_dev.shape[0])
+        out = _dev.empty((max(m, 1),), torch.complex128)
+        _native.call("sfftb_spline_sum_points", *self._args(), _dev.ptr(X_dev), m,
+                     _dev.ptr(out), _dev.stream())
+        return out[:m]
+
+    def lattice_device(self, zmat_dev, M, tails_dev, G, L, t_dim):
+        """(G*L, M) complex128 values at [(j z mod M)/M | tail_g] (dimincr.py:186-191)."""
+        out = _dev.empty((G * L, M), torch.complex128)
+        _native.call("sfftb_spline_sum_lattice", *self._args(), _dev.ptr(zmat_dev), G, L, M,
+                     t_dim, _dev.ptr(tails_dev), _dev.ptr(out), _dev.stream())
+        return out
+
+
+def bspline_values(m, x):
+    """N_m at torus points x (polyeval.py:216-225), on the device."""
+    x = np.asarray(x, dtype=np.float64)
+    f = SplineSum(1, (((0,), int(m)),))
+    vals = _dev.download(f.points_device(_dev.upload(x.reshape(-1, 1))))
+    return vals.real.reshape(x.shape)
+
+
+_F10 = None
+
+
+def _f10():
+    global _F10
+    if _F10 is None:
+        _F10 = SplineSum(F10_DIM, F10_GROUPS)
+    return _F10
+
+
+def f10_values(X):
+    """Test-function values at an (m, 10) array of torus points (polyeval.py:261-272)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[1] != F10_DIM:
+        raise ParameterError("points must be an (m, 10) array")
+    return _dev.download(_f10().points_device(_dev.upload(X))).real
+
+
+class SplineOracle(SamplingOracle):
+    """Black-box oracle of a SplineSum whose evaluations run on the device:
+    sample_many / sample_lattice evaluate at the given points, and the sfft
+    driver's batched fixed-tail lattice samplings (sample_lattices_device)
+    never leave the GPU.  Counts advance like the reference's
+    SamplingOracle (polyeval.py:107-130)."""
+
+    __slots__ = ("spline",)
+
+    def __init__(self, spline):
+        super().__init__(self._host_fn, spline.dim)
+        self.spline = spline
+
+    def _host_fn(self, X):
+        return _dev.download(self.spline.points_device(_dev.upload(np.asarray(X, np.float64))))
+
+    def sample_lattices_device(self, zmat_dev, M, tails_dev, G, L, t_dim):
+        vals = self.spline.lattice_device(zmat_dev, M, tails_dev, G, L, t_dim)
+        self.count += G * L * M
+        return vals
+
+
+def f10_oracle():
+    """SamplingOracle of f10 (polyeval.py:275-277), sampled on the device."""
+    return SplineOracle(_f10())
+
+
+def _summand_coeffs(elems, axes, m):
+    """Coefficients of one tensor-product summand: the product of its axes'
+    spline coefficients where every other component is zero, else 0."""
+    vals = np.zeros(elems.shape[0])
+    on = ~np.delete(elems, list(axes), axis=1).any(axis=1)
+    if on.any():
+        cols = np.stack([bspline_coeffs(m, elems[on, a]) for a in axes], axis=1)
+        vals[on] = np.multiply.reduce(cols, axis=1)
+    return vals
+
+
+def f10_coeffs(elems):
+    """Exact Fourier coefficients of f10 at (n, 10) indices (polyeval.py:280-300):
+    the groups use disjoint axes, so only k = 0 collects more than one summand."""
+    elems = np.asarray(elems, dtype=np.int64)
+    if elems.ndim != 2 or elems.shape[1] != F10_DIM:
+        raise ParameterError("indices must be an (n, 10) array")
+    total = np.zeros(elems.shape[0])
+    for axes, m in F10_GROUPS:
+        total = total + _summand_coeffs(elems, axes, m)
+    return total
+
+
+def f10_coeff(k):
+    k = np.asarray(k, dtype=np.int64)
+    if k.shape != (F10_DIM,):
+        raise ParameterError("index must have 10 components")
+    return float(f10_coeffs(k.reshape(1, F10_DIM))[0])
+
+
+def f10_sq_norm():
+    """||f10||^2 (polyeval.py:310-322): each summand has unit norm and two
+    summands overlap only in their k = 0 coefficient C_m^|axes|."""
+    from itertools import combinations
+
+    zero_coeff = [bspline_norm_constant(m) ** len(axes) for axes, m in F10_GROUPS]
+    total = float(len(zero_coeff))
+    for a, b in combinations(zero_coeff, 2):
+        total += 2.0 * a * b
+    return total
+
+
+def rel_l2_error(I, coeffs, f_sq_norm, f_coeff_fn):
+    """||f - sum_{k in I} c_k e_k|| / ||f|| by Parseval (polyeval.py:325-347):
+    ||f||^2 - sum_I |f_k|^2 + sum_I |c_k - f_k|^2, clamped at 0 for roundoff,
+    ParameterError when it is clearly negative."""
+    if f_sq_norm <= 0:
+        raise ParameterError("f_sq_norm must be positive")
+    if isinstance(coeffs, dict):
+        coeffs = [coeffs[k] for k in I]
+    c = np.asarray(coeffs, dtype=np.complex128)
+    if c.shape != (len(I),):
+        raise ParameterError("need one coefficient per frequency")
+    rad = f_sq_norm
+    if len(I):
+        fk = np.asarray(f_coeff_fn(I.elems), dtype=np.complex128)
+        rad = f_sq_norm - float(np.sum(np.abs(fk) ** 2)) + float(np.sum(np.abs(c - fk) ** 2))
+    if rad < -1e-12 * f_sq_norm:
+        raise ParameterError(f"negative radicand {rad} in error formula")
+    return _math.sqrt(max(rad, 0.0) / f_sq_norm)

@@ -324,10 +324,121 @@ def gen_sfft_cfg2():
     save_sfft("sfft_cfg2", w, res, dt)
 
 
+def _ref_analysis():
+    from latfft import analysis as ran
+
+    return ran
+
+
+ANALYSIS_SPECS = {
+    # reference tests/test_analysis.py desk_spec (redraw "both", tiny M)
+    "desk": dict(name="unit", candidates={"kind": "random-box", "d": 2, "lo": -60, "hi": 60,
+                                          "count": 400},
+                 support={"kind": "random-subset", "count": 8}, L_values=[3, 9], trials=6,
+                 master_seed=99, pfp_budgets=(0, 10)),
+    # test_lattices_only_redraw_fixes_sets
+    "hc_small": dict(name="unit", candidates={"kind": "hyperbolic", "d": 3, "N": 6,
+                                              "weights": None},
+                     support={"kind": "hyperbolic", "N": 2, "weights": "t^1.08"},
+                     L_values=[5], trials=3, master_seed=99, pfp_budgets=(0, 10),
+                     redraw="lattices"),
+    # fixed sets, M in the fused-transform range: every trial of one L is one
+    # device batch
+    "hc_fused": dict(name="hc-fused", candidates={"kind": "hyperbolic", "d": 4, "N": 64,
+                                                  "weights": None},
+                     support={"kind": "hyperbolic", "N": 32, "weights": "t^1.08"},
+                     L_values=[5, 7, 9, 11, 13], trials=24, master_seed=2023,
+                     redraw="lattices"),
+    # per-trial candidate sets, fused-range M
+    "box_fused": dict(name="box-fused", candidates={"kind": "random-box", "d": 3, "lo": -200,
+                                                    "hi": 200, "count": 30000},
+                      support={"kind": "random-subset", "count": 450}, L_values=[7, 9],
+                      trials=4, master_seed=2023),
+}
+
+
+def gen_analysis():
+    """run_success_experiment records + aggregates, and pfp_pfn_count
+    classifications (reference tests/test_analysis.py recipes, scaled)."""
+    ran = _ref_analysis()
+    out = {}
+    for key, kw in ANALYSIS_SPECS.items():
+        spec = ran.ExperimentSpec(**kw)
+        t0 = time.perf_counter()
+        recs, agg = ran.run_success_experiment(spec)
+        print(f"  {key}: {len(recs)} trials in {time.perf_counter() - t0:.1f}s")
+        out[key] = {"spec": spec.as_dict(), "records": [r.as_jsonable() for r in recs],
+                    "aggregate": agg}
+    # pfp_pfn_count on explicit configurations
+    rng = np.random.default_rng(77)
+    cases = []
+    g = rfs.random_subset(rfs.Box(2, -9, 9), 30, rng)
+    I = rfs.random_subset(g, 4, rng)
+    cfg = rlat.MultiLatticeConfig([rlat.Rank1Lattice([0, 0], 47) for _ in range(3)], 0.5,
+                                  10.33, 0.5)
+    cases.append((g, I, cfg))
+    for _ in range(12):
+        d = int(rng.integers(1, 4))
+        M = int(rng.choice([11, 13, 17, 19, 23, 29, 31]))
+        box = rfs.Box(d, -4, 4)
+        g = rfs.random_subset(box, min(int(rng.integers(6, 30)), box.size), rng)
+        I = rfs.random_subset(g, int(rng.integers(1, 7)), rng)
+        L = int(rng.choice([3, 5]))
+        lats = [rlat.Rank1Lattice(rng.integers(0, M, d), M) for _ in range(L)]
+        cases.append((g, I, rlat.MultiLatticeConfig(lats, 0.5, 10.33, 0.5)))
+    for d, n, s, L in ((3, 5000, 40, 7), (4, 20000, 420, 9)):
+        g = rfs.random_subset(rfs.Box(d, -40, 40), n, rng)
+        I = rfs.random_subset(g, s, rng)
+        cases.append((g, I, rlat.draw_config(g, s, 0.5, rng=rng, L=L)))
+    arrs = {"ncases": np.array(len(cases))}
+    for k, (g, I, cfg) in enumerate(cases):
+        o = ran.pfp_pfn_count(I, g, cfg)
+        arrs.update({f"gamma_{k}": g.elems, f"I_{k}": I.elems,
+                     f"z_{k}": np.array([lat.z for lat in cfg.lattices], dtype=np.int64),
+                     f"M_{k}": np.array([lat.M for lat in cfg.lattices], dtype=np.int64),
+                     f"pfn_{k}": o.pfn.elems, f"pfp_{k}": o.pfp.elems,
+                     f"anomalies_{k}": np.array(o.anomalies)})
+    save_npz("pfp_pfn_cases", **arrs)
+    ba = {"bound": [ran.theoretical_failure_bound(1e7, L, 10.33) for L in (0, 9, 37, 41)],
+          "guaranteed": ran.guaranteed_sample_budget(1000, 10**7, 0.5)}
+    out["budgets"] = ba
+    save_json("analysis_cases", out)
+
+
+def gen_f10():
+    """B-spline / f10 values and coefficients, and one small B-spline study
+    row (reference tests/test_polyeval.py, test_analysis.py:186-194)."""
+    rng = np.random.default_rng(1010)
+    out = {"norm": {str(m): rpe.bspline_norm_constant(m) for m in (1, 2, 3, 4, 6)}}
+    x = rng.uniform(-1.5, 2.5, size=257)
+    x[:4] = [0.0, 0.5, 1.0 / 3.0, -0.25]
+    out["x"] = x.tolist()
+    out["bspline"] = {str(m): rpe.bspline_values(m, x).tolist() for m in (2, 4, 6)}
+    X = rng.uniform(0, 1, size=(300, 10))
+    out["X"] = X.tolist()
+    out["f10"] = rpe.f10_values(X).tolist()
+    K = rng.integers(-3, 4, size=(200, 10))
+    K[::3, [1, 3, 4, 5, 6, 8, 9]] = 0
+    K[1::3, [0, 2, 3, 6, 7, 8]] = 0
+    K[5] = 0
+    out["K"] = K.tolist()
+    out["f10_coeffs"] = rpe.f10_coeffs(K).tolist()
+    out["sq_norm"] = rpe.f10_sq_norm()
+    from latfft import analysis as ran
+
+    t0 = time.perf_counter()
+    rows = ran.run_bspline_experiment(4, 30, runs=1, master_seed=5, r=1, delta=0.9,
+                                      L_scale=0.5)
+    print(f"  bspline study: {time.perf_counter() - t0:.1f}s")
+    out["study"] = {"args": [4, 30, 1, 5, 1, 0.9, 0.5], "rows": rows}
+    save_json("f10_cases", out)
+
+
 GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
-       "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2}
+       "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
+       "analysis": gen_analysis, "f10": gen_f10}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(GEN)
