@@ -431,6 +431,16 @@ def gen_f10():
                                       L_scale=0.5)
     print(f"  bspline study: {time.perf_counter() - t0:.1f}s")
     out["study"] = {"args": [4, 30, 1, 5, 1, 0.9, 0.5], "rows": rows}
+    # the paper's f10 setting (N = 16, r = 5, delta = 0.999, L_scale = 1/4)
+    out["studies_paper"] = []
+    for args in ([16, 200, 1, 3, 2, 0.999, 0.25], [16, 1000, 1, 3, 5, 0.999, 0.25]):
+        N, s, runs, seed, r, delta, Ls = args
+        t0 = time.perf_counter()
+        rows = ran.run_bspline_experiment(N, s, runs=runs, master_seed=seed, r=r, delta=delta,
+                                          L_scale=Ls)
+        dt = time.perf_counter() - t0
+        print(f"  bspline study {args}: {dt:.1f}s")
+        out["studies_paper"].append({"args": args, "rows": rows, "ref_seconds": dt})
     save_json("f10_cases", out)
 
 
