@@ -965,6 +965,27 @@ static int grid_for(int64_t work, int threads) {
 // hash dispatch
 // ---------------------------------------------------------------------------
 
+// CTAs per group (grid.x): every CTA of a group strides over the same number
+// of row tiles, so the launch runs in ceil(gx*G / slots) equal waves.  Pick
+// the smallest gx >= ceil(slots/G) whose last wave is >= 95% full (e.g. G =
+// 198 trial groups on 148 SMs: gx = 7, 9.4 waves, instead of gx = 1 and a
+// one-third-full second wave).
+static int hash_grid_x(int64_t ntiles, int64_t G, int64_t slots) {
+    const int64_t lo = std::max<int64_t>(1, ceil_div(slots, G));
+    int64_t best = lo;
+    double best_eff = 0.0;
+    for (int64_t gx = lo; gx <= lo * 16 && gx <= ntiles; ++gx) {
+        const int64_t ctas = gx * G;
+        const double eff = (double)ctas / (double)(slots * ceil_div(ctas, slots));
+        if (eff > best_eff + 1e-9) {
+            best = gx;
+            best_eff = eff;
+        }
+        if (eff >= 0.95) break;
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, best));
+}
+
 template <int D, int R, bool WIDE, int NT, bool SLOT, int X>
 static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
     auto kern = hash_rows<D, R, WIDE, NT, SLOT, X>;
@@ -974,8 +995,7 @@ static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
     per_sm = std::max(per_sm, 1);
     constexpr int TILE = (NT / 32) * 32 * R;
     const int64_t ntiles = ceil_div(a.n, TILE);
-    const int64_t want = ceil_div((int64_t)num_sms() * per_sm, a.G);
-    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, want));
+    const int gx = hash_grid_x(ntiles, a.G, (int64_t)num_sms() * per_sm);
     kern<<<dim3(gx, a.G), NT, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;

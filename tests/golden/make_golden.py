@@ -405,6 +405,39 @@ def gen_analysis():
     save_json("analysis_cases", out)
 
 
+FULLSCALE_SPEC = {
+    # the paper's hyperbolic-cross worst-case study: |Gamma| = 10,665,297 (d = 8),
+    # |I| = 1069, M = 11047 (reference pkg/configs hyperbolic sweep parameters)
+    "name": "hyperbolic-fullscale", "candidates": {"kind": "hyperbolic", "d": 8, "N": 32,
+                                                   "weights": None},
+    "support": {"kind": "hyperbolic", "N": 32, "weights": "t^1.08"},
+    "L_values": [9, 37], "trials": 3, "master_seed": 2023, "redraw": "lattices",
+    "pfp_budgets": [10, 100]}
+
+
+def gen_fullscale():
+    """Three trials at L = 9 and 37 of the full-scale hyperbolic sweep, with
+    the reference's seconds per trial (its CPU cost at paper scale)."""
+    ran = _ref_analysis()
+    spec = ran.ExperimentSpec.from_dict(FULLSCALE_SPEC)
+    t0 = time.perf_counter()
+    rng = np.random.default_rng(np.random.SeedSequence((spec.master_seed, 0xFACE)))
+    gamma = ran._make_candidates(spec.candidates, rng)
+    I = ran._make_support(spec.support, gamma, rng)
+    M = ran.next_valid_prime(gamma, spec.c * len(I))
+    setup = time.perf_counter() - t0
+    recs, secs = [], []
+    for L in spec.L_values:
+        for trial in range(spec.trials):
+            t = time.perf_counter()
+            recs.append(ran._trial(spec, L, trial, (gamma, I, M)).as_jsonable())
+            secs.append(time.perf_counter() - t)
+            print(f"  L={L} trial {trial}: {secs[-1]:.1f}s")
+    save_json("analysis_fullscale", {"spec": spec.as_dict(), "records": recs,
+                                     "ref_seconds_per_trial": secs, "ref_setup_seconds": setup,
+                                     "gamma_size": len(gamma), "support_size": len(I), "M": M})
+
+
 def gen_f10():
     """B-spline / f10 values and coefficients, and one small B-spline study
     row (reference tests/test_polyeval.py, test_analysis.py:186-194)."""
@@ -448,7 +481,7 @@ GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
        "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
-       "analysis": gen_analysis, "f10": gen_f10}
+       "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(GEN)

@@ -145,3 +145,15 @@ def test_bspline_paper_setting_matches_reference(cuda, which):
     for got, want in zip(rows, st["rows"]):
         assert got["samples"] == want["samples"]
         assert got["rel_l2_error"] == pytest.approx(want["rel_l2_error"], rel=1e-6)
+
+
+def test_fullscale_hyperbolic_trials_match_reference(cuda):
+    """Paper scale: |Gamma| = 10.7M (hyperbolic cross, d = 8), |I| = 1069,
+    M = 11047; three trials each at L = 9 (about 6300 potential false
+    positives per trial) and L = 37, against the reference's records."""
+    from paper_2006_13053_b200 import analysis
+
+    case = golden("analysis_fullscale.json")
+    spec = analysis.ExperimentSpec.from_dict(case["spec"])
+    recs, _ = analysis.run_success_experiment(spec)
+    assert [r.as_jsonable() for r in recs] == case["records"]
