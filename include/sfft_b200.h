@@ -419,8 +419,9 @@ typedef struct {
     int64_t *uidx;              /* (n) */
     int64_t *ucount;            /* (1) */
     int64_t *host_counts;       /* pinned (G + 1) */
-    /* optional: 7 cudaEvent_t recorded at the phase boundaries (candidates |
-     * sampler | transforms | hashing | compaction+medians | top-s+union) */
+    /* optional: 9 cudaEvent_t recorded at the phase boundaries: candidates
+     * start, end | sampler start | transforms start, end | hashing start, end
+     * | compaction+medians end | top-s+union end */
     void *const *events;
     /* elements between consecutive groups in zmat_host (0: dense G*L*tdim);
      * lets the host pre-draw L_cap >= L generators per group before L is known */
@@ -432,6 +433,13 @@ typedef struct {
     /* 1: the top-s selection runs grid-wide (sfftb_topk_grid) -- set when
      * large detected sets are expected (the previous stage saturated) */
     int64_t topk_grid;
+    /* 0: the whole stage.  1: spectra only -- the zmat/tails copies, the
+     * sampler and the transforms (ghat, theta0, bits), which do not depend on
+     * the candidate set, so the driver enqueues them for stage t+1 before it
+     * waits for stage t's counts.  2: the rest (candidates, hashing,
+     * compaction, medians, top-s, union) on the spectra of an earlier phase-1
+     * call with the same G, L, M, zmat and call0. */
+    int64_t phase;
 } sfftb_stage_t;
 
 int sfftb_sfft_stage(const sfftb_stage_t *st, void *stream);

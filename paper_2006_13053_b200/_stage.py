@@ -38,12 +38,18 @@ class StageDesc(ctypes.Structure):
         ("counts", _p), ("med", _p), ("ws_compact", _p), ("kidx", _p), ("kco", _p),
         ("kcounts", _p), ("ws_topk", _p), ("umask", _p), ("uidx", _p), ("ucount", _p),
         ("host_counts", _p), ("events", _p), ("zmat_host_ld", _i64), ("ptab", _p),
-        ("vtab", _p), ("topk_grid", _i64),
+        ("vtab", _p), ("topk_grid", _i64), ("phase", _i64),
     ]
 
 
 PHASES = ("candidates", "sampler", "transforms", "hashing", "compaction+medians",
           "top-s+union")
+# (first, last) event of each phase (sfftb_stage_t.events), and the phases a
+# call of each stage phase (0 whole, 1 spectra, 2 detection) records
+_SPANS = {"candidates": (0, 1), "sampler": (2, 3), "transforms": (3, 4), "hashing": (5, 6),
+          "compaction+medians": (6, 7), "top-s+union": (7, 8)}
+_CALL = {0: (PHASES, (0, 8)), 1: (("sampler", "transforms"), (2, 4)),
+         2: (("candidates", "hashing", "compaction+medians", "top-s+union"), (0, 8))}
 
 
 class Arena:
@@ -51,6 +57,18 @@ class Arena:
 
     def __init__(self):
         self._bufs = {}
+        # replaced buffers stay alive until settle(): a stage enqueued ahead
+        # (spectra of t+1, planned buffers of t+1) may grow a buffer whose old
+        # address an earlier descriptor still holds for pending device work
+        self._old = []
+
+    def settle(self):
+        """Free replaced buffers -- only when no enqueued work can use them
+        (the start of a reconstruction; an early return may have left spectra
+        enqueued, so the stream is drained first)."""
+        if self._old:
+            torch.cuda.current_stream().synchronize()
+            self._old.clear()
 
     def get(self, name, numel, dtype=torch.int64, pinned=False):
         numel = max(int(numel), 1)
@@ -58,6 +76,8 @@ class Arena:
         # a name is one buffer kind: never reinterpret another dtype / memory
         buf = ent[0] if ent is not None and ent[1] == dtype and ent[2] == pinned else None
         if buf is None or buf.numel() < numel:
+            if ent is not None:
+                self._old.append(ent[0])
             grow = numel if buf is None else max(numel, buf.numel() * 5 // 4)
             if pinned:
                 buf = torch.empty(grow, dtype=dtype, pin_memory=True)
@@ -96,13 +116,14 @@ def release():
 
 
 def run(desc):
-    """One stage call; under a _native.Timeline the phase boundaries are
-    recorded (CUDA events on the launch stream) as 'stage:<phase>' entries."""
+    """One stage call (desc.phase: 0 whole stage, 1 spectra, 2 detection);
+    under a _native.Timeline the phase boundaries are recorded (CUDA events
+    on the launch stream) as 'stage:<phase>' entries."""
     lib = _native.lib()
     tl = _native._TIMELINE
     evs = None
     if tl is not None:
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(PHASES) + 1)]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
         for e in evs:
             e.record()  # materialise the cudaEvent_t; the stage re-records it
         arr = (ctypes.c_void_p * len(evs))(*[e.cuda_event for e in evs])
@@ -111,9 +132,11 @@ def run(desc):
         desc.events = None
     rc = lib.sfftb_sfft_stage(ctypes.addressof(desc), _dev.stream())
     if evs is not None:
-        for k, ph in enumerate(PHASES):
-            tl.records.append((f"stage:{ph}", evs[k], evs[k + 1]))
-        tl.records.append(("sfftb_sfft_stage", evs[0], evs[-1]))
+        phases, (a, b) = _CALL[int(desc.phase)]
+        for ph in phases:
+            i, j = _SPANS[ph]
+            tl.records.append((f"stage:{ph}", evs[i], evs[j]))
+        tl.records.append(("sfftb_sfft_stage", evs[a], evs[b]))
         desc.events = None
     _native.check(rc, "sfftb_sfft_stage")
 
@@ -130,9 +153,11 @@ def buffers(A, desc, G, L, M, n, s, fused, slot):
     P = A.ptr
     desc.anchored = P("anchored", 2 * G * max(s, 1), f64)
     desc.bins = P("bins", 2 * rows * M, f64)
-    desc.ghat = P("ghat", 2 * rows * M, f64)
-    desc.theta0 = P("theta0", G, f64)
-    desc.bits = P("bits", rows * W, torch.int32)
+    # the spectra of stage t+1 may be enqueued before stage t's detection:
+    # what the detection reads (ghat, theta0, bits) is per slot
+    desc.ghat = P(f"ghat{slot}", 2 * rows * M, f64)
+    desc.theta0 = P(f"theta0{slot}", G, f64)
+    desc.bits = P(f"bits{slot}", rows * W, torch.int32)
     if fused:
         desc.samples = desc.sumsq = None
         desc.ws_dft = A.bytes("ws_dft", lib.sfftb_sample_detect_workspace_bytes(rows, M))

@@ -1,5 +1,7 @@
 // One detection stage of the dimension-incremental driver as a single host
-// call (include/sfft_b200.h: sfftb_sfft_stage).  No new device code: the
+// call (include/sfft_b200.h: sfftb_sfft_stage), or its two halves: the
+// spectra (phase 1: sampler + transforms, independent of the candidate set)
+// and the detection on them (phase 2).  No new device code: the
 // stage is the sequence of the library's own entry points that the Python
 // driver issued one ctypes call at a time (dimincr.py _detect_stage +
 // _engine), composed here so the ~12 launches of a stage cost microseconds
@@ -14,33 +16,39 @@
         if (rc_ != SFFTB_OK) return rc_; \
     } while (0)
 
-extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
-    SFFTB_REQUIRE(a != nullptr, "stage: null descriptor");
-    SFFTB_REQUIRE(a->G >= 1 && a->L >= 1 && a->M >= 1 && a->tdim >= 1 && a->n >= 0,
-                  "stage: bad sizes");
-    SFFTB_REQUIRE(a->d >= a->tdim && a->tail_w >= 1, "stage: bad dimensions");
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t G = a->G, L = a->L, M = a->M, n = a->n, tdim = a->tdim;
-    const int64_t rows = G * L;
-    auto mark = [&](int k) -> int {
+namespace {
+
+struct Marks {
+    const sfftb_stage_t* a;
+    cudaStream_t st;
+    int operator()(int k) const {
         if (a->events && a->events[k])
             SFFTB_CUDA(cudaEventRecord((cudaEvent_t)a->events[k], st));
         return SFFTB_OK;
-    };
-    SFFTB_TRY(mark(0));
+    }
+};
 
-    // candidates
+// prefix gather + pair product
+int stage_candidates(const sfftb_stage_t* a, void* stream, const Marks& mark) {
+    SFFTB_TRY(mark(0));
     if (a->prev_J) {
         SFFTB_TRY(sfftb_gather_rows(a->prev_J, a->t, a->prev_uidx, a->prev_ucount, a->n1,
                                     a->prefix, stream));
     }
     if (a->vals) {
-        SFFTB_REQUIRE(a->n1 * a->n2 == n && a->t + 1 == tdim, "stage: pair sizes");
+        SFFTB_REQUIRE(a->n1 * a->n2 == a->n && a->t + 1 == a->tdim, "stage: pair sizes");
         SFFTB_TRY(sfftb_pair_product(a->prefix, a->n1, a->t, a->vals, a->n2, a->J, stream));
     }
-
-    // generators and tails drawn on the host
     SFFTB_TRY(mark(1));
+    return SFFTB_OK;
+}
+
+// generators/tails H2D, structured sampler, transforms -> ghat, theta0, bits
+int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = a->G, L = a->L, M = a->M, tdim = a->tdim;
+    const int64_t rows = G * L;
+    SFFTB_TRY(mark(2));
     if (a->zmat_host_ld > 0 && a->zmat_host_ld != L * tdim) {
         SFFTB_REQUIRE(a->zmat_host_ld >= L * tdim, "stage: zmat_host_ld < L*tdim");
         SFFTB_CUDA(cudaMemcpy2DAsync(a->zmat, (size_t)(L * tdim) * sizeof(int64_t), a->zmat_host,
@@ -64,7 +72,7 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
                                  a->bins, nullptr, stream));
 
     // samples -> zero test, spectra, bitmaps
-    SFFTB_TRY(mark(2));
+    SFFTB_TRY(mark(3));
     if (a->fused) {
         SFFTB_TRY(sfftb_sample_detect_dft(a->bins, G, L, M, a->noise_seed, a->call0, a->sigma,
                                           a->ghat, a->theta0, a->bits, a->ws_dft, stream));
@@ -87,9 +95,16 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
         }
         SFFTB_TRY(sfftb_nonzero_bitmap(a->ghat, G, L, M, a->theta0, a->bits, stream));
     }
+    SFFTB_TRY(mark(4));
+    return SFFTB_OK;
+}
 
-    // hashing, compaction, medians, top-s
-    SFFTB_TRY(mark(3));
+// hashing, compaction, medians, top-s, union, count read-back
+int stage_detect(const sfftb_stage_t* a, void* stream, const Marks& mark) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t G = a->G, L = a->L, M = a->M, n = a->n, tdim = a->tdim;
+    const int64_t rows = G * L;
+    SFFTB_TRY(mark(5));
     // Cartesian J (pair stages): residues from per-lattice tables of the
     // prefix and value parts -- n1 + n2 dot products per lattice, not n1*n2
     // (table hashing beats the resident dot-product kernel from ~8 coordinates
@@ -108,7 +123,7 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
             SFFTB_TRY(sfftb_hash_hits(a->J, n, tdim, a->zmat, G, L, M, a->bits, a->kbound,
                                       a->min_hits, nullptr, a->detmask, stream));
         }
-        SFFTB_TRY(mark(4));
+        SFFTB_TRY(mark(6));
         SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
                                      stream));
         if (pairs)
@@ -118,10 +133,10 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
             SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts,
                                     n, a->med, stream));
     } else {
-        SFFTB_TRY(mark(4));
+        SFFTB_TRY(mark(6));
         SFFTB_CUDA(cudaMemsetAsync(a->counts, 0, (size_t)G * sizeof(int64_t), st));
     }
-    SFFTB_TRY(mark(5));
+    SFFTB_TRY(mark(7));
     const int64_t cap = n > 0 ? n : 1;
     if (a->topk_grid && cap >= 16384)
         SFFTB_TRY(sfftb_topk_grid(a->idx, a->med, a->counts, G, cap, a->theta, a->s_tilde,
@@ -146,6 +161,21 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
         SFFTB_CUDA(cudaMemcpyAsync(a->host_counts + G, a->ucount, sizeof(int64_t),
                                    cudaMemcpyDeviceToHost, st));
     }
-    SFFTB_TRY(mark(6));
+    SFFTB_TRY(mark(8));
     return SFFTB_OK;
+}
+
+}  // namespace
+
+extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
+    SFFTB_REQUIRE(a != nullptr, "stage: null descriptor");
+    SFFTB_REQUIRE(a->G >= 1 && a->L >= 1 && a->M >= 1 && a->tdim >= 1 && a->n >= 0,
+                  "stage: bad sizes");
+    SFFTB_REQUIRE(a->d >= a->tdim && a->tail_w >= 1, "stage: bad dimensions");
+    SFFTB_REQUIRE(a->phase >= 0 && a->phase <= 2, "stage: phase must be 0, 1 or 2");
+    const Marks mark{a, (cudaStream_t)stream};
+    if (a->phase == 1) return stage_spectra(a, stream, mark);
+    SFFTB_TRY(stage_candidates(a, stream, mark));
+    if (a->phase == 0) SFFTB_TRY(stage_spectra(a, stream, mark));
+    return stage_detect(a, stream, mark);
 }

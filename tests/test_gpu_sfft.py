@@ -112,3 +112,31 @@ def test_sfft_fused_path_vs_oracle(cuda, oracle_lib, sigma):
     assert [(e["candidates"], e["kept"]) for e in res.stage_log] == \
         [(e["candidates"], e["kept"]) for e in ref[3]]
     assert workloads.rel_l2(res.coeffs, ref[1]) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["metric_config", "config5"])
+def test_spectra_ahead_modes_bitwise(cuda, monkeypatch, name):
+    """Stage spectra enqueued ahead of the previous stage's counts (hit, and
+    forced miss -> whole-stage fallback) give bit-identical results to the
+    in-order stage calls, noisy oracle included (harness call numbers)."""
+    from paper_2006_13053_b200 import dimincr
+
+    w = getattr(workloads, name)()
+    p = cuda.SparsePoly(cuda.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+
+    def run():
+        orc = cuda.oracle_from_poly(p, noise_sigma=w.sigma, noise_seed=w.noise_seed)
+        return cuda.sfft(orc, cuda.Box(w.d, w.lo, w.hi),
+                         cuda.SfftParams(w.s, w.delta, theta=w.theta, r=w.r), seed=w.seed)
+
+    outs = []
+    for ahead, bias in ((False, 0), (True, 0), (True, -2)):
+        monkeypatch.setattr(dimincr, "_SPECTRA_AHEAD", ahead)
+        monkeypatch.setattr(dimincr, "_SPEC_L_BIAS", bias)
+        outs.append(run())
+    base = outs[0]
+    for o in outs[1:]:
+        assert np.array_equal(o.support.elems, base.support.elems)
+        assert np.array_equal(o.coeffs, base.coeffs)
+        assert o.sample_count == base.sample_count
+        assert o.stage_log == base.stage_log
