@@ -304,6 +304,16 @@ int sfftb_eval_dense(const int64_t *support, int64_t s, int64_t d,
                      double *out, void *stream);
 
 /*
+ * Step 1's coordinate-line samples (dimincr.py:137-141) without building the
+ * nodes on the host: out[q*K + j] = p(x) with x = base row q (nlines x d)
+ * and coordinate q / r set to j / K.  Same arithmetic as sfftb_eval_dense on
+ * those nodes.
+ */
+int sfftb_eval_lines(const int64_t *support, int64_t s, int64_t d,
+                     const double *coeffs, const double *base, int64_t nlines,
+                     int64_t K, int64_t r, double *out, void *stream);
+
+/*
  * Harness noise: rows r of x (length M each) get sigma*(N(0,1) + i N(0,1))
  * from Philox4x32-10 keyed by seed with counter (m, call0 + r)  (the config-5
  * noise stream; restated in oracle/port.py:noise_for_call).

@@ -63,6 +63,7 @@ _SIGS = {
     "sfftb_scatter_bins": (_int, [_p, _i64, _i64, _i64, _p, _p, _i64, _i64, _i64, _p, _p,
                                   _p]),
     "sfftb_eval_dense": (_int, [_p, _i64, _i64, _p, _p, _i64, _p, _p]),
+    "sfftb_eval_lines": (_int, [_p, _i64, _i64, _p, _p, _i64, _i64, _i64, _p, _p]),
     "sfftb_add_noise": (_int, [_p, _i64, _i64, _u64, _i64, _dbl, _p]),
     "sfftb_injective_mod_dev": (_int, [_p, _i64, _i64, _i64, ctypes.POINTER(_int), _p]),
     "sfftb_sfft_stage": (_int, [_p, _p]),

@@ -224,15 +224,24 @@ __global__ void __launch_bounds__(kScatterRsThreads)
 // then a fixed shuffle tree adds the 32 partial sums (deterministic).
 static constexpr int kEvalThreads = 256;
 
+// LINES: point p = q*K + j of coordinate line q is base row q with
+// coordinate q / r replaced by j / K (step 1's line nodes, dimincr.py:137-141).
+template <bool LINES>
 __global__ void __launch_bounds__(kEvalThreads)
     eval_dense_kernel(const int64_t* __restrict__ support, int64_t s, int d,
                       const double2* __restrict__ coeffs, const double* __restrict__ X, int64_t m,
-                      double2* __restrict__ out) {
+                      double2* __restrict__ out, int64_t K, int64_t r) {
     const int lane = threadIdx.x & 31;
     const int64_t p = blockIdx.x * (int64_t)(kEvalThreads / 32) + (threadIdx.x >> 5);
     if (p >= m) return;
     double x[32];
-    for (int j = 0; j < d; ++j) x[j] = X[p * d + j];
+    if (LINES) {
+        const int64_t q = p / K, jj = p % K;
+        for (int j = 0; j < d; ++j) x[j] = X[q * d + j];
+        x[q / r] = (double)jj / (double)K;
+    } else {
+        for (int j = 0; j < d; ++j) x[j] = X[p * d + j];
+    }
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t k = lane; k < s; k += 32) {
         double phi = 0.0;
@@ -325,9 +334,25 @@ extern "C" int sfftb_eval_dense(const int64_t* support, int64_t s, int64_t d,
                                 void* stream) {
     SFFTB_REQUIRE(d >= 1 && d <= 32, "eval_dense: 1 <= d <= 32");
     if (m == 0) return SFFTB_OK;
-    eval_dense_kernel<<<(unsigned)ceil_div(m, kEvalThreads / 32), kEvalThreads, 0,
-                        (cudaStream_t)stream>>>(support, s, (int)d, (const double2*)coeffs, X, m,
-                                                (double2*)out);
+    eval_dense_kernel<false><<<(unsigned)ceil_div(m, kEvalThreads / 32), kEvalThreads, 0,
+                               (cudaStream_t)stream>>>(support, s, (int)d,
+                                                       (const double2*)coeffs, X, m,
+                                                       (double2*)out, 1, 1);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_eval_lines(const int64_t* support, int64_t s, int64_t d,
+                                const double* coeffs, const double* base, int64_t nlines,
+                                int64_t K, int64_t r, double* out, void* stream) {
+    SFFTB_REQUIRE(d >= 1 && d <= 32, "eval_lines: 1 <= d <= 32");
+    SFFTB_REQUIRE(K >= 1 && r >= 1 && nlines <= d * r, "eval_lines: bad sizes");
+    const int64_t m = nlines * K;
+    if (m == 0) return SFFTB_OK;
+    eval_dense_kernel<true><<<(unsigned)ceil_div(m, kEvalThreads / 32), kEvalThreads, 0,
+                              (cudaStream_t)stream>>>(support, s, (int)d,
+                                                      (const double2*)coeffs, base, m,
+                                                      (double2*)out, K, r);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
