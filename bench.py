@@ -220,10 +220,10 @@ def run_sfft_arm(args, world, rank):
     shapes = []
     orig_run = _stage.run
 
-    def run_rec(desc):
+    def run_rec(desc, stream=None):
         if desc.phase != 2:  # the calls that run transforms (whole stage or spectra)
             shapes.append((desc.G, desc.L, desc.M, bool(desc.fused)))
-        return orig_run(desc)
+        return orig_run(desc, stream)
 
     flush_l2(flush)
     torch.cuda.synchronize()

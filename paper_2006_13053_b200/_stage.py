@@ -68,6 +68,8 @@ class Arena:
         enqueued, so the stream is drained first)."""
         if self._old:
             torch.cuda.current_stream().synchronize()
+            side_stream().synchronize()
+            det_stream().synchronize()
             self._old.clear()
 
     def get(self, name, numel, dtype=torch.int64, pinned=False):
@@ -115,7 +117,33 @@ def release():
     _LOCAL.arena = None
 
 
-def run(desc):
+def _stream(kind, priority):
+    dev = torch.cuda.current_device()
+    cache = getattr(_LOCAL, kind, None)
+    if cache is None:
+        cache = {}
+        setattr(_LOCAL, kind, cache)
+    st = cache.get(dev)
+    if st is None:
+        st = cache[dev] = torch.cuda.Stream(device=dev, priority=priority)
+    return st
+
+
+def side_stream():
+    """The calling thread's spectra stream (non-blocking, normal priority):
+    stage t+1's sampler + transforms run there while stage t's detection
+    runs on det_stream()."""
+    return _stream("side", 0)
+
+
+def det_stream():
+    """The calling thread's detection stream (non-blocking, high priority:
+    its short, latency-bound kernels get SMs ahead of the transforms that
+    overlap them, and the host waits on their counts)."""
+    return _stream("det", -1)
+
+
+def run(desc, stream=None):
     """One stage call (desc.phase: 0 whole stage, 1 spectra, 2 detection);
     under a _native.Timeline the phase boundaries are recorded (CUDA events
     on the launch stream) as 'stage:<phase>' entries."""
@@ -130,7 +158,8 @@ def run(desc):
         desc.events = ctypes.addressof(arr)
     else:
         desc.events = None
-    rc = lib.sfftb_sfft_stage(ctypes.addressof(desc), _dev.stream())
+    rc = lib.sfftb_sfft_stage(ctypes.addressof(desc),
+                              _dev.stream() if stream is None else stream)
     if evs is not None:
         phases, (a, b) = _CALL[int(desc.phase)]
         for ph in phases:

@@ -162,12 +162,24 @@ __global__ void __launch_bounds__(kScatterRsThreads)
             for (int i = threadIdx.x; i < cnt; i += blockDim.x)
                 atomicAdd(&base[(r0[i] >> shift) & 255u], 1u);
             __syncthreads();
-            if (threadIdx.x == 0) {  // exclusive scan of the 256 digit counts
-                uint32_t run = 0;
-                for (int b = 0; b < 256; ++b) {
-                    const uint32_t v = base[b];
-                    base[b] = run;
-                    run += v;
+            if (warp == 0) {  // exclusive scan of the 256 digit counts: 8 per lane
+                uint32_t v[8], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    v[q] = base[lane * 8 + q];
+                    sum += v[q];
+                }
+                uint32_t inc = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                uint32_t run = inc - sum;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    base[lane * 8 + q] = run;
+                    run += v[q];
                 }
             }
             __syncthreads();

@@ -49,14 +49,16 @@ from paper_2006_13053_b200 import _stage, dimincr  # noqa: E402
 orig_run = _stage.run
 
 
-def run(desc):
+def run(desc, stream=None):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream() if stream is None else torch.cuda.ExternalStream(stream)
     h = time.perf_counter()
-    e0.record()
-    orig_run(desc)
-    e1.record()
-    log.append((f"<stage G={desc.G} L={desc.L} M={desc.M} n={desc.n}>", h, time.perf_counter(),
+    e0.record(st)
+    orig_run(desc, stream)
+    e1.record(st)
+    kind = {0: "stage", 1: "spectra", 2: "detect"}[int(desc.phase)]
+    log.append((f"<{kind} G={desc.G} L={desc.L} M={desc.M} n={desc.n}>", h, time.perf_counter(),
                 e0, e1))
 
 
