@@ -117,6 +117,18 @@ int sfftb_sample_detect_dft(const double *bins, int64_t G, int64_t L, int64_t M,
                             uint64_t seed, int64_t call0, double sigma, double *ghat,
                             double *theta, uint32_t *bits, void *ws, void *stream);
 
+/*
+ * The same with the sampler's bins given sparsely (sfftb_scatter_list): per
+ * transform b, ls entries list_r[b*ls + k] (residue, ~0 = none) and list_v
+ * (complex128 bin value).  The first column pass drops the listed bins into
+ * its shared-memory tile instead of reading a dense (G*L x M) bins array.
+ */
+int sfftb_sample_detect_dft_list(const uint32_t *list_r, const double *list_v,
+                                 int64_t ls, int64_t G, int64_t L, int64_t M,
+                                 uint64_t seed, int64_t call0, double sigma,
+                                 double *ghat, double *theta, uint32_t *bits,
+                                 void *ws, void *stream);
+
 /* out[b] = sum_j |x[b, j]|^2 (for default_zero_test, detect.py:42-53). */
 int sfftb_sumsq(const double *x, int64_t stride, int64_t batch, int64_t M,
                 double *out, void *stream);
@@ -294,6 +306,20 @@ int sfftb_scatter_bins(const int64_t *support, int64_t s, int64_t d,
                        int64_t t_dim, const double *anchored,
                        const int64_t *zmat, int64_t G, int64_t L, int64_t M,
                        double *bins, void *ws, void *stream);
+
+/*
+ * The sampler bins as per-lattice lists instead of a dense array (s <= 4096,
+ * M <= 2^24): list_r[(g*L + l)*s + k], list_v[...] = (residue, bin sum) for
+ * the k-th coefficient in residue order when it heads its residue's run (the
+ * run summed in ascending coefficient order, like np.bincount), residue ~0
+ * otherwise.  Bins without coefficients are implicit zeros.  The values carry
+ * the sampler's first Bluestein product, conj(bin) * chirp_M[residue] (the
+ * input sfftb_sample_detect_dft_list expects).
+ */
+int sfftb_scatter_list(const int64_t *support, int64_t s, int64_t d, int64_t t_dim,
+                       const double *anchored, const int64_t *zmat, int64_t G,
+                       int64_t L, int64_t M, uint32_t *list_r, double *list_v,
+                       void *stream);
 
 /*
  * Dense evaluation p(x) = sum_k c_k exp(2 pi i k . x) at m points X (m, d)

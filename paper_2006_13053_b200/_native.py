@@ -42,6 +42,8 @@ _SIGS = {
     "sfftb_sample_detect_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_sample_detect_dft": (_int, [_p, _i64, _i64, _i64, _u64, _i64, _dbl, _p, _p, _p, _p,
                                        _p]),
+    "sfftb_sample_detect_dft_list": (_int, [_p, _p, _i64, _i64, _i64, _i64, _u64, _i64, _dbl,
+                                            _p, _p, _p, _p, _p]),
     "sfftb_zero_thresholds": (_int, [_p, _i64, _i64, _i64, _p, _p]),
     "sfftb_bitmap_words": (_i64, [_i64]),
     "sfftb_nonzero_bitmap": (_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
@@ -61,6 +63,8 @@ _SIGS = {
     "sfftb_anchor_coeffs": (_int, [_p, _i64, _i64, _i64, _p, _p, _i64, _p, _p]),
     "sfftb_scatter_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_scatter_bins": (_int, [_p, _i64, _i64, _i64, _p, _p, _i64, _i64, _i64, _p, _p,
+                                  _p]),
+    "sfftb_scatter_list": (_int, [_p, _i64, _i64, _i64, _p, _p, _i64, _i64, _i64, _p, _p,
                                   _p]),
     "sfftb_eval_dense": (_int, [_p, _i64, _i64, _p, _p, _i64, _p, _p]),
     "sfftb_eval_lines": (_int, [_p, _i64, _i64, _p, _p, _i64, _i64, _i64, _p, _p]),

@@ -87,6 +87,9 @@ inline cudaError_t occupancy(int* out, K kernel, int threads, size_t smem) {
     return occupancy_raw(out, reinterpret_cast<const void*>(kernel), threads, smem);
 }
 
+// Bluestein chirp of length M from the plan cache (csrc/fft.cu).
+int bluestein_chirp(int64_t M, const double2** chirp);
+
 // complex double helpers (interleaved re, im == numpy complex128 layout)
 struct cplx {
     double x, y;

@@ -261,6 +261,11 @@ struct DftArgs {
     int L;
     uint32_t* bits;         // [batch][W] nonzero bitmaps
     int64_t W;
+    // sparse sampler input (fs2_colA<.., SPARSE>): per transform a list of
+    // ls entries (residue, bin value), residue ~0 = no entry
+    const uint32_t* lr;
+    const double2* lv;
+    int64_t ls;
 };
 
 template <bool C>
@@ -502,7 +507,7 @@ struct Fs2Layout {
     static constexpr int DATA = F * SLOT;
 };
 
-template <int N2, bool INV>
+template <int N2, bool INV, bool SPARSE = false>
 __global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
     using Lay = Fs2Layout<N2>;
     constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
@@ -522,15 +527,53 @@ __global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
         const int64_t b = tile / per_b;
         const int n1 = (int)(tile % per_b) * F + f;
-        const double2* x = a.x + b * a.xs;
         double2 v[16];
+        if (SPARSE) {
+            // the tile's columns [n1_0, n1_0 + F) of the N1 x N2 view: zero
+            // them in the slots, drop in the listed bins, read them back
+            const int n1_0 = n1 - f;
+            __syncthreads();  // previous tile done with the slots
+            for (int i = tid; i < F * N2; i += 256) smem[(i / N2) * SLOT + (i % N2)] =
+                make_double2(0.0, 0.0);
+            __syncthreads();
+            // list values already carry the chirp product (sfftb_scatter_list);
+            // residues and values of U entries per thread are loaded at once
+            const uint32_t* lr = a.lr + b * a.ls;
+            const double2* lv = a.lv + b * a.ls;
+            // r / N1 by multiply-high with ceil(2^32 / N1): exact for r < 2^24
+            const uint32_t magic = (uint32_t)((0x100000000ull + (uint32_t)N1 - 1) / (uint32_t)N1);
+            constexpr int U = 4;
+            for (int64_t k0 = tid; k0 < a.ls; k0 += 256 * U) {
+                uint32_t rr[U];
+                double2 vv[U];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int64_t j = n1 + (int64_t)N1 * (t + r * T);
-            v[r] = make_double2(0.0, 0.0);
-            if (j < a.M) v[r] = cmul(conj_if<INV>(__ldg(x + j)), __ldg(a.chirp + j));
+                for (int u = 0; u < U; ++u) {
+                    const int64_t k = k0 + 256 * u;
+                    rr[u] = k < a.ls ? __ldg(lr + k) : ~0u;
+                    vv[u] = k < a.ls ? __ldg(lv + k) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (rr[u] == ~0u) continue;
+                    const uint32_t q = __umulhi(rr[u], magic);
+                    const int c = (int)(rr[u] - q * (uint32_t)N1) - n1_0;
+                    if (c >= 0 && c < F) smem[c * SLOT + (int)q] = vv[u];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = slot[t + r * T];
+            __syncthreads();  // fft2pass reuses the slots
+        } else {
+            const double2* x = a.x + b * a.xs;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int64_t j = n1 + (int64_t)N1 * (t + r * T);
+                v[r] = make_double2(0.0, 0.0);
+                if (j < a.M) v[r] = cmul(conj_if<INV>(__ldg(x + j)), __ldg(a.chirp + j));
+            }
+            __syncthreads();  // previous tile done with the slots
         }
-        __syncthreads();  // previous tile done with the slots
         fft2pass<N2, false>(v, slot, t, tw2);
         out_twiddle<N2, false>(v, n1, t, hi, lo);
         double2* Tw = a.work + b * (int64_t)N;
@@ -923,7 +966,7 @@ static int rows_dispatch(int N1, const DftArgs& a, int64_t batch, int N2, cudaSt
     return SFFTB_EINVAL;
 }
 
-template <int N2, bool INV>
+template <int N2, bool INV, bool SPARSE = false>
 static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bool first) {
     using Lay = Fs2Layout<N2>;
     const size_t hi = a.hi_in_smem ? (size_t)(N1 * N2 / 64) : 0;
@@ -932,8 +975,8 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
     c.ntiles = (int64_t)(N1 / Lay::F) * batch;
     const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
     if (first) {
-        SFFTB_CUDA(allow_smem(fs2_colA<N2, INV>, sm));
-        fs2_colA<N2, INV><<<grid, 256, sm, st>>>(c, N1);
+        SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE>, sm));
+        fs2_colA<N2, INV, SPARSE><<<grid, 256, sm, st>>>(c, N1);
     } else {
         SFFTB_CUDA(allow_smem(fs2_colC<N2, INV>, sm));
         fs2_colC<N2, INV><<<grid, 256, sm, st>>>(c, N1);
@@ -1073,10 +1116,10 @@ extern "C" int64_t sfftb_sample_detect_workspace_bytes(int64_t batch, int64_t M)
            batch * (int64_t)sizeof(double);
 }
 
-extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L, int64_t M,
-                                       uint64_t seed, int64_t call0, double sigma,
-                                       double* ghat, double* theta, uint32_t* bits,
-                                       void* ws, void* stream) {
+static int sample_detect(const double* bins, const uint32_t* lr, const double* lv, int64_t ls,
+                         int64_t G, int64_t L, int64_t M, uint64_t seed, int64_t call0,
+                         double sigma, double* ghat, double* theta, uint32_t* bits, void* ws,
+                         void* stream) {
     SFFTB_REQUIRE(G >= 1 && L >= 1 && M >= 1, "sample_detect: bad sizes");
     BluesteinPlan* p = nullptr;
     int rc = get_plan(M, &p);
@@ -1112,10 +1155,17 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
     a.L = (int)L;
     a.bits = bits;
     a.W = sfftb_bitmap_words(M);
+    a.lr = lr;
+    a.lv = (const double2*)lv;
+    a.ls = ls;
     // sampler: inverse DFT (scale 1) -- colA (conj input) and rowB
     a.scale = 1.0;
-    rc = p->N2 == 256 ? fs2_cols<256, true>(a, batch, p->N1, st, true)
-                      : fs2_cols<128, true>(a, batch, p->N1, st, true);
+    if (lr)
+        rc = p->N2 == 256 ? fs2_cols<256, true, true>(a, batch, p->N1, st, true)
+                          : fs2_cols<128, true, true>(a, batch, p->N1, st, true);
+    else
+        rc = p->N2 == 256 ? fs2_cols<256, true>(a, batch, p->N1, st, true)
+                          : fs2_cols<128, true>(a, batch, p->N1, st, true);
     if (rc) return rc;
     rc = fs2_rows_any(a, batch, p->N1, p->N2, st);
     if (rc) return rc;
@@ -1176,6 +1226,36 @@ extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L,
     }
     return SFFTB_OK;
 }
+
+extern "C" int sfftb_sample_detect_dft(const double* bins, int64_t G, int64_t L, int64_t M,
+                                       uint64_t seed, int64_t call0, double sigma,
+                                       double* ghat, double* theta, uint32_t* bits,
+                                       void* ws, void* stream) {
+    return sample_detect(bins, nullptr, nullptr, 0, G, L, M, seed, call0, sigma, ghat, theta,
+                         bits, ws, stream);
+}
+
+extern "C" int sfftb_sample_detect_dft_list(const uint32_t* list_r, const double* list_v,
+                                            int64_t ls, int64_t G, int64_t L, int64_t M,
+                                            uint64_t seed, int64_t call0, double sigma,
+                                            double* ghat, double* theta, uint32_t* bits,
+                                            void* ws, void* stream) {
+    SFFTB_REQUIRE(list_r && list_v && ls >= 1, "sample_detect_list: empty list");
+    return sample_detect(nullptr, list_r, list_v, ls, G, L, M, seed, call0, sigma, ghat, theta,
+                         bits, ws, stream);
+}
+
+namespace sfftb {
+// The Bluestein chirp of length M (plan cache), for producers that fold the
+// sampler's chirp product into their output (sfftb_scatter_list).
+int bluestein_chirp(int64_t M, const double2** chirp) {
+    BluesteinPlan* p = nullptr;
+    const int rc = get_plan(M, &p);
+    if (rc != SFFTB_OK) return rc;
+    *chirp = p->chirp;
+    return SFFTB_OK;
+}
+}  // namespace sfftb
 
 extern "C" int sfftb_plan_cache_clear(void) {
     std::lock_guard<std::mutex> lk(g_plan_mu);

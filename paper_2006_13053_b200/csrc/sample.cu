@@ -120,7 +120,9 @@ static constexpr int kScatterRsChunk = 4096;
 __global__ void __launch_bounds__(kScatterRsThreads)
     scatter_rs_kernel(const int64_t* __restrict__ support, int64_t s, int d, int t_dim,
                       const double2* __restrict__ anchored, const int64_t* __restrict__ zmat,
-                      int L, int64_t M, int npass, double2* __restrict__ bins) {
+                      int L, int64_t M, int npass, double2* __restrict__ bins,
+                      uint32_t* __restrict__ list_r, double2* __restrict__ list_v,
+                      const double2* __restrict__ chirp) {
     constexpr int W = kScatterRsThreads / 32;
     extern __shared__ uint32_t rs_dsm[];
     uint32_t* ra = rs_dsm;
@@ -137,8 +139,12 @@ __global__ void __launch_bounds__(kScatterRsThreads)
     for (int j = threadIdx.x; j < t_dim; j += blockDim.x)
         zs[j] = (uint64_t)reduce_mod(zmat[lat * t_dim + j], M);
     for (int b = threadIdx.x; b < W * 256; b += blockDim.x) wcnt[0][b] = 0;
-    double2* B = bins + lat * M;
-    for (int64_t h = threadIdx.x; h < M; h += blockDim.x) B[h] = make_double2(0.0, 0.0);
+    // list mode (s <= one chunk): no dense bins; entry i of the lattice's
+    // list is (residue, run sum) at run heads and residue ~0 elsewhere
+    const bool listed = list_r != nullptr;
+    double2* B = listed ? nullptr : bins + lat * M;
+    if (!listed)
+        for (int64_t h = threadIdx.x; h < M; h += blockDim.x) B[h] = make_double2(0.0, 0.0);
     __syncthreads();
     const double2* a = anchored + g * s;
     for (int64_t c0 = 0; c0 < s; c0 += kScatterRsChunk) {
@@ -219,14 +225,22 @@ __global__ void __launch_bounds__(kScatterRsThreads)
         // run heads accumulate their run in ascending coefficient order
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const uint32_t r = r0[i];
-            if (i > 0 && r0[i - 1] == r) continue;
-            double2 acc = B[r];
+            if (i > 0 && r0[i - 1] == r) {
+                if (listed) list_r[lat * s + i] = ~0u;
+                continue;
+            }
+            double2 acc = listed ? make_double2(0.0, 0.0) : B[r];
             for (int q = i; q < cnt && r0[q] == r; ++q) {
                 const double2 v = a[c0 + i0[q]];
                 acc.x += v.x;
                 acc.y += v.y;
             }
-            B[r] = acc;
+            if (listed) {  // the sampler's first Bluestein product, folded in
+                list_r[lat * s + i] = r;
+                list_v[lat * s + i] = cmul(make_double2(acc.x, -acc.y), chirp[r]);
+            } else {
+                B[r] = acc;
+            }
         }
         __syncthreads();
     }
@@ -328,7 +342,7 @@ extern "C" int sfftb_scatter_bins(const int64_t* support, int64_t s, int64_t d, 
         SFFTB_CUDA(smem_opt_in(scatter_rs_kernel, rsm));
         scatter_rs_kernel<<<(unsigned)lat, kScatterRsThreads, rsm, (cudaStream_t)stream>>>(
             support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M, npass,
-            (double2*)bins);
+            (double2*)bins, nullptr, nullptr, nullptr);
         SFFTB_CHECK_LAUNCH();
         return SFFTB_OK;
     }
@@ -337,6 +351,29 @@ extern "C" int sfftb_scatter_bins(const int64_t* support, int64_t s, int64_t d, 
     scatter_kernel<<<(unsigned)lat, kScatterThreads, sm, (cudaStream_t)stream>>>(
         support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M,
         (double2*)bins);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+extern "C" int sfftb_scatter_list(const int64_t* support, int64_t s, int64_t d, int64_t t_dim,
+                                  const double* anchored, const int64_t* zmat, int64_t G,
+                                  int64_t L, int64_t M, uint32_t* list_r, double* list_v,
+                                  void* stream) {
+    SFFTB_REQUIRE(t_dim >= 0 && t_dim <= 64 && t_dim <= d, "scatter_list: bad t_dim");
+    SFFTB_REQUIRE(M >= 1 && M <= (int64_t(1) << 24), "scatter_list: M must be <= 2^24");
+    SFFTB_REQUIRE(s >= 1 && s <= kScatterRsChunk, "scatter_list: 1 <= s <= 4096");
+    const int64_t lat = G * L;
+    if (lat == 0) return SFFTB_OK;
+    int npass = 1;
+    while (npass < 4 && (int64_t(1) << (8 * npass)) < M) ++npass;
+    const size_t rsm = sizeof(uint32_t) * (4 * kScatterRsChunk + 256 * (kScatterRsThreads / 32));
+    SFFTB_CUDA(smem_opt_in(scatter_rs_kernel, rsm));
+    const double2* chirp = nullptr;
+    const int rc = bluestein_chirp(M, &chirp);
+    if (rc != SFFTB_OK) return rc;
+    scatter_rs_kernel<<<(unsigned)lat, kScatterRsThreads, rsm, (cudaStream_t)stream>>>(
+        support, s, (int)d, (int)t_dim, (const double2*)anchored, zmat, (int)L, M, npass,
+        nullptr, list_r, (double2*)list_v, chirp);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }

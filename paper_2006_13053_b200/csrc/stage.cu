@@ -68,12 +68,25 @@ int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
     if (a->s > 0)
         SFFTB_TRY(sfftb_anchor_coeffs(a->support, a->s, a->d, tdim, a->coeffs, a->tails, G,
                                       a->anchored, stream));
-    SFFTB_TRY(sfftb_scatter_bins(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L, M,
-                                 a->bins, nullptr, stream));
+    // fused path with few coefficients: sparse bins (residue lists) in the
+    // bins buffer -- no dense zero fill, the first column pass drops them in
+    const bool listed = a->fused && a->s >= 1 && a->s <= 4096 && M <= (int64_t(1) << 24) &&
+                        M >= 2 * a->s;
+    uint32_t* list_r = reinterpret_cast<uint32_t*>(a->bins + 2 * rows * a->s);
+    if (listed)
+        SFFTB_TRY(sfftb_scatter_list(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L,
+                                     M, list_r, a->bins, stream));
+    else
+        SFFTB_TRY(sfftb_scatter_bins(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L,
+                                     M, a->bins, nullptr, stream));
 
     // samples -> zero test, spectra, bitmaps
     SFFTB_TRY(mark(3));
-    if (a->fused) {
+    if (listed) {
+        SFFTB_TRY(sfftb_sample_detect_dft_list(list_r, a->bins, a->s, G, L, M, a->noise_seed,
+                                               a->call0, a->sigma, a->ghat, a->theta0, a->bits,
+                                               a->ws_dft, stream));
+    } else if (a->fused) {
         SFFTB_TRY(sfftb_sample_detect_dft(a->bins, G, L, M, a->noise_seed, a->call0, a->sigma,
                                           a->ghat, a->theta0, a->bits, a->ws_dft, stream));
     } else {
