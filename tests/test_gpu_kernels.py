@@ -333,3 +333,70 @@ def test_pair_tables_match_generic_hashing_and_medians(cuda, t, n1, n2, G, L, M)
     _native.call("sfftb_medians_pairs", _dev.ptr(P), _dev.ptr(V), n1, n2, G, L, M,
                  _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(cnt), k, _dev.ptr(o2), st)
     assert np.array_equal(_dev.download(o1).view(np.int64), _dev.download(o2).view(np.int64))
+
+
+@pytest.mark.parametrize("M,G,L,s,sigma", [(20663, 2, 5, 1000, 0.0), (10331, 3, 3, 4096, 1e-3),
+                                           (4099, 1, 7, 40, 0.0)])
+def test_sampler_lists_match_dense_bins(cuda, M, G, L, s, sigma):
+    """Sparse sampler (sfftb_scatter_list + sfftb_sample_detect_dft_list) ==
+    dense bins (sfftb_scatter_bins + sfftb_sample_detect_dft), bit for bit:
+    ghat, zero thresholds and bitmaps.  Small coordinates force residue
+    collisions, so runs are summed in coefficient order in both."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine, _native
+
+    rng = np.random.default_rng(M + s)
+    d = 4
+    sup = rng.integers(-6, 7, size=(s, d), dtype=np.int64)
+    anch = rng.normal(size=(G, s)) + 1j * rng.normal(size=(G, s))
+    z = rng.integers(0, M, size=(G * L, d), dtype=np.int64)
+    sup_d, a_d, z_d = _dev.upload(sup), _dev.upload(anch), _dev.upload(z)
+    bins = _dev.empty((G * L, M), torch.complex128)
+    _native.call("sfftb_scatter_bins", _dev.ptr(sup_d), s, d, d, _dev.ptr(a_d), _dev.ptr(z_d),
+                 G, L, M, _dev.ptr(bins), None, _dev.stream())
+    want = _engine.sample_spectra_fused(bins, M, G, L, 31, 4, sigma)
+    lr = _dev.empty((G * L * s,), torch.int32)
+    lv = _dev.empty((G * L * s,), torch.complex128)
+    _native.call("sfftb_scatter_list", _dev.ptr(sup_d), s, d, d, _dev.ptr(a_d), _dev.ptr(z_d),
+                 G, L, M, _dev.ptr(lr), _dev.ptr(lv), _dev.stream())
+    W = int(_native.lib().sfftb_bitmap_words(M))
+    ghat = _dev.empty((G * L, M), torch.complex128)
+    theta = _dev.empty((G,), torch.float64)
+    bits = _dev.empty((G * L * W,), torch.int32)
+    ws = _dev.workspace(_native.lib().sfftb_sample_detect_workspace_bytes(G * L, M))
+    _native.call("sfftb_sample_detect_dft_list", _dev.ptr(lr), _dev.ptr(lv), s, G, L, M, 31, 4,
+                 sigma, _dev.ptr(ghat), _dev.ptr(theta), _dev.ptr(bits), _dev.ptr(ws),
+                 _dev.stream())
+    for got, exp in zip((ghat, theta, bits), want):
+        assert np.array_equal(_dev.download(got), _dev.download(exp))
+    # every listed residue is a run head of the sorted residues, once
+    r = _dev.download(lr).view(np.uint32).reshape(G * L, s)
+    for row in range(G * L):
+        heads = r[row][r[row] != 0xFFFFFFFF]
+        assert np.all(np.diff(heads.astype(np.int64)) > 0)
+
+
+def test_eval_lines_matches_dense_nodes(cuda):
+    """sfftb_eval_lines == sfftb_eval_dense on the explicit step-1 line nodes."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    rng = np.random.default_rng(3)
+    d, r, K, s = 6, 3, 33, 200
+    sup = rng.integers(-16, 17, size=(s, d), dtype=np.int64)
+    c = rng.normal(size=s) + 1j * rng.normal(size=s)
+    base = rng.uniform(size=(d * r, d))
+    nodes = np.repeat(base, K, axis=0).reshape(d * r, K, d)
+    for q in range(d * r):
+        nodes[q, :, q // r] = np.arange(K) / K
+    sup_d, c_d, b_d = _dev.upload(sup), _dev.upload(c), _dev.upload(base)
+    X_d = _dev.upload(nodes.reshape(-1, d))
+    want = _dev.empty((d * r * K,), torch.complex128)
+    got = _dev.empty((d * r * K,), torch.complex128)
+    _native.call("sfftb_eval_dense", _dev.ptr(sup_d), s, d, _dev.ptr(c_d), _dev.ptr(X_d),
+                 d * r * K, _dev.ptr(want), _dev.stream())
+    _native.call("sfftb_eval_lines", _dev.ptr(sup_d), s, d, _dev.ptr(c_d), _dev.ptr(b_d),
+                 d * r, K, r, _dev.ptr(got), _dev.stream())
+    assert np.array_equal(_dev.download(got), _dev.download(want))
