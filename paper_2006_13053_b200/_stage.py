@@ -189,7 +189,9 @@ def buffers(A, desc, G, L, M, n, s, fused, slot):
     desc.bits = P(f"bits{slot}", rows * W, torch.int32)
     if fused:
         desc.samples = desc.sumsq = None
-        desc.ws_dft = A.bytes("ws_dft", lib.sfftb_sample_detect_workspace_bytes(rows, M))
+        # + slack for per-group 256-B aligned regions (stage.cu)
+        desc.ws_dft = A.bytes("ws_dft",
+                              lib.sfftb_sample_detect_workspace_bytes(rows, M) + 256 * G + 256)
     else:
         desc.samples = P("samples", 2 * rows * M, f64)
         desc.sumsq = P("sumsq", rows, f64)

@@ -7,6 +7,8 @@
 // _engine), composed here so the ~12 launches of a stage cost microseconds
 // of host time instead of ~0.3 ms of interpreter overhead while the GPU idles
 // between stages.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "../../include/sfft_b200.h"
 
@@ -82,7 +84,37 @@ int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
 
     // samples -> zero test, spectra, bitmaps
     SFFTB_TRY(mark(3));
-    if (listed) {
+    const char* split_env = getenv("SFFTB_SPLIT_GROUPS");
+    const bool split = listed && G >= 2 && split_env && atoi(split_env) > 0;
+    if (split) {
+        // one transform chain per group, alternating between this stream and a
+        // second one: a group's 5 passes stay in L2 and the two chains fill
+        // each other's kernel tails
+        static cudaStream_t st2[64] = {nullptr};
+        static cudaEvent_t evs[64][2];
+        int dev = 0;
+        SFFTB_CUDA(cudaGetDevice(&dev));
+        if (!st2[dev]) {
+            SFFTB_CUDA(cudaStreamCreateWithFlags(&st2[dev], cudaStreamNonBlocking));
+            SFFTB_CUDA(cudaEventCreateWithFlags(&evs[dev][0], cudaEventDisableTiming));
+            SFFTB_CUDA(cudaEventCreateWithFlags(&evs[dev][1], cudaEventDisableTiming));
+        }
+        SFFTB_CUDA(cudaEventRecord(evs[dev][0], st));
+        SFFTB_CUDA(cudaStreamWaitEvent(st2[dev], evs[dev][0], 0));
+        const int64_t W = sfftb_bitmap_words(M);
+        // per-group workspace regions, 256-B aligned (the caller's buffer has
+        // G * 256 bytes of slack: sfftb_stage_t.ws_dft)
+        const int64_t wsg = (sfftb_sample_detect_workspace_bytes(L, M) + 255) & ~int64_t(255);
+        for (int64_t g = 0; g < G; ++g) {
+            cudaStream_t sg = (g & 1) ? st2[dev] : st;
+            SFFTB_TRY(sfftb_sample_detect_dft_list(
+                list_r + g * L * a->s, a->bins + 2 * g * L * a->s, a->s, 1, L, M, a->noise_seed,
+                a->call0 + g * L, a->sigma, a->ghat + 2 * g * L * M, a->theta0 + g,
+                a->bits + g * L * W, (char*)a->ws_dft + g * wsg, sg));
+        }
+        SFFTB_CUDA(cudaEventRecord(evs[dev][1], st2[dev]));
+        SFFTB_CUDA(cudaStreamWaitEvent(st, evs[dev][1], 0));
+    } else if (listed) {
         SFFTB_TRY(sfftb_sample_detect_dft_list(list_r, a->bins, a->s, G, L, M, a->noise_seed,
                                                a->call0, a->sigma, a->ghat, a->theta0, a->bits,
                                                a->ws_dft, stream));
