@@ -140,3 +140,28 @@ def test_spectra_ahead_modes_bitwise(cuda, monkeypatch, name):
         assert np.array_equal(o.coeffs, base.coeffs)
         assert o.sample_count == base.sample_count
         assert o.stage_log == base.stage_log
+
+
+@pytest.mark.parametrize("d,r,sigma", [(2, 3, 0.0), (3, 2, 0.0), (3, 2, 1e-3), (5, 3, 0.0)])
+def test_sfft_few_dims_vs_oracle(cuda, oracle_lib, d, r, sigma):
+    """Few coordinate stages: the stage plans enqueued ahead reach the final
+    coefficient stage already at start-up (d <= the number of slots)."""
+    pkg = cuda
+    w = workloads.small_sfft(40 + d, d, 12, 60, r=r, sigma=sigma,
+                             theta=1e-6 if sigma else 1e-12)
+    p = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+    orc = pkg.oracle_from_poly(p, noise_sigma=w.sigma, noise_seed=w.noise_seed)
+    res = pkg.sfft(orc, pkg.Box(w.d, w.lo, w.hi),
+                   pkg.SfftParams(w.s, 0.9, theta=w.theta, r=w.r), seed=w.seed)
+    ref = oracle_lib.sfft(oracle_lib.PolyOracle(w.support, w.coeffs, mode="structured",
+                                                sigma=w.sigma, noise_seed=w.noise_seed),
+                          oracle_lib.Box(w.d, w.lo, w.hi), w.s, 0.9, w.seed, theta=w.theta,
+                          r=w.r)
+    assert np.array_equal(res.support.elems, ref[0])
+    assert res.sample_count == ref[2]
+    assert [(e["candidates"], e["kept"], e["samples"]) for e in res.stage_log] == \
+        [(e["candidates"], e["kept"], e["samples"]) for e in ref[3]]
+    assert workloads.rel_l2(res.coeffs, ref[1]) < 1e-10
+    if sigma == 0:
+        order = np.lexsort(w.support.T[::-1])
+        assert np.array_equal(res.support.elems, w.support[order])
