@@ -576,8 +576,8 @@ __device__ __forceinline__ double median_stable(const double (&v)[S], const doub
 }
 
 template <int S>
-__device__ __forceinline__ double2 warp_median2(const double (&re)[S], const double (&im)[S],
-                                                const double2* sv, int L, int lane) {
+__device__ __forceinline__ double2 warp_median2_exact(const double (&re)[S], const double (&im)[S],
+                                                      const double2* sv, int L, int lane) {
     int lr[S], li[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) lr[s] = li[s] = 0;
@@ -595,6 +595,86 @@ __device__ __forceinline__ double2 warp_median2(const double (&re)[S], const dou
     if (!fr) mr = median_stable<S>(re, sv, false, L, lane);
     if (!fi) mi = median_stable<S>(im, sv, true, L, lane);
     return make_double2(mr, mi);
+}
+
+// Top 31 bits of an order-preserving integer image of a double: monotone,
+// not strictly, in the double order (-0.0 sorts below +0.0 here; the exact
+// check below decides).
+__device__ __forceinline__ int32_t order_key31(double x) {
+    const long long b = __double_as_longlong(x);
+    return (int32_t)((b ^ ((b >> 63) & 0x7FFFFFFFFFFFFFFFLL)) >> 33);
+}
+
+// acc + (a < b) for |a|, |b| < 2^30: the sign bit of a - b, added with one
+// LEA.HI (the compiler's own lowering is a compare, a select and moves)
+__device__ __forceinline__ unsigned add_sign_bit(unsigned acc, int a, int b) {
+    unsigned d, r;
+    asm("sub.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    asm("{\n\t.reg .u32 t;\n\tshr.u32 t, %1, 31;\n\tadd.u32 %0, %2, t;\n\t}"
+        : "=r"(r) : "r"(d), "r"(acc));
+    return r;
+}
+
+// The lowest-index value whose approximate rank is floor(L/2), accepted only
+// when its exact rank is floor(L/2) and no other value compares equal to it:
+// then it is the stable-sort median whatever the approximate ranks were.
+template <int S>
+__device__ __forceinline__ bool median_verified(const double (&v)[S], const unsigned (&lt)[S],
+                                                int L, int lane, double& out) {
+    const int target = L >> 1;
+    bool found = false;
+    double p = 0.0;
+#pragma unroll
+    for (int s = S - 1; s >= 0; --s) {
+        const unsigned b = __ballot_sync(0xffffffffu, lane + 32 * s < L && (int)lt[s] == target);
+        if (b) {
+            p = __shfl_sync(0xffffffffu, v[s], __ffs(b) - 1);
+            found = true;
+        }
+    }
+    if (!found) return false;
+    int nlt = 0, neq = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const bool ok = lane + 32 * s < L;
+        nlt += __popc(__ballot_sync(0xffffffffu, ok && v[s] < p));
+        neq += __popc(__ballot_sync(0xffffffffu, ok && v[s] == p));
+    }
+    out = p;
+    return nlt == target && neq == 1;
+}
+
+// Componentwise median: ranks from 31-bit integer keys (two integer ops per
+// comparison instead of a DSETP and a select), each candidate verified
+// exactly; a component that fails verification (near-ties in the top bits,
+// equal values, signed zeros) takes the exact path.
+template <int S>
+__device__ __forceinline__ double2 warp_median2(const double (&re)[S], const double (&im)[S],
+                                                const double2* sv, const int2* sk, int L,
+                                                int lane) {
+    int kr[S], ki[S];
+    unsigned lr[S], li[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        kr[s] = order_key31(re[s]);
+        ki[s] = order_key31(im[s]);
+        lr[s] = li[s] = 0u;
+    }
+#pragma unroll 4
+    for (int j = 0; j < L; ++j) {
+        const int2 o = sk[j];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            lr[s] = add_sign_bit(lr[s], o.x, kr[s]);
+            li[s] = add_sign_bit(li[s], o.y, ki[s]);
+        }
+    }
+    double mr, mi;
+    const bool okr = median_verified<S>(re, lr, L, lane, mr);
+    const bool oki = median_verified<S>(im, li, L, lane, mi);
+    if (okr && oki) return make_double2(mr, mi);
+    const double2 e = warp_median2_exact<S>(re, im, sv, L, lane);
+    return make_double2(okr ? mr : e.x, oki ? mi : e.y);
 }
 
 // Residue tables of a Cartesian candidate set J = prefix x vals (the
@@ -616,6 +696,7 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                                                       int64_t cap, double2* __restrict__ coeffs,
                                                       PairTables pt = PairTables{}) {
     __shared__ double2 sv[8][32 * S];
+    __shared__ int2 sk[8][32 * S];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -628,6 +709,12 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
         int64_t k = w;
         while (k >= counts[g]) k -= counts[g++];
         const int64_t row = idx[(int64_t)g * cap + k];
+        int64_t i1 = 0, i2 = 0;
+        if (PAIRS) {  // row = i1 * n2 + i2 (< 2^32: 32-bit division)
+            const uint32_t q = (uint32_t)row / (uint32_t)pt.n2;
+            i1 = q;
+            i2 = row - (int64_t)q * pt.n2;
+        }
         double re[S], im[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -638,7 +725,6 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                 int64_t r;
                 if (PAIRS) {
                     const int64_t gl = (int64_t)g * L + l;
-                    const int64_t i1 = row / pt.n2, i2 = row - i1 * pt.n2;
                     r = (int64_t)pt.P[gl * pt.n1 + i1] + pt.V[gl * pt.n2 + i2];
                     if (r >= M) r -= M;
                 } else {
@@ -649,9 +735,10 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
                 im[s] = v.y;
             }
             sv[wib][l] = make_double2(re[s], im[s]);
+            sk[wib][l] = make_int2(order_key31(re[s]), order_key31(im[s]));
         }
         __syncwarp();
-        const double2 m = warp_median2<S>(re, im, sv[wib], L, lane);
+        const double2 m = warp_median2<S>(re, im, sv[wib], sk[wib], L, lane);
         if (lane == 0) coeffs[(int64_t)g * cap + k] = m;
         __syncwarp();  // the next row's stores wait for these reads
     }
@@ -1293,6 +1380,7 @@ extern "C" int sfftb_medians_pairs(const int32_t* P, const int32_t* V, int64_t n
                                    double* coeffs, void* stream) {
     SFFTB_REQUIRE(L >= 1 && L <= 128 && (L % 2) == 1, "medians require odd L <= 128");
     SFFTB_REQUIRE(G >= 1 && M >= 1 && n2 >= 1, "medians_pairs: bad sizes");
+    SFFTB_REQUIRE(n1 * n2 < (int64_t(1) << 32), "medians_pairs: n1 * n2 must be < 2^32");
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = num_sms() * 8;
     const PairTables pt{P, V, n1, n2};
