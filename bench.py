@@ -478,6 +478,45 @@ def measured_traffic(kernel):
         return None
 
 
+def _pipe_peaks():
+    """Measured FP64 FMA and IMAD pipe peaks (tools/micro/pipe_peaks.cu on a
+    B200 of this pool, profiles/r01/pipe_peaks.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                        "pipe_peaks.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def _fp64_frac(tflops):
+    pk = _pipe_peaks()
+    if not pk:
+        return {}
+    return {"fp64_peak_tflops": pk["fp64_fma_tflops"],
+            "fp64_frac": round(tflops / pk["fp64_fma_tflops"], 4),
+            "fp64_peak_source": "measured DFMA peak (profiles/r01/pipe_peaks.json)"}
+
+
+def _imad_bound(h):
+    """The hash kernel's integer-pipe floor: 12 IMAD-pipe ops per (row,
+    lattice) pair (10 for the dot product, 2 for the reduction; DESIGN.md
+    K3) at the measured IMAD lane rate."""
+    pk = _pipe_peaks()
+    if not pk:
+        return {}
+    pairs = h["n"] * h["L"]
+    floor_ms = pairs * 12 / (pk["imad_lanes_per_clk_per_sm"] * pk["sms"]
+                             * pk["clock_mhz"] * 1e6) * 1e3
+    return {"int_pipe": {"imad_per_pair": 12, "floor_ms": round(floor_ms, 3),
+                         "frac_of_floor": round(floor_ms / h["hash_ms"], 4),
+                         "note": "exact int64 residues need d multiply-adds per pair on the "
+                                 "IMAD pipe; its floor caps this kernel at "
+                                 f"{round(h['n'] * (8 * h['d'] + 8) / (floor_ms * 1e-3) / 1e9)} "
+                                 "GB/s of algorithmic traffic"}}
+
+
 def roofline_hash(h, peak, src):
     """Algorithmic bytes of one hashing launch: rows (n*8d) + int64 hits
     (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8)."""
@@ -490,7 +529,7 @@ def roofline_hash(h, peak, src):
     return {"bound": "hbm", "kernel": "hash_rows (sfftb_hash_hits)", "achieved": round(ach, 1),
             "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
             "algorithmic_bytes": bytes_, "peak_source": src,
-            "launch_ms": round(h["hash_ms"], 4)}
+            "launch_ms": round(h["hash_ms"], 4), **_imad_bound(h)}
 
 
 def fft_flops(N):
@@ -553,6 +592,7 @@ def roofline_sfft(r, peak, src):
                 "achieved": round(ach, 1), "frac": round(ach / peak, 4),
                 "algorithmic_bytes": int(bytes_),
                 "fp64_tflops": round(flops / (t * 1e-3) / 1e12, 3),
+                **_fp64_frac(flops / (t * 1e-3) / 1e12),
                 "algorithmic_flops": flops})
     return out
 
