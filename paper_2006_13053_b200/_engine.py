@@ -116,12 +116,30 @@ def gather(ghat, theta0, bits, M, zmat, G, L, rows, kbound, nu, want_medians=Tru
     return Batch(G, L, M, n, ghat, theta0, hits, idx, counts, coeffs)
 
 
+class PendingHost:
+    """A host array being filled by asynchronous device-to-host copies: the
+    numpy view is handed out once its event has completed."""
+
+    __slots__ = ("array", "event", "_keep")
+
+    def __init__(self, array, event, keep):
+        self.array, self.event, self._keep = array, event, keep
+
+    def result(self):
+        self.event.synchronize()
+        self._keep = None
+        return self.array
+
+
 def gather_streamed(ghat, theta0, bits, M, zmat, L, host_rows, kbound, nu, want_medians=True,
                     want_hits=False, chunk_rows=1 << 22):
     """gather() for one group whose candidate rows are still on the host:
     the rows go up in chunks on a copy stream while each landed chunk is
     hashed on the compute stream (PCIe and hashing overlap); compaction and
-    medians follow on the whole set.  Returns (Batch, device rows)."""
+    medians follow on the whole set.  With want_hits the hit counts of each
+    hashed chunk go down on a third stream while later chunks go up (PCIe is
+    full duplex), and Batch.hits is a PendingHost.  Returns (Batch, device
+    rows)."""
     n, d = int(host_rows.shape[0]), int(host_rows.shape[1])
     st = _dev.stream()
     dev = _dev.device()
@@ -134,6 +152,9 @@ def gather_streamed(ghat, theta0, bits, M, zmat, L, host_rows, kbound, nu, want_
     copy = torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream(dev)
     copy.wait_stream(main)  # the buffers above were allocated on the main stream
+    if hits is not None:
+        down = torch.cuda.Stream(device=dev)
+        hits_host = torch.empty((max(n, 1),), dtype=torch.int64, pin_memory=True)
     for c0 in range(0, n, chunk_rows):
         c1 = min(n, c0 + chunk_rows)
         with torch.cuda.stream(copy):
@@ -145,6 +166,12 @@ def gather_streamed(ghat, theta0, bits, M, zmat, L, host_rows, kbound, nu, want_
                      M, _dev.ptr(bits), int(kbound), min_hits,
                      None if hits is None else hits[c0:c1].data_ptr(),
                      detmask[c0 // 32:].data_ptr(), st)
+        if hits is not None:
+            hashed = torch.cuda.Event()
+            hashed.record(main)
+            down.wait_event(hashed)
+            with torch.cuda.stream(down):
+                hits_host[c0:c1].copy_(hits[c0:c1], non_blocking=True)
     rows.record_stream(copy)
     src_keep = src  # the host rows must outlive the async copies: synchronise below
     idx = _dev.empty((max(n, 1),), torch.int64)
@@ -162,6 +189,10 @@ def gather_streamed(ghat, theta0, bits, M, zmat, L, host_rows, kbound, nu, want_
                          st)
     copy.synchronize()
     del src_keep
+    if hits is not None:
+        done = torch.cuda.Event()
+        done.record(down)
+        hits = PendingHost(hits_host.numpy()[:n], done, (hits, hits_host, down))
     return Batch(1, L, M, n, ghat, theta0, hits, idx, counts, coeffs), rows[:n]
 
 

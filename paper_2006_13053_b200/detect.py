@@ -41,6 +41,8 @@ class ZeroTest:
 def _lazy_np(v):
     if isinstance(v, torch.Tensor):
         return _dev.download(v)
+    if isinstance(v, _engine.PendingHost):
+        return v.result()
     return v
 
 
