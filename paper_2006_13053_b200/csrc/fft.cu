@@ -507,8 +507,9 @@ struct Fs2Layout {
     static constexpr int DATA = F * SLOT;
 };
 
-template <int N2, bool INV, bool SPARSE = false>
-__global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
+template <int N2, bool INV, bool SPARSE = false, int N1C = 0>
+__global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1_rt) {
+    const int N1 = N1C ? N1C : N1_rt;  // compile-time N1: immediate offsets
     using Lay = Fs2Layout<N2>;
     constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
     extern __shared__ double2 smem[];
@@ -520,8 +521,9 @@ __global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1) {
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
     stage(lo, a.tw_lo, 64);
-    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
-    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    const bool hi_smem = N1C ? true : (bool)a.hi_in_smem;
+    if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = hi_smem ? hi_s : a.tw_hi;
     double2* slot = smem + f * SLOT;
     const int per_b = N1 / F;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -629,7 +631,9 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB(DftArgs a, int N2) {
 // layout [s][t]) in 212 double2 -- the +4 pad puts neighbouring rows in the
 // other half of the banks for the remapped middle pass.
 static constexpr int kR192Slot = 212;
-__global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2) {
+template <int N2C = 0>
+__global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
+    const int N2 = N2C ? N2C : N2_rt;  // compile-time N2: immediate offsets
     constexpr int N1 = 192, F = 16;
     extern __shared__ double2 smem[];
     double2* tw1 = smem + F * kR192Slot;  // e^{-2 pi i m/192}
@@ -643,8 +647,9 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2) {
     const int N = N1 * N2;
     stage(tw1, a.tw_n1, N1);
     stage(lo, a.tw_lo, 64);
-    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
-    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    const bool hi_smem = N2C ? true : (bool)a.hi_in_smem;
+    if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = hi_smem ? hi_s : a.tw_hi;
     double2* slot = smem + f * kR192Slot;
     double2* slot2 = smem + f2 * kR192Slot;
     const int per_b = N2 / F;
@@ -747,8 +752,12 @@ __global__ void __launch_bounds__(256, 2) fs2_colC(DftArgs a, int N1) {
 // four-step twiddle.  Samples never reach HBM.  colC_bits = detection colC
 // that also emits the nonzero bitmap (|ghat| > theta, _core.pyx:195).
 // ---------------------------------------------------------------------------
-template <int N2, bool NOISE>
-__global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
+// N1C: the row length N1 as a compile-time constant (0: runtime N1); with it
+// every load/store offset of a thread folds into an immediate, which keeps
+// the kernel inside its 128 registers without spilling addresses
+template <int N2, bool NOISE, int N1C = 0>
+__global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1_rt) {
+    const int N1 = N1C ? N1C : N1_rt;
     using Lay = Fs2Layout<N2>;
     constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
     extern __shared__ double2 smem[];
@@ -761,8 +770,10 @@ __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
     stage(lo, a.tw_lo, 64);
-    if (a.hi_in_smem) stage(hi_s, a.tw_hi, N / 64);
-    const double2* hi = a.hi_in_smem ? hi_s : a.tw_hi;
+    // compile-time N1: N <= 256 * 256, so N / 64 <= 2048 twiddles always fit
+    const bool hi_smem = N1C ? true : (bool)a.hi_in_smem;
+    if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = hi_smem ? hi_s : a.tw_hi;
     double2* slot = smem + f * SLOT;
     const int per_b = N1 / F;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -812,8 +823,9 @@ __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1) {
     }
 }
 
-template <int N2>
-__global__ void __launch_bounds__(256, 2) fs2_colC_bits(DftArgs a, int N1) {
+template <int N2, int N1C = 0>
+__global__ void __launch_bounds__(256, 2) fs2_colC_bits(DftArgs a, int N1_rt) {
+    const int N1 = N1C ? N1C : N1_rt;
     using Lay = Fs2Layout<N2>;
     constexpr int T = Lay::T, F = Lay::F, SLOT = Lay::SLOT;
     static_assert(F == 16 || F == 32, "bit groups of F consecutive bins");
@@ -975,8 +987,13 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
     c.ntiles = (int64_t)(N1 / Lay::F) * batch;
     const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
     if (first) {
-        SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE>, sm));
-        fs2_colA<N2, INV, SPARSE><<<grid, 256, sm, st>>>(c, N1);
+        if (N1 == 192) {
+            SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE, 192>, sm));
+            fs2_colA<N2, INV, SPARSE, 192><<<grid, 256, sm, st>>>(c, N1);
+        } else {
+            SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE>, sm));
+            fs2_colA<N2, INV, SPARSE><<<grid, 256, sm, st>>>(c, N1);
+        }
     } else {
         SFFTB_CUDA(allow_smem(fs2_colC<N2, INV>, sm));
         fs2_colC<N2, INV><<<grid, 256, sm, st>>>(c, N1);
@@ -991,8 +1008,9 @@ static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / 16) * batch;
     const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
-    SFFTB_CUDA(allow_smem(fs2_rowB192, sm));
-    fs2_rowB192<<<grid, 256, sm, st>>>(c, N2);
+    // (a compile-time N2 spills more here and is no faster: runtime N2)
+    SFFTB_CUDA(allow_smem(fs2_rowB192<>, sm));
+    fs2_rowB192<><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
@@ -1176,25 +1194,27 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         c.ntiles = (int64_t)(p->N1 / F) * batch;
         const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
         const size_t hi = a.hi_in_smem ? (size_t)(N / 64) : 0;
-        if (p->N2 == 256) {
-            const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256 + 64 + hi);
-            if (sigma > 0.0) {
-                SFFTB_CUDA(allow_smem(fs2_colCA<256, true>, sm));
-                fs2_colCA<256, true><<<grid, 256, sm, st>>>(c, p->N1);
-            } else {
-                SFFTB_CUDA(allow_smem(fs2_colCA<256, false>, sm));
-                fs2_colCA<256, false><<<grid, 256, sm, st>>>(c, p->N1);
-            }
-        } else {
-            const size_t sm = sizeof(double2) * (Fs2Layout<128>::DATA + 128 + 64 + hi);
-            if (sigma > 0.0) {
-                SFFTB_CUDA(allow_smem(fs2_colCA<128, true>, sm));
-                fs2_colCA<128, true><<<grid, 256, sm, st>>>(c, p->N1);
-            } else {
-                SFFTB_CUDA(allow_smem(fs2_colCA<128, false>, sm));
-                fs2_colCA<128, false><<<grid, 256, sm, st>>>(c, p->N1);
-            }
-        }
+        auto launch_ca = [&](auto kern, size_t sm) -> int {
+            SFFTB_CUDA(allow_smem(kern, sm));
+            kern<<<grid, 256, sm, st>>>(c, p->N1);
+            return SFFTB_OK;
+        };
+        const size_t sm256 = sizeof(double2) * (Fs2Layout<256>::DATA + 256 + 64 + hi);
+        const size_t sm128 = sizeof(double2) * (Fs2Layout<128>::DATA + 128 + 64 + hi);
+        int rcl = SFFTB_OK;
+        if (p->N2 == 256 && p->N1 == 192)
+            rcl = sigma > 0.0 ? launch_ca(fs2_colCA<256, true, 192>, sm256)
+                              : launch_ca(fs2_colCA<256, false, 192>, sm256);
+        else if (p->N2 == 256)
+            rcl = sigma > 0.0 ? launch_ca(fs2_colCA<256, true>, sm256)
+                              : launch_ca(fs2_colCA<256, false>, sm256);
+        else if (p->N1 == 192)
+            rcl = sigma > 0.0 ? launch_ca(fs2_colCA<128, true, 192>, sm128)
+                              : launch_ca(fs2_colCA<128, false, 192>, sm128);
+        else
+            rcl = sigma > 0.0 ? launch_ca(fs2_colCA<128, true>, sm128)
+                              : launch_ca(fs2_colCA<128, false>, sm128);
+        if (rcl) return rcl;
         SFFTB_CHECK_LAUNCH();
         const int per_b = p->N1 / F;
         partial_sumsq_reduce<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(a.sumsq_part, batch,
@@ -1215,8 +1235,13 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
         if (p->N2 == 256) {
             const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256);
-            SFFTB_CUDA(allow_smem(fs2_colC_bits<256>, sm));
-            fs2_colC_bits<256><<<grid, 256, sm, st>>>(c, p->N1);
+            if (p->N1 == 192) {
+                SFFTB_CUDA(allow_smem(fs2_colC_bits<256, 192>, sm));
+                fs2_colC_bits<256, 192><<<grid, 256, sm, st>>>(c, p->N1);
+            } else {
+                SFFTB_CUDA(allow_smem(fs2_colC_bits<256>, sm));
+                fs2_colC_bits<256><<<grid, 256, sm, st>>>(c, p->N1);
+            }
         } else {
             const size_t sm = sizeof(double2) * (Fs2Layout<128>::DATA + 128);
             SFFTB_CUDA(allow_smem(fs2_colC_bits<128>, sm));

@@ -14,7 +14,7 @@ import paper_2006_13053_b200 as pkg  # noqa: E402
 from paper_2006_13053_b200 import _dev, _native  # noqa: E402
 import workloads  # noqa: E402
 
-w = workloads.metric_config()
+w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "metric_config")()
 box = pkg.Box(w.d, w.lo, w.hi)
 params = pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
 poly = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
