@@ -647,9 +647,10 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
     const int N = N1 * N2;
     stage(tw1, a.tw_n1, N1);
     stage(lo, a.tw_lo, 64);
-    const bool hi_smem = N2C ? true : (bool)a.hi_in_smem;
-    if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
-    const double2* hi = hi_smem ? hi_s : a.tw_hi;
+    // N = 192 * N2 <= 49152: the N / 64 <= 768 high twiddles always fit in
+    // shared memory (a.hi_in_smem is set for them), so no generic pointer
+    stage(hi_s, a.tw_hi, N / 64);
+    const double2* hi = hi_s;
     double2* slot = smem + f * kR192Slot;
     double2* slot2 = smem + f2 * kR192Slot;
     const int per_b = N2 / F;
@@ -1003,7 +1004,7 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
 }
 
 static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
-    const size_t hi = a.hi_in_smem ? (size_t)(192 * N2 / 64) : 0;
+    const size_t hi = (size_t)(192 * N2 / 64);  // always staged (fs2_rowB192)
     const size_t sm = sizeof(double2) * (16 * kR192Slot + 192 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / 16) * batch;
