@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/sfft_b200.h"
 
@@ -160,6 +161,41 @@ __device__ __forceinline__ double2 harness_noise(uint64_t seed, uint64_t call, i
     sincospi(2.0 * u2, &sn, &cs);
     return make_double2(rad * cs, rad * sn);
 }
+}  // namespace sfftb
+
+// ---- programmatic dependent launch (sm_90+) ----
+// pdl_wait: block until the preceding kernel of the stream has completed and
+// its writes are visible (no-op when not launched with PDL); pdl_launch: let
+// the next kernel of the stream start launching (its CTAs fill SMs as ours
+// exit and run their prologue until their own pdl_wait).
+namespace sfftb {
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// <<<>>> or, with pdl, cudaLaunchKernelEx with programmatic stream
+// serialization (the kernel must pdl_wait before reading its predecessor's
+// output)
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(Exp...), dim3 grid, dim3 block,
+                                    size_t smem, cudaStream_t st, Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+}
+
+// zero-test thresholds (hash.cu) launched inside the fused transform chain
+int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,
+                           cudaStream_t st, bool pdl);
 }  // namespace sfftb
 
 // ---- mbarrier + 1-D bulk copy (TMA engine) helpers, sm_90+/sm_100a ----

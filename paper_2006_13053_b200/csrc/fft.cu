@@ -266,6 +266,7 @@ struct DftArgs {
     const uint32_t* lr;
     const double2* lv;
     int64_t ls;
+    int pdl = 0;  // launch the fused chain's kernels with programmatic dependent launch
 };
 
 template <bool C>
@@ -524,6 +525,8 @@ __global__ void __launch_bounds__(256, 2) fs2_colA(DftArgs a, int N1_rt) {
     const bool hi_smem = N1C ? true : (bool)a.hi_in_smem;
     if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = hi_smem ? hi_s : a.tw_hi;
+    pdl_wait();    // the predecessor's output (constant tables staged above)
+    pdl_launch();
     double2* slot = smem + f * SLOT;
     const int per_b = N1 / F;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -651,6 +654,8 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
     // shared memory (a.hi_in_smem is set for them), so no generic pointer
     stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = hi_s;
+    pdl_wait();    // the predecessor's output (constant tables staged above)
+    pdl_launch();
     double2* slot = smem + f * kR192Slot;
     double2* slot2 = smem + f2 * kR192Slot;
     const int per_b = N2 / F;
@@ -775,6 +780,8 @@ __global__ void __launch_bounds__(256, 2) fs2_colCA(DftArgs a, int N1_rt) {
     const bool hi_smem = N1C ? true : (bool)a.hi_in_smem;
     if (hi_smem) stage(hi_s, a.tw_hi, N / 64);
     const double2* hi = hi_smem ? hi_s : a.tw_hi;
+    pdl_wait();    // the predecessor's output (constant tables staged above)
+    pdl_launch();
     double2* slot = smem + f * SLOT;
     const int per_b = N1 / F;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -837,6 +844,8 @@ __global__ void __launch_bounds__(256, 2) fs2_colC_bits(DftArgs a, int N1_rt) {
     const int lane = tid & 31;
     const int N = N1 * N2;
     stage(tw2, a.tw_n2, N2);
+    pdl_wait();    // the predecessor's output (constant tables staged above)
+    pdl_launch();
     double2* slot = smem + f * SLOT;
     const int per_b = N1 / F;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -880,6 +889,8 @@ __global__ void __launch_bounds__(256, 2) fs2_colC_bits(DftArgs a, int N1_rt) {
 
 __global__ void partial_sumsq_reduce(const double* __restrict__ part, int64_t rows, int per_b,
                                      double* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
          r += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -990,7 +1001,8 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
     if (first) {
         if (N1 == 192) {
             SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE, 192>, sm));
-            fs2_colA<N2, INV, SPARSE, 192><<<grid, 256, sm, st>>>(c, N1);
+            SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_colA<N2, INV, SPARSE, 192>, dim3(grid),
+                                        dim3(256), sm, st, c, N1));
         } else {
             SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE>, sm));
             fs2_colA<N2, INV, SPARSE><<<grid, 256, sm, st>>>(c, N1);
@@ -1011,7 +1023,7 @@ static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
     // (a compile-time N2 spills more here and is no faster: runtime N2)
     SFFTB_CUDA(allow_smem(fs2_rowB192<>, sm));
-    fs2_rowB192<><<<grid, 256, sm, st>>>(c, N2);
+    SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_rowB192<>, dim3(grid), dim3(256), sm, st, c, N2));
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
@@ -1177,6 +1189,11 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
     a.lr = lr;
     a.lv = (const double2*)lv;
     a.ls = ls;
+    {
+        const char* e = getenv("SFFTB_PDL");
+        a.pdl = (!e || atoi(e) != 0) && p->N1 == 192 && p->N2 == 256;
+    }
+    SFFTB_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * batch * a.W, st));
     // sampler: inverse DFT (scale 1) -- colA (conj input) and rowB
     a.scale = 1.0;
     if (lr)
@@ -1197,7 +1214,7 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         const size_t hi = a.hi_in_smem ? (size_t)(N / 64) : 0;
         auto launch_ca = [&](auto kern, size_t sm) -> int {
             SFFTB_CUDA(allow_smem(kern, sm));
-            kern<<<grid, 256, sm, st>>>(c, p->N1);
+            SFFTB_CUDA(launch_maybe_pdl(c.pdl, kern, dim3(grid), dim3(256), sm, st, c, (int)p->N1));
             return SFFTB_OK;
         };
         const size_t sm256 = sizeof(double2) * (Fs2Layout<256>::DATA + 256 + 64 + hi);
@@ -1218,16 +1235,17 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         if (rcl) return rcl;
         SFFTB_CHECK_LAUNCH();
         const int per_b = p->N1 / F;
-        partial_sumsq_reduce<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(a.sumsq_part, batch,
-                                                                             per_b, sumsq);
+        SFFTB_CUDA(launch_maybe_pdl(a.pdl, partial_sumsq_reduce, dim3((unsigned)ceil_div(batch, 128)),
+                                    dim3(128), 0, st, (const double*)a.sumsq_part, batch, per_b,
+                                    sumsq));
         SFFTB_CHECK_LAUNCH();
     }
-    rc = sfftb_zero_thresholds(sumsq, G, L, M, theta, st);
+    rc = zero_thresholds_launch(sumsq, G, L, M, theta, st, a.pdl != 0);
     if (rc) return rc;
     // detection: rowB, then colC emitting ghat (scale 1/M) and the bitmap
+    // (bits zeroed at the start of the chain, so the two kernels are adjacent)
     rc = fs2_rows_any(a, batch, p->N1, p->N2, st);
     if (rc) return rc;
-    SFFTB_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * batch * a.W, st));
     {
         DftArgs c = a;
         c.scale = 1.0 / (double)M;
@@ -1238,7 +1256,8 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
             const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256);
             if (p->N1 == 192) {
                 SFFTB_CUDA(allow_smem(fs2_colC_bits<256, 192>, sm));
-                fs2_colC_bits<256, 192><<<grid, 256, sm, st>>>(c, p->N1);
+                SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_colC_bits<256, 192>, dim3(grid), dim3(256),
+                                            sm, st, c, (int)p->N1));
             } else {
                 SFFTB_CUDA(allow_smem(fs2_colC_bits<256>, sm));
                 fs2_colC_bits<256><<<grid, 256, sm, st>>>(c, p->N1);

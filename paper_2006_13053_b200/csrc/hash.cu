@@ -957,6 +957,8 @@ __global__ void sumsq_kernel(const double2* __restrict__ x, int64_t stride, int6
 // #{j < i : v_j == v_i}), the holders of ranks (L-1)/2 and L/2 publish them.
 __global__ void zero_threshold_kernel(const double* __restrict__ sumsq, int G, int L, int64_t M,
                                       double* __restrict__ theta) {
+    pdl_wait();  // inside the fused chain: the partial sums of the previous kernel
+    pdl_launch();
     extern __shared__ double zt_v[];
     __shared__ double mids[2];
     const int g = blockIdx.x;
@@ -1420,15 +1422,22 @@ extern "C" int sfftb_sumsq(const double* x, int64_t stride, int64_t batch, int64
     return SFFTB_OK;
 }
 
-extern "C" int sfftb_zero_thresholds(const double* sumsq, int64_t G, int64_t L, int64_t M,
-                                     double* theta, void* stream) {
+namespace sfftb {
+int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,
+                           cudaStream_t st, bool pdl) {
     SFFTB_REQUIRE(L >= 1 && L <= 256, "zero test: 1 <= L <= 256");
     const size_t zsm = sizeof(double) * (size_t)L;
     SFFTB_CUDA(smem_opt_in(zero_threshold_kernel, zsm));
-    zero_threshold_kernel<<<(unsigned)G, 128, zsm, (cudaStream_t)stream>>>(sumsq, (int)G, (int)L,
-                                                                         M, theta);
+    SFFTB_CUDA(launch_maybe_pdl(pdl, zero_threshold_kernel, dim3((unsigned)G), dim3(128), zsm, st,
+                                sumsq, (int)G, (int)L, M, theta));
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
+}
+}  // namespace sfftb
+
+extern "C" int sfftb_zero_thresholds(const double* sumsq, int64_t G, int64_t L, int64_t M,
+                                     double* theta, void* stream) {
+    return zero_thresholds_launch(sumsq, G, L, M, theta, (cudaStream_t)stream, false);
 }
 
 extern "C" int sfftb_mark_indices(const int64_t* idx, const int64_t* counts, int64_t G,
