@@ -15,7 +15,9 @@ import threading
 from .errors import ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libsfftb200.so")
+# SFFTB_LIB_PATH: an alternative build of the same library (A/B timing of
+# kernel variants on one box); the in-tree build otherwise
+LIB_PATH = os.environ.get("SFFTB_LIB_PATH") or os.path.join(HERE, "_lib", "libsfftb200.so")
 
 SFFTB_OK, SFFTB_EINVAL, SFFTB_ENOMEM, SFFTB_ECUDA = 0, 1, 2, 3
 
