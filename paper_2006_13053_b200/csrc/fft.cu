@@ -269,6 +269,21 @@ struct DftArgs {
     int pdl = 0;  // launch the fused chain's kernels with programmatic dependent launch
 };
 
+// Grid of the four-step passes: 8 CTAs per SM (2 resident at a time), each
+// striding over ~2 tiles at the metric's stage shape.  Measured on B200 against
+// fully persistent grids (2 per SM): the reconstruction 4.40 -> 4.17 ms, the
+// standalone chain 0.405 -> 0.395 ms -- finer CTA granularity lets the
+// high-priority detection kernels of the other stream interleave, and evens
+// out the last wave (tools/env_sweep.sh SFFTB_FS_CTAS 2 4 6 8 12 16 100).
+static int fs_grid(int64_t ntiles) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        const char* e = getenv("SFFTB_FS_CTAS");
+        per_sm = e ? std::max(1, atoi(e)) : 8;
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm));
+}
+
 template <bool C>
 __device__ __forceinline__ double2 conj_if(double2 v) {
     return C ? make_double2(v.x, -v.y) : v;
@@ -939,7 +954,7 @@ static int launch_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st,
     const size_t sm = sizeof(double2) * (Lay::DATA + N2 + (first ? 64 + hi : 0));
     DftArgs c = a;
     c.ntiles = (int64_t)(N1 / F) * batch;
-    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    const int grid = fs_grid(c.ntiles);
     if (first) {
         SFFTB_CUDA(allow_smem(fs_colA<N2, INV>, sm));
         fs_colA<N2, INV><<<grid, 256, sm, st>>>(c, N1);
@@ -960,7 +975,7 @@ static int launch_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     SFFTB_CUDA(allow_smem(fs_rowB<N1>, sm));
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / F) * batch;
-    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    const int grid = fs_grid(c.ntiles);
     fs_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
@@ -997,7 +1012,7 @@ static int fs2_cols(const DftArgs& a, int64_t batch, int N1, cudaStream_t st, bo
     const size_t sm = sizeof(double2) * (Lay::DATA + N2 + (first ? 64 + hi : 0));
     DftArgs c = a;
     c.ntiles = (int64_t)(N1 / Lay::F) * batch;
-    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    const int grid = fs_grid(c.ntiles);
     if (first) {
         if (N1 == 192) {
             SFFTB_CUDA(allow_smem(fs2_colA<N2, INV, SPARSE, 192>, sm));
@@ -1020,7 +1035,7 @@ static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     const size_t sm = sizeof(double2) * (16 * kR192Slot + 192 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / 16) * batch;
-    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    const int grid = fs_grid(c.ntiles);
     // (a compile-time N2 spills more here and is no faster: runtime N2)
     SFFTB_CUDA(allow_smem(fs2_rowB192<>, sm));
     SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_rowB192<>, dim3(grid), dim3(256), sm, st, c, N2));
@@ -1038,7 +1053,7 @@ static int fs2_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
     const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / Lay::F) * batch;
-    const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+    const int grid = fs_grid(c.ntiles);
     SFFTB_CUDA(allow_smem(fs2_rowB<N1>, sm));
     fs2_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();
@@ -1210,7 +1225,7 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         const int F = p->N2 == 256 ? Fs2Layout<256>::F : Fs2Layout<128>::F;
         DftArgs c = a;
         c.ntiles = (int64_t)(p->N1 / F) * batch;
-        const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+        const int grid = fs_grid(c.ntiles);
         const size_t hi = a.hi_in_smem ? (size_t)(N / 64) : 0;
         auto launch_ca = [&](auto kern, size_t sm) -> int {
             SFFTB_CUDA(allow_smem(kern, sm));
@@ -1251,7 +1266,7 @@ static int sample_detect(const double* bins, const uint32_t* lr, const double* l
         c.scale = 1.0 / (double)M;
         const int F = p->N2 == 256 ? Fs2Layout<256>::F : Fs2Layout<128>::F;
         c.ntiles = (int64_t)(p->N1 / F) * batch;
-        const int grid = (int)std::min<int64_t>(c.ntiles, (int64_t)num_sms() * 2);
+        const int grid = fs_grid(c.ntiles);
         if (p->N2 == 256) {
             const size_t sm = sizeof(double2) * (Fs2Layout<256>::DATA + 256);
             if (p->N1 == 192) {
