@@ -221,7 +221,7 @@ def run_sfft_arm(args, world, rank):
     orig_run = _stage.run
 
     def run_rec(desc, stream=None):
-        if desc.phase != 2:  # the calls that run transforms (whole stage or spectra)
+        if desc.phase in (0, 1, 4):  # the calls that run transforms
             shapes.append((desc.G, desc.L, desc.M, bool(desc.fused)))
         return orig_run(desc, stream)
 

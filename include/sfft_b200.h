@@ -474,7 +474,9 @@ typedef struct {
      * the candidate set, so the driver enqueues them for stage t+1 before it
      * waits for stage t's counts.  2: the rest (candidates, hashing,
      * compaction, medians, top-s, union) on the spectra of an earlier phase-1
-     * call with the same G, L, M, zmat and call0. */
+     * call with the same G, L, M, zmat and call0.  3 and 4 split phase 1: the
+     * sampler (zmat/tails copies, anchor, scatter into bins) and the
+     * transforms on those bins, so the sampler can run on another stream. */
     int64_t phase;
 } sfftb_stage_t;
 

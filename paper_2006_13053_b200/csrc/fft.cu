@@ -275,13 +275,16 @@ struct DftArgs {
 // standalone chain 0.405 -> 0.395 ms -- finer CTA granularity lets the
 // high-priority detection kernels of the other stream interleave, and evens
 // out the last wave (tools/env_sweep.sh SFFTB_FS_CTAS 2 4 6 8 12 16 100).
-static int fs_grid(int64_t ntiles) {
-    static int per_sm = -1;
+static int fs_grid(int64_t ntiles, bool rows = false) {
+    static int per_sm = -1, per_sm_rows = -1;
     if (per_sm < 0) {
         const char* e = getenv("SFFTB_FS_CTAS");
         per_sm = e ? std::max(1, atoi(e)) : 8;
+        const char* er = getenv("SFFTB_FS_CTAS_ROWS");
+        per_sm_rows = er ? std::max(1, atoi(er)) : 16;  // rows: 16 measured ~0.5% better
     }
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm));
+    const int k = rows ? per_sm_rows : per_sm;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * k));
 }
 
 template <bool C>
@@ -1035,7 +1038,7 @@ static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     const size_t sm = sizeof(double2) * (16 * kR192Slot + 192 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / 16) * batch;
-    const int grid = fs_grid(c.ntiles);
+    const int grid = fs_grid(c.ntiles, true);
     // (a compile-time N2 spills more here and is no faster: runtime N2)
     SFFTB_CUDA(allow_smem(fs2_rowB192<>, sm));
     SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_rowB192<>, dim3(grid), dim3(256), sm, st, c, N2));
@@ -1053,7 +1056,7 @@ static int fs2_rows(const DftArgs& a, int64_t batch, int N2, cudaStream_t st) {
     const size_t sm = sizeof(double2) * (Lay::DATA + N1 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / Lay::F) * batch;
-    const int grid = fs_grid(c.ntiles);
+    const int grid = fs_grid(c.ntiles, true);
     SFFTB_CUDA(allow_smem(fs2_rowB<N1>, sm));
     fs2_rowB<N1><<<grid, 256, sm, st>>>(c, N2);
     SFFTB_CHECK_LAUNCH();

@@ -45,11 +45,22 @@ int stage_candidates(const sfftb_stage_t* a, void* stream, const Marks& mark) {
     return SFFTB_OK;
 }
 
-// generators/tails H2D, structured sampler, transforms -> ghat, theta0, bits
-int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
+// generators/tails H2D, structured sampler (parts & 1), transforms -> ghat,
+// theta0, bits (parts & 2)
+int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark, int parts) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t G = a->G, L = a->L, M = a->M, tdim = a->tdim;
     const int64_t rows = G * L;
+    // fused path with few coefficients: sparse bins (residue lists) in the
+    // bins buffer -- no dense zero fill, the first column pass drops them in
+    static const bool lists_on = [] {
+        const char* e = getenv("SFFTB_LISTS");
+        return !e || atoi(e) != 0;
+    }();
+    const bool listed = lists_on && a->fused && a->s >= 1 && a->s <= 4096 &&
+                        M <= (int64_t(1) << 24) && M >= 2 * a->s;
+    uint32_t* list_r = reinterpret_cast<uint32_t*>(a->bins + 2 * rows * a->s);
+    if (parts & 1) {
     SFFTB_TRY(mark(2));
     if (a->zmat_host_ld > 0 && a->zmat_host_ld != L * tdim) {
         SFFTB_REQUIRE(a->zmat_host_ld >= L * tdim, "stage: zmat_host_ld < L*tdim");
@@ -70,11 +81,6 @@ int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
     if (a->s > 0)
         SFFTB_TRY(sfftb_anchor_coeffs(a->support, a->s, a->d, tdim, a->coeffs, a->tails, G,
                                       a->anchored, stream));
-    // fused path with few coefficients: sparse bins (residue lists) in the
-    // bins buffer -- no dense zero fill, the first column pass drops them in
-    const bool listed = a->fused && a->s >= 1 && a->s <= 4096 && M <= (int64_t(1) << 24) &&
-                        M >= 2 * a->s;
-    uint32_t* list_r = reinterpret_cast<uint32_t*>(a->bins + 2 * rows * a->s);
     if (listed)
         SFFTB_TRY(sfftb_scatter_list(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L,
                                      M, list_r, a->bins, stream));
@@ -82,8 +88,12 @@ int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark) {
         SFFTB_TRY(sfftb_scatter_bins(a->support, a->s, a->d, tdim, a->anchored, a->zmat, G, L,
                                      M, a->bins, nullptr, stream));
 
-    // samples -> zero test, spectra, bitmaps
     SFFTB_TRY(mark(3));
+    }
+    if (!(parts & 2)) return SFFTB_OK;
+
+    // samples -> zero test, spectra, bitmaps
+    if (!(parts & 1)) SFFTB_TRY(mark(3));
     const char* split_env = getenv("SFFTB_SPLIT_GROUPS");
     const bool split = listed && G >= 2 && split_env && atoi(split_env) > 0;
     if (split) {
@@ -217,10 +227,12 @@ extern "C" int sfftb_sfft_stage(const sfftb_stage_t* a, void* stream) {
     SFFTB_REQUIRE(a->G >= 1 && a->L >= 1 && a->M >= 1 && a->tdim >= 1 && a->n >= 0,
                   "stage: bad sizes");
     SFFTB_REQUIRE(a->d >= a->tdim && a->tail_w >= 1, "stage: bad dimensions");
-    SFFTB_REQUIRE(a->phase >= 0 && a->phase <= 2, "stage: phase must be 0, 1 or 2");
+    SFFTB_REQUIRE(a->phase >= 0 && a->phase <= 4, "stage: phase must be 0 .. 4");
     const Marks mark{a, (cudaStream_t)stream};
-    if (a->phase == 1) return stage_spectra(a, stream, mark);
+    if (a->phase == 1) return stage_spectra(a, stream, mark, 3);
+    if (a->phase == 3) return stage_spectra(a, stream, mark, 1);
+    if (a->phase == 4) return stage_spectra(a, stream, mark, 2);
     SFFTB_TRY(stage_candidates(a, stream, mark));
-    if (a->phase == 0) SFFTB_TRY(stage_spectra(a, stream, mark));
+    if (a->phase == 0) SFFTB_TRY(stage_spectra(a, stream, mark, 3));
     return stage_detect(a, stream, mark);
 }

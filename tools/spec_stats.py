@@ -30,5 +30,5 @@ for name in ("metric_config", "config3", "config5", "config2"):
              seed=w.seed)
     torch.cuda.synchronize()
     ph = [c[0] for c in calls]
-    print(name, "spectra", ph.count(1), "reused", ph.count(2), "fallback", ph.count(0))
+    print(name, "spectra", ph.count(1) + ph.count(4), "reused", ph.count(2), "fallback", ph.count(0))
     print("   ", [(c[0], c[2], c[3]) for c in calls])

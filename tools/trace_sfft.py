@@ -57,7 +57,7 @@ def run(desc, stream=None):
     e0.record(st)
     orig_run(desc, stream)
     e1.record(st)
-    kind = {0: "stage", 1: "spectra", 2: "detect"}[int(desc.phase)]
+    kind = {0: "stage", 1: "spectra", 2: "detect", 3: "sampler", 4: "transforms"}[int(desc.phase)]
     log.append((f"<{kind} G={desc.G} L={desc.L} M={desc.M} n={desc.n}>", h, time.perf_counter(),
                 e0, e1))
 
