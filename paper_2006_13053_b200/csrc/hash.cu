@@ -686,7 +686,9 @@ struct PairTables {
     int64_t n1, n2;
 };
 
-template <int S, bool PAIRS = false>
+// SMALL (pair tables): every table / spectrum offset < 2^31, so the per-row
+// index arithmetic is 32-bit
+template <int S, bool PAIRS = false, bool SMALL = false>
 __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict__ elems, int d,
                                                       const int64_t* __restrict__ zmat, int G,
                                                       int L, int64_t M,
@@ -702,12 +704,17 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     // one flat work list over the groups' detected rows (g, k), so small
     // groups do not serialise one latency-bound round per group
+    __shared__ int64_t cnt_s[32];
+    const bool cnt_in_smem = G <= 32;
+    if (cnt_in_smem && threadIdx.x < G) cnt_s[threadIdx.x] = counts[threadIdx.x];
+    __syncthreads();
+    const int64_t* cnt = cnt_in_smem ? cnt_s : counts;
     int64_t total = 0;
-    for (int g = 0; g < G; ++g) total += counts[g];
+    for (int g = 0; g < G; ++g) total += cnt[g];
     for (int64_t w = gwarp; w < total; w += nwarps) {
         int g = 0;
         int64_t k = w;
-        while (k >= counts[g]) k -= counts[g++];
+        while (k >= cnt[g]) k -= cnt[g++];
         const int64_t row = idx[(int64_t)g * cap + k];
         int64_t i1 = 0, i2 = 0;
         if (PAIRS) {  // row = i1 * n2 + i2 (< 2^32: 32-bit division)
@@ -723,14 +730,24 @@ __global__ void __launch_bounds__(256) medians_kernel(const int64_t* __restrict_
             im[s] = 0.0;
             if (l < L) {
                 int64_t r;
-                if (PAIRS) {
-                    const int64_t gl = (int64_t)g * L + l;
-                    r = (int64_t)pt.P[gl * pt.n1 + i1] + pt.V[gl * pt.n2 + i2];
-                    if (r >= M) r -= M;
+                double2 v;
+                if (PAIRS && SMALL) {
+                    const uint32_t gl = (uint32_t)(g * L + l);
+                    uint32_t r32 = (uint32_t)pt.P[gl * (uint32_t)pt.n1 + (uint32_t)i1] +
+                                   (uint32_t)pt.V[gl * (uint32_t)pt.n2 + (uint32_t)i2];
+                    if (r32 >= (uint32_t)M) r32 -= (uint32_t)M;
+                    v = ghat[gl * (uint32_t)M + r32];
                 } else {
-                    r = residue_exact(elems + row * d, zmat + ((int64_t)g * L + l) * d, d, M);
+                    if (PAIRS) {
+                        const int64_t gl = (int64_t)g * L + l;
+                        r = (int64_t)pt.P[gl * pt.n1 + i1] + pt.V[gl * pt.n2 + i2];
+                        if (r >= M) r -= M;
+                    } else {
+                        r = residue_exact(elems + row * d, zmat + ((int64_t)g * L + l) * d, d,
+                                          M);
+                    }
+                    v = ghat[((int64_t)g * L + l) * M + r];
                 }
-                const double2 v = ghat[((int64_t)g * L + l) * M + r];
                 re[s] = v.x;
                 im[s] = v.y;
             }
@@ -1386,18 +1403,19 @@ extern "C" int sfftb_medians_pairs(const int32_t* P, const int32_t* V, int64_t n
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = num_sms() * 8;
     const PairTables pt{P, V, n1, n2};
+    const int64_t lim = int64_t(1) << 31;
+    const bool small = G * L * std::max<int64_t>(std::max<int64_t>(n1, n2), M) < lim;
+    auto go = [&](auto kern) {
+        kern<<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
+                                     (const double2*)ghat, idx, counts, cap, (double2*)coeffs,
+                                     pt);
+    };
     if (L <= 32)
-        medians_kernel<1, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
-                                                        (const double2*)ghat, idx, counts, cap,
-                                                        (double2*)coeffs, pt);
+        small ? go(medians_kernel<1, true, true>) : go(medians_kernel<1, true>);
     else if (L <= 64)
-        medians_kernel<2, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
-                                                        (const double2*)ghat, idx, counts, cap,
-                                                        (double2*)coeffs, pt);
+        small ? go(medians_kernel<2, true, true>) : go(medians_kernel<2, true>);
     else
-        medians_kernel<4, true><<<blocks, 256, 0, st>>>(nullptr, 0, nullptr, (int)G, (int)L, M,
-                                                        (const double2*)ghat, idx, counts, cap,
-                                                        (double2*)coeffs, pt);
+        small ? go(medians_kernel<4, true, true>) : go(medians_kernel<4, true>);
     SFFTB_CHECK_LAUNCH();
     return SFFTB_OK;
 }
