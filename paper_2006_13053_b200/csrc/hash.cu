@@ -415,9 +415,9 @@ __global__ void nonzero_bitmap_kernel(const double2* __restrict__ ghat, int64_t 
 // compaction of a per-row bitmask into ascending indices
 // ---------------------------------------------------------------------------
 
-static constexpr int kCompactWordsPerBlock = 4096;
+static constexpr int kCompactWordsPerBlock = 512;  // 16k rows per block
 static constexpr int kCompactThreads = 256;
-static constexpr int64_t kCompactSingleWords = 8192;  // one 1024-thread CTA per group
+static constexpr int64_t kCompactSingleWords = 1024;  // one 1024-thread CTA per group
 
 __global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
                               int64_t nblk, int64_t* __restrict__ blocksum) {
@@ -437,18 +437,51 @@ __global__ void compact_count(const uint32_t* __restrict__ mask, int64_t nwords,
     if (threadIdx.x == 0) blocksum[(int64_t)g * nblk + blockIdx.x] = red[0];
 }
 
-__global__ void compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts, int64_t cap,
-                             int64_t* totals) {
+// Exclusive scan of a group's per-block counts, one CTA of kCompactScanThreads
+// per group: chunks of blockDim entries, warp shuffles + one shared pass each.
+static constexpr int kCompactScanThreads = 1024;
+
+__global__ void __launch_bounds__(kCompactScanThreads)
+    compact_scan(int64_t* blocksum, int64_t nblk, int64_t* counts, int64_t cap,
+                 int64_t* totals) {
     const int g = blockIdx.x;
-    if (threadIdx.x != 0) return;
-    int64_t run = 0;
-    for (int64_t b = 0; b < nblk; ++b) {
-        const int64_t v = blocksum[(int64_t)g * nblk + b];
-        blocksum[(int64_t)g * nblk + b] = run;
-        run += v;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int64_t wsum[kCompactScanThreads / 32];
+    __shared__ int64_t carry_s;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    int64_t* bs = blocksum + (int64_t)g * nblk;
+    for (int64_t c0 = 0; c0 < nblk; c0 += blockDim.x) {
+        const int64_t b = c0 + threadIdx.x;
+        const int64_t v = b < nblk ? bs[b] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t x = lane < (int)(blockDim.x / 32) ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t t = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += t;
+            }
+            if (lane < (int)(blockDim.x / 32)) wsum[lane] = x;  // inclusive warp prefix
+        }
+        __syncthreads();
+        const int64_t base = carry_s + (warp ? wsum[warp - 1] : 0);
+        if (b < nblk) bs[b] = base + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s += wsum[blockDim.x / 32 - 1];
+        __syncthreads();
     }
-    counts[g] = min(run, cap);
-    if (totals) totals[g] = run;
+    if (threadIdx.x == 0) {
+        counts[g] = min(carry_s, cap);
+        if (totals) totals[g] = carry_s;
+    }
 }
 
 // SINGLE: one CTA per group walks all words with a running carry and writes
@@ -481,15 +514,23 @@ __global__ void __launch_bounds__(NT)
         __syncthreads();
         int64_t before = carry;
         for (int k = 0; k < warp; ++k) before += warp_tot[k];
-        int64_t pos = before + incl - cnt;
-        uint32_t b = bitsw;
-        while (b) {
-            const int bit = __ffs(b) - 1;
-            b &= b - 1;
-            const int64_t row = w * 32 + bit;
-            if (row < n) {
-                if (pos < cap) idx[(int64_t)g * cap + pos] = row;
-                ++pos;
+        const int64_t pos = before + incl - cnt;
+        // expand the warp's 32 words cooperatively: for each word, lane j
+        // writes row 32 w + j when bit j is set -- one coalesced store per
+        // word instead of a lane writing its own word's rows one by one
+        // (dense masks: every candidate detected); set bits are rows < n
+        const unsigned below = (1u << lane) - 1u;
+        unsigned any = __ballot_sync(0xffffffffu, bitsw != 0u);
+        while (any) {
+            const int src = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t wb = __shfl_sync(0xffffffffu, bitsw, src);
+            const int64_t p0 = __shfl_sync(0xffffffffu, pos, src);
+            const int64_t ws = __shfl_sync(0xffffffffu, w, src);
+            if ((wb >> lane) & 1u) {
+                const int64_t q = p0 + __popc(wb & below);
+                const int64_t row = ws * 32 + lane;
+                if (row < n && q < cap) idx[(int64_t)g * cap + q] = row;
             }
         }
         __syncthreads();
@@ -1282,7 +1323,7 @@ extern "C" int sfftb_compact_mask_cap(const uint32_t* mask, int64_t G, int64_t n
     compact_count<<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(mask, nwords,
                                                                                  nblk, bs);
     SFFTB_CHECK_LAUNCH();
-    compact_scan<<<(unsigned)G, 32, 0, st>>>(bs, nblk, counts, cap, totals);
+    compact_scan<<<(unsigned)G, kCompactScanThreads, 0, st>>>(bs, nblk, counts, cap, totals);
     SFFTB_CHECK_LAUNCH();
     compact_write<false><<<dim3((unsigned)nblk, (unsigned)G), kCompactThreads, 0, st>>>(
         mask, nwords, n, nblk, bs, idx, counts, cap, totals);
