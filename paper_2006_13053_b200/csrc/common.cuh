@@ -193,6 +193,12 @@ inline cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(Exp...), dim3 grid, d
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
+// medians on pair tables (hash.cu); dense: most candidates detected
+int medians_pairs_launch(const int32_t* P, const int32_t* V, int64_t n1, int64_t n2, int64_t G,
+                         int64_t L, int64_t M, const double* ghat, const int64_t* idx,
+                         const int64_t* counts, int64_t cap, double* coeffs, void* stream,
+                         bool dense);
+
 // zero-test thresholds (hash.cu) launched inside the fused transform chain
 int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,
                            cudaStream_t st, bool pdl);

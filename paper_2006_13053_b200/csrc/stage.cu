@@ -181,9 +181,10 @@ int stage_detect(const sfftb_stage_t* a, void* stream, const Marks& mark) {
         SFFTB_TRY(mark(6));
         SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
                                      stream));
-        if (pairs)
-            SFFTB_TRY(sfftb_medians_pairs(a->ptab, a->vtab, a->n1, a->n2, G, L, M, a->ghat,
-                                          a->idx, a->counts, n, a->med, stream));
+        if (pairs)  // noisy data: (nearly) every candidate detected
+            SFFTB_TRY(sfftb::medians_pairs_launch(a->ptab, a->vtab, a->n1, a->n2, G, L, M,
+                                                  a->ghat, a->idx, a->counts, n, a->med, stream,
+                                                  a->sigma > 0.0));
         else
             SFFTB_TRY(sfftb_medians(a->J, tdim, a->zmat, G, L, M, a->ghat, a->idx, a->counts,
                                     n, a->med, stream));
