@@ -199,6 +199,11 @@ int medians_pairs_launch(const int32_t* P, const int32_t* V, int64_t n1, int64_t
                          const int64_t* counts, int64_t cap, double* coeffs, void* stream,
                          bool dense);
 
+// mask compaction (hash.cu) with the single-CTA threshold in words per group
+int compact_mask_launch(const uint32_t* mask, int64_t G, int64_t n, int64_t cap, int64_t* idx,
+                        int64_t* counts, int64_t* totals, void* ws, void* stream,
+                        int64_t single_words);
+
 // zero-test thresholds (hash.cu) launched inside the fused transform chain
 int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,
                            cudaStream_t st, bool pdl);

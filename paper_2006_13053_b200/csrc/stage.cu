@@ -179,8 +179,11 @@ int stage_detect(const sfftb_stage_t* a, void* stream, const Marks& mark) {
                                       a->min_hits, nullptr, a->detmask, stream));
         }
         SFFTB_TRY(mark(6));
-        SFFTB_TRY(sfftb_compact_mask(a->detmask, G, n, a->idx, a->counts, a->ws_compact,
-                                     stream));
+        // noisy data detects (nearly) every candidate: dense masks compact
+        // faster over many blocks
+        SFFTB_TRY(sfftb::compact_mask_launch(a->detmask, G, n, n, a->idx, a->counts, nullptr,
+                                             a->ws_compact, stream,
+                                             a->sigma > 0.0 ? 1024 : 8192));
         if (pairs)  // noisy data: (nearly) every candidate detected
             SFFTB_TRY(sfftb::medians_pairs_launch(a->ptab, a->vtab, a->n1, a->n2, G, L, M,
                                                   a->ghat, a->idx, a->counts, n, a->med, stream,
