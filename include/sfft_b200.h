@@ -159,11 +159,22 @@ int sfftb_nonzero_bitmap(const double *ghat, int64_t G, int64_t L, int64_t M,
  * is fused).  kbound = sum_j max_i |elems[i, j]| when known (enables the
  * 32-bit residue path), else -1.  hits64 (G*n int64) may be NULL;
  * detmask[g*ceil(n/32) + w] bit b is set when hits of row 32w+b >= min_hits.
+ * Replaces _core.pyx:164-197 (the hit half of detect_gather).
+ *
+ * G == 1 sets of >= 2^16 rows with even d <= 16 run on the tensor cores
+ * (csrc/hash_tc.cu): residues as an exact u8 x u8 -> s32 GEMM of the raw row
+ * bytes against per-lattice coefficient limbs (tcgen05.mma kind::i8), exact
+ * for ANY int64 rows (kbound is not needed there; rows beyond the GEMM range
+ * take an exact 64-bit path inside the same kernel).
  */
 int sfftb_hash_hits(const int64_t *elems, int64_t n, int64_t d,
                     const int64_t *zmat, int64_t G, int64_t L, int64_t M,
                     const uint32_t *bits, int64_t kbound, int64_t min_hits,
                     int64_t *hits64, uint32_t *detmask, void *stream);
+
+/* Rows the tensor-core hash sent to its exact 64-bit path since the last
+ * reset (reset != 0 zeroes the counter); synchronous, for tests. */
+int64_t sfftb_hash_tc_recomputed(int reset);
 
 /*
  * Ascending indices of set bits per group: idx[g*n + k], counts[g].

@@ -204,6 +204,12 @@ int compact_mask_launch(const uint32_t* mask, int64_t G, int64_t n, int64_t cap,
                         int64_t* counts, int64_t* totals, void* ws, void* stream,
                         int64_t single_words);
 
+// candidate hashing on the tensor cores (hash_tc.cu): 1 = handled, 0 = shape
+// outside the byte-GEMM path (use the CUDA-core kernels), < 0 = -status
+int hash_hits_tc(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat, int64_t L,
+                 int64_t M, const uint32_t* bits, int64_t min_hits, int64_t* hits64,
+                 uint32_t* detmask, cudaStream_t st);
+
 // zero-test thresholds (hash.cu) launched inside the fused transform chain
 int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,
                            cudaStream_t st, bool pdl);

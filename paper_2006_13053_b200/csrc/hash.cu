@@ -1360,6 +1360,12 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     SFFTB_REQUIRE(M < (int64_t(1) << 31), "hash: M must be < 2^31");
     if (n == 0) return SFFTB_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    // tensor-core path (csrc/hash_tc.cu): exact for any int64 rows, no bound
+    if (G == 1) {
+        const int rc = hash_hits_tc(elems, n, d, zmat, L, M, bits, min_hits, hits64, detmask, st);
+        if (rc < 0) return -rc;
+        if (rc == 1) return SFFTB_OK;
+    }
     const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
     HashArgs a;
     a.elems = elems;

@@ -477,14 +477,61 @@ def gen_f10():
     save_json("f10_cases", out)
 
 
+def gen_cfg4_full():
+    """Config 4 at its stated size, run by the reference end to end.
+
+    Gamma = _random_from_box(Box(10,-4096,4096), 2^26, default_rng(2026))
+    (called directly: random_subset(Box) overflows len()),
+    then I = random_subset(Gamma, 1e4), |c| ~ U[1,10], arg c ~ U[0,2pi),
+    draw_config(Gamma, 1e4, 0.1), lattice samples, detect_and_compute.
+    About 15 min and 18 GB of RSS here, so only digests are stored: the full
+    hits array (2^26 int64) as sha256, the detections and coefficients in
+    full, the RNG state after Gamma (to pin the device generator's stream)
+    and 4096 sampled Gamma rows.  Not part of the default fixture set.
+    """
+    d, N, n, s = 10, 4096, 1 << 26, 10_000
+    rng = np.random.default_rng(2026)
+    t0 = time.perf_counter()
+    G = rfs._random_from_box(rfs.Box(d, -N, N), n, rng)
+    t_gen = time.perf_counter() - t0
+    st_after_gamma = rng.bit_generator.state
+    full_gamma = hashlib.sha256(np.ascontiguousarray(G.elems).tobytes()).hexdigest()
+    pos = np.linspace(0, n - 1, 4096).astype(np.int64)
+    I = rfs.random_subset(G, s, rng)
+    mags = rng.uniform(1, 10, s)
+    ph = rng.uniform(0, 2 * np.pi, s)
+    p = rpe.SparsePoly(I, mags * np.exp(1j * ph))
+    t0 = time.perf_counter()
+    cfg = rlat.draw_config(G, s, 0.1, rng=rng)
+    t_cfg = time.perf_counter() - t0
+    oracle = rpe.oracle_from_poly(p)
+    samples = [oracle.sample_lattice(lat) for lat in cfg.lattices]
+    t0 = time.perf_counter()
+    res = rdetect.detect_and_compute(samples, cfg, G)
+    t_det = time.perf_counter() - t0
+    hits = np.ascontiguousarray(res.hits, dtype=np.int64)
+    save_npz("cfg4_full",
+             gamma_sha256=np.array(full_gamma), gamma_rows=G.elems[pos], gamma_pos=pos,
+             rng_state_after_gamma=np.array(json.dumps(st_after_gamma)),
+             support_digest=np.array(digest(I.elems)), coeffs_true=mags * np.exp(1j * ph),
+             M=np.array(cfg.shared_M), zmat=np.vstack([lat.z for lat in cfg.lattices]),
+             samples_digest=np.array(digest(np.array(samples))),
+             hits_sha256=np.array(hashlib.sha256(hits.tobytes()).hexdigest()),
+             hits_hist=np.bincount(hits, minlength=len(cfg.lattices) + 1),
+             idx=res.detected_idx, coeffs=res.coeffs, theta0=np.array(res.theta_zero),
+             ref_seconds=np.array([t_gen, t_cfg, t_det]))
+
+
 GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
        "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
-       "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale}
+       "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale,
+       "cfg4_full": gen_cfg4_full}
+SLOW = {"cfg4_full"}
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(GEN)
+    names = sys.argv[1:] or [k for k in GEN if k not in SLOW]
     for nm in names:
         t0 = time.perf_counter()
         GEN[nm]()
