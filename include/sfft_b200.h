@@ -560,6 +560,33 @@ int sfftb_pcg64_random(uint64_t *states, int64_t rows, int64_t count,
 int sfftb_pcg64_integers(uint64_t *states, int64_t rows, int64_t low,
                          int64_t high_incl, int64_t count, int64_t *out);
 
+/* Advance one stream's PCG64 by `delta` 64-bit outputs (LCG jump-ahead).
+ * tables (may be NULL): the jump-by-2^i maps s -> A_i s + C_i, i < 64, as
+ * (A hi, A lo, C hi, C lo) -- the input of sfftb_box_integers. */
+int sfftb_pcg64_advance(uint64_t *state, uint64_t delta, uint64_t *tables);
+
+/* Generator.choice(pop, size, replace=False) in numpy's tail-shuffle regime
+ * (pop > 10000 and size > pop // 50; _generator.pyx _shuffle_int from the
+ * top of arange(pop)): out (size) the chosen indices in numpy's order, the
+ * state advanced exactly.  final_shuffle must be 0 to match numpy 2.x. */
+int sfftb_pcg64_choice_tail(uint64_t *state, int64_t pop, int64_t size,
+                            int final_shuffle, int64_t *out);
+
+/*
+ * Generator.integers(low, high_incl + 1, size=n, dtype=int64) on the DEVICE
+ * in numpy's exact stream (freqset.py:273-275; csrc/boxgen.cu), for
+ * high_incl - low < 2^32 - 1: out (device, n).  state6 (host) is the stream
+ * before the draw and is not modified; jump = sfftb_pcg64_advance tables of
+ * it.  extra = spare 32-bit words for Lemire rejections.  Synchronous: on
+ * return *words_used = 32-bit words consumed, *last_hi = the high half of the
+ * 64-bit output that held the last one (the caller rebuilds the state).
+ */
+int64_t sfftb_box_integers_workspace_bytes(int64_t n, int64_t extra);
+int sfftb_box_integers(const uint64_t *state6, const uint64_t *jump, int64_t low,
+                       int64_t high_incl, int64_t n, int64_t extra, int64_t *out,
+                       void *ws, int64_t *words_used, uint64_t *last_hi,
+                       void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,11 @@ _SIGS = {
     "sfftb_pcg64_seed": (_int, [_p, _i64, _i64, _p]),
     "sfftb_pcg64_random": (_int, [_p, _i64, _i64, _p]),
     "sfftb_pcg64_integers": (_int, [_p, _i64, _i64, _i64, _i64, _p]),
+    "sfftb_pcg64_advance": (_int, [_p, _u64, _p]),
+    "sfftb_pcg64_choice_tail": (_int, [_p, _i64, _i64, _int, _p]),
+    "sfftb_box_integers_workspace_bytes": (_i64, [_i64, _i64]),
+    "sfftb_box_integers": (_int, [_p, _p, _i64, _i64, _i64, _i64, _p, _p,
+                                  ctypes.POINTER(_i64), ctypes.POINTER(_u64), _p]),
 }
 
 _LIB = None

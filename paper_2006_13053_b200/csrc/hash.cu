@@ -19,6 +19,8 @@
 //    only for those rows, one warp per row.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sfftb {
@@ -47,6 +49,8 @@ struct HashArgs {
     int64_t nwords;
     int xsplit;          // FP64 coordinates of the 32-bit path (0: all IMAD)
     int variant;         // tuning-table entry (d = 10)
+    int64_t auto_sum;    // AUTO: rows with sum_j |k_j| <= auto_sum take the 32-bit path
+    int64_t auto_bias;   // AUTO: multiple of M >= d * M * (M/2), keeps 64-bit sums >= 0
 };
 
 // FP64/IMAD split of the 32-bit dot product (see hash_rows): opt-in only
@@ -140,7 +144,8 @@ __device__ __forceinline__ void load_bits(uint32_t* dst, const HashArgs& a, int 
 template <int D, int R, bool WIDE>
 __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int lane,
                                           int32_t (&k)[R][D], uint32_t (&ku)[WIDE ? R : 1][WIDE ? D : 1],
-                                          bool (&valid)[R]) {
+                                          bool (&valid)[R], bool* all_safe = nullptr) {
+    bool safe = true;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const int64_t i = base + q * 32 + lane;
@@ -170,6 +175,34 @@ __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int l
                 k[q][j] = (int32_t)v[j];
             }
         }
+        if (all_safe) {  // AUTO: the 32-bit path is exact for this row?
+            int64_t sum = 0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint64_t m = v[j] < 0 ? (uint64_t)0 - (uint64_t)v[j] : (uint64_t)v[j];
+                sum += m >= ((uint64_t)1 << 40) ? ((int64_t)1 << 40) : (int64_t)m;
+            }
+            safe = safe && sum <= a.auto_sum;
+        }
+    }
+    if (all_safe) *all_safe = __all_sync(0xffffffffu, safe);
+}
+
+// AUTO tiles with a row outside the 32-bit bound: the rows again, reduced mod M
+// (exact for any int64), into the same registers.
+template <int D, int R>
+__device__ __forceinline__ void load_rows_reduced(const HashArgs& a, int64_t base, int lane,
+                                                  int32_t (&k)[R][D]) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int64_t i = base + q * 32 + lane;
+        const int64_t* row = a.elems + (i < a.n ? i : 0) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            int64_t m = __ldg(row + j) % a.M;
+            if (m < 0) m += a.M;
+            k[q][j] = (int32_t)m;
+        }
     }
 }
 
@@ -187,7 +220,11 @@ __device__ __forceinline__ void load_rows(const HashArgs& a, int64_t base, int l
 // at 1.5*2^52 + offset: every partial sum is an exact integer in [2^52, 2^53)
 // whose low 32 mantissa bits are (offset + sum_{j<X} k_j z_j) mod 2^32, and
 // that word seeds the integer chain -- bit-identical to the all-IMAD sum.
-template <int D, int R, bool WIDE, int NT = kHashThreads, bool SLOT = false, int X = 0>
+// AUTO (32-bit instantiation only): no host bound on the rows; each warp
+// checks its rows (sum_j |k_j| <= auto_sum) and takes the 32-bit chain when
+// all pass, otherwise the exact 64-bit chain on rows reduced mod M.
+template <int D, int R, bool WIDE, int NT = kHashThreads, bool SLOT = false, int X = 0,
+          bool AUTO = false>
 __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     const int g = blockIdx.y;
@@ -251,7 +288,9 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
         int32_t k[R][D];
         uint32_t ku[WIDE ? R : 1][WIDE ? D : 1];
         bool valid[R];
-        load_rows<D, R, WIDE>(a, base, lane, k, ku, valid);
+        bool all_safe = true;
+        load_rows<D, R, WIDE>(a, base, lane, k, ku, valid, AUTO ? &all_safe : nullptr);
+        if (AUTO && !all_safe) load_rows_reduced<D, R>(a, base, lane, k);
         double kd[R][X > 0 ? X : 1];
 #pragma unroll
         for (int q = 0; q < R; ++q)
@@ -267,6 +306,8 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
         }
         int hits[R];
         uint32_t bacc[R];
+        auto run = [&](auto wide_tag) {
+        constexpr bool WT = decltype(wide_tag)::value;
         int nbits = 0;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -291,7 +332,12 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     uint32_t r;
-                    if (!WIDE) {
+                    if (!WIDE && WT) {  // AUTO tile with wide rows: exact signed 64-bit
+                        int64_t acc = a.auto_bias;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) acc += (int64_t)k[q][j] * (int64_t)zr[j];
+                        r = (uint32_t)mod_u64((uint64_t)acc, (uint64_t)a.M, invM);
+                    } else if (!WIDE) {
                         uint32_t u = a.offset;
                         if (X > 0) {
                             double acc = dmagic;
@@ -327,6 +373,9 @@ __global__ void __launch_bounds__(NT, 1) hash_rows(HashArgs a) {
                 ++qc;
             }
         }
+        };
+        if (AUTO && !all_safe) run(std::true_type{});
+        else run(std::false_type{});
 #pragma unroll
         for (int q = 0; q < R; ++q) hits[q] += __popc(bacc[q]);
 #pragma unroll
@@ -1277,9 +1326,9 @@ static int hash_grid_x(int64_t ntiles, int64_t G, int64_t slots) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, best));
 }
 
-template <int D, int R, bool WIDE, int NT, bool SLOT, int X>
+template <int D, int R, bool WIDE, int NT, bool SLOT, int X, bool AUTO = false>
 static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
-    auto kern = hash_rows<D, R, WIDE, NT, SLOT, X>;
+    auto kern = hash_rows<D, R, WIDE, NT, SLOT, X, AUTO>;
     SFFTB_CUDA(smem_opt_in(kern, smem));
     int per_sm = 0;
     SFFTB_CUDA(occupancy(&per_sm, kern, NT, smem));
@@ -1292,20 +1341,23 @@ static int launch_hash_s(HashArgs& a, size_t smem, cudaStream_t st) {
     return SFFTB_OK;
 }
 
-template <int D, int R, bool WIDE, int NT = kHashThreads, int X = 0>
+template <int D, int R, bool WIDE, int NT = kHashThreads, int X = 0, bool AUTO = false>
 static int launch_hash_t(HashArgs& a, size_t smem, cudaStream_t st) {
     const bool pow2 = (a.slot_words & (a.slot_words - 1)) == 0;
-    return pow2 ? launch_hash_s<D, R, WIDE, NT, true, X>(a, smem, st)
-                : launch_hash_s<D, R, WIDE, NT, false, X>(a, smem, st);
+    return pow2 ? launch_hash_s<D, R, WIDE, NT, true, X, AUTO>(a, smem, st)
+                : launch_hash_s<D, R, WIDE, NT, false, X, AUTO>(a, smem, st);
 }
 
 // 640 threads (20 warps) per SM with R rows per thread, R*D <= ~60 int32
 // registers of candidate rows: measured on B200 (cfg4 shape, 2^26 rows):
 // 512x8 4.57 ms, 768x4 4.05 ms, 640x6 4.00 ms, 256x16 4.87 ms.
-template <int D, bool WIDE>
+template <int D, bool WIDE, bool AUTO = false>
 static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
     constexpr int R = D <= 5 ? 12 : (D <= 7 ? 8 : (D <= 10 ? 6 : (D <= 15 ? 4 : 3)));
     constexpr int RW = R / 2 > 0 ? R / 2 : 1;  // the 64-bit path needs wider temporaries
+    if constexpr (AUTO) {
+        return launch_hash_t<D, R, false, 640, 0, true>(a, smem, st);
+    }
     if constexpr (D == 10 && !WIDE) {
         // opt-in FP64/IMAD split (SFFTB_HASH_VARIANT=1|2); measured slower
         // than the all-IMAD default on B200 (profiles/r01/SUMMARY.md)
@@ -1317,11 +1369,11 @@ static int launch_hash_d(HashArgs& a, size_t smem, cudaStream_t st) {
     return launch_hash_t<D, (WIDE ? RW : R), WIDE, 640>(a, smem, st);
 }
 
-template <bool WIDE>
+template <bool WIDE, bool AUTO = false>
 static int hash_dispatch(int d, HashArgs& a, size_t smem, cudaStream_t st) {
     switch (d) {
 #define SFFTB_HD(X) \
-    case X: return launch_hash_d<X, WIDE>(a, smem, st);
+    case X: return launch_hash_d<X, WIDE, AUTO>(a, smem, st);
         SFFTB_HD(1) SFFTB_HD(2) SFFTB_HD(3) SFFTB_HD(4) SFFTB_HD(5) SFFTB_HD(6) SFFTB_HD(7)
         SFFTB_HD(8) SFFTB_HD(9) SFFTB_HD(10) SFFTB_HD(11) SFFTB_HD(12) SFFTB_HD(13)
         SFFTB_HD(14) SFFTB_HD(15) SFFTB_HD(16) SFFTB_HD(17) SFFTB_HD(18) SFFTB_HD(19)
@@ -1433,6 +1485,14 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     // 64-bit path: exact while d*(M-1)^2 < 2^62 (the reference's own bound,
     // detect.py:128-129); beyond that the 128-bit generic kernel
     const bool wide_ok = (__int128)d * (M - 1) * (M - 1) < ((__int128)1 << 62);
+    if (kbound < 0 && d >= 1 && d <= 20 && wide_ok && M <= ((int64_t)1 << 30)) {
+        // no host bound: the rows themselves pick the chain, warp by warp
+        a.offset = (uint32_t)((((int64_t)1 << 31) / M) * M);
+        const int64_t room = std::min<int64_t>(a.offset, (int64_t)0xFFFFFFFF - a.offset);
+        a.auto_sum = room / std::max<int64_t>(zmax, 1);
+        a.auto_bias = d * (M / 2 + 1) * M;
+        return hash_dispatch<false, true>((int)d, a, smem, st);
+    }
     if (d >= 1 && d <= 20 && wide_ok) {
         a.offset = 0;
         return hash_dispatch<true>((int)d, a, smem, st);

@@ -23,6 +23,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <new>
+
 namespace {
 
 typedef unsigned __int128 u128;
@@ -202,6 +204,89 @@ int sfftb_pcg64_integers(uint64_t* states, int64_t rows, int64_t low, int64_t hi
         fill_int(p, low, rng, count, out + r * count);
         store(p, states + 6 * r);
     }
+    return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Candidate-set generation in the reference's stream (freqset.py:266-280:
+// integers -> _canonicalize -> Generator.choice(replace=False) -> sort).
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// bounded draw in [0, rng] as numpy's random_bounded_uint64(off=0, rng, mask,
+// use_masked=0): nothing for rng == 0, Lemire on buffered 32-bit words up to
+// 2^32 - 2, one raw 32-bit word at 2^32 - 1, Lemire on 64-bit words above.
+inline uint64_t bounded(Pcg& p, uint64_t rng) {
+    if (rng == 0) return 0;
+    if (rng < 0xFFFFFFFFull) return lemire32(p, (uint32_t)rng);
+    if (rng == 0xFFFFFFFFull) return next32(p);
+    if (rng == UINT64_MAX) return next64(p);
+    return lemire64(p, rng);
+}
+
+// Fisher-Yates of _generator.pyx's _shuffle_int: i from n-1 down to first.
+void shuffle_int(Pcg& p, int64_t n, int64_t first, int64_t* data) {
+    for (int64_t i = n - 1; i >= first; --i) {
+        const int64_t j = (int64_t)bounded(p, (uint64_t)i);
+        const int64_t t = data[j];
+        data[j] = data[i];
+        data[i] = t;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Advance a PCG64 state by `delta` 64-bit outputs (LCG jump-ahead; the
+// 32-bit buffer is untouched).  tables: if non-null, receives the 128 pairs
+// (A_i, C_i) of the jump by 2^i as 4 uint64 each (hi, lo of A, hi, lo of C).
+int sfftb_pcg64_advance(uint64_t* state, uint64_t delta, uint64_t* tables) {
+    Pcg p;
+    load(state, p);
+    u128 A = kMult, C = p.inc;  // jump by 2^i: s -> A s + C
+    u128 accA = 1, accC = 0;
+    for (int i = 0; i < 64; ++i) {
+        if (tables) {
+            tables[4 * i + 0] = (uint64_t)(A >> 64);
+            tables[4 * i + 1] = (uint64_t)A;
+            tables[4 * i + 2] = (uint64_t)(C >> 64);
+            tables[4 * i + 3] = (uint64_t)C;
+        }
+        if ((delta >> i) & 1u) {
+            accA = A * accA;
+            accC = A * accC + C;
+        }
+        C = A * C + C;
+        A = A * A;
+    }
+    p.state = accA * p.state + accC;
+    store(p, state);
+    return 0;
+}
+
+// Generator.choice(pop, size, replace=False) in numpy's tail-shuffle regime
+// (pop > 10000 and size > pop // 50): arange(pop), _shuffle_int(pop,
+// max(pop - size, 1)), keep the last `size`, and -- when final_shuffle --
+// _shuffle_int(size, 1) of those.  out (size) gets the chosen indices in
+// numpy's order; the state advances exactly as numpy's does.
+int sfftb_pcg64_choice_tail(uint64_t* state, int64_t pop, int64_t size, int final_shuffle,
+                            int64_t* out) {
+    if (pop < 0 || size < 0 || size > pop) return 1;
+    Pcg p;
+    load(state, p);
+    int64_t* data = new (std::nothrow) int64_t[pop > 0 ? pop : 1];
+    if (!data) return 2;
+    for (int64_t i = 0; i < pop; ++i) data[i] = i;
+    const int64_t first = pop - size > 1 ? pop - size : 1;
+    shuffle_int(p, pop, first, data);
+    memcpy(out, data + (pop - size), (size_t)size * sizeof(int64_t));
+    delete[] data;
+    if (final_shuffle) shuffle_int(p, size, 1, out);
+    store(p, state);
     return 0;
 }
 

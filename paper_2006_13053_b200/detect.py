@@ -175,7 +175,19 @@ def default_zero_test(samples):
 STREAM_UPLOAD_BYTES = 256 << 20
 
 
+# candidate sets at least this large hash without a host bound (-1): the hash
+# kernel checks the rows warp by warp on the device and takes the 32-bit
+# residue chain where it is exact, the 64-bit chain elsewhere (csrc/hash.cu
+# AUTO), so no host pass over the rows (a min/max over 5.4 GB at config 4)
+AUTO_BOUND_ROWS = 1 << 16
+
+
 def _kbound(gamma):
+    kb = gamma.memo_get("kbound")
+    if kb is not None:
+        return kb
+    if len(gamma) >= AUTO_BOUND_ROWS and gamma.memo_get("bounds") is None:
+        return -1
     return gamma.memo("kbound", gamma.kbound)
 
 

@@ -164,3 +164,74 @@ def grid(master, tag, ts, indices):
 def streams(master, tag, t, indices):
     """Streams for SeedSequence((master, tag, t, i)), i in indices."""
     return grid(master, tag, [t], indices)
+
+
+# ---------------------------------------------------------------------------
+# one numpy Generator's state as the 6-word layout of csrc/hostrng.cpp
+# ---------------------------------------------------------------------------
+
+def state6(g):
+    """np.uint64[6] of a numpy Generator(PCG64)."""
+    st = g.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("only PCG64 generators are restated natively")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    return np.array([s >> 64, s & 0xFFFFFFFFFFFFFFFF, inc >> 64, inc & 0xFFFFFFFFFFFFFFFF,
+                     st["has_uint32"], st["uinteger"]], dtype=np.uint64)
+
+
+def set_state6(g, st):
+    """Write a 6-word state back into the numpy Generator (numpy continues
+    exactly where the native draws stopped)."""
+    s = [int(v) for v in st]
+    g.bit_generator.state = {"bit_generator": "PCG64",
+                             "state": {"state": (s[0] << 64) | s[1],
+                                       "inc": (s[2] << 64) | s[3]},
+                             "has_uint32": s[4], "uinteger": s[5]}
+
+
+def advance(st, delta):
+    """Advance st (6 words, in place) by delta 64-bit outputs."""
+    _native.check(_native.lib().sfftb_pcg64_advance(_ptr(st), int(delta), None), "pcg64_advance")
+
+
+def jump_tables(st):
+    """(256,) uint64: the jump-by-2^i maps of st's LCG (sfftb_box_integers)."""
+    tab = np.zeros(256, dtype=np.uint64)
+    tmp = st.copy()
+    _native.check(_native.lib().sfftb_pcg64_advance(_ptr(tmp), 0, _ptr(tab)), "pcg64_advance")
+    return tab
+
+
+def after_words(st, words_used, last_hi):
+    """The state after `words_used` buffered 32-bit words were drawn from st
+    (numpy's next_uint32 buffering); last_hi = the high half of the 64-bit
+    output holding the last word."""
+    out = st.copy()
+    j = int(words_used)
+    if j <= 0:
+        return out
+    if out[4]:
+        out[4] = 0  # the buffered high half went first
+        j -= 1
+        if j == 0:
+            return out
+    advance(out, (j + 1) // 2)
+    out[4] = j & 1
+    out[5] = int(last_hi)
+    return out
+
+
+def choice_no_replace(g, pop, size):
+    """Generator.choice(pop, size, replace=False) with g advanced exactly as
+    numpy advances it: numpy's tail-shuffle regime (pop > 10000 and
+    size > pop // 50) natively (csrc/hostrng.cpp), Floyd's regime by numpy."""
+    pop, size = int(pop), int(size)
+    if not (pop > 10000 and size > pop // 50):
+        return g.choice(pop, size=size, replace=False)
+    st = state6(g)
+    out = np.empty(size, dtype=np.int64)
+    _native.check(_native.lib().sfftb_pcg64_choice_tail(_ptr(st), pop, size, 0, _ptr(out)),
+                  "pcg64_choice_tail")
+    set_state6(g, st)
+    return out

@@ -72,3 +72,45 @@ def test_config4_shape_vs_oracle(cuda, oracle_lib):
     assert np.max(np.abs(res.coeffs - co)) <= 1e-10 * np.max(np.abs(co))
     fr = pkg.detect_frequencies(smp, cfg, G)
     assert np.array_equal(fr.detected_idx, idx)
+
+
+def test_config4_full_size_vs_reference_golden(cuda, oracle_lib):
+    """Config 4 at its stated size against the REFERENCE run end to end
+    (tests/golden/make_golden.py gen_cfg4_full, ~11 min of the reference):
+    Gamma (2^26 rows of [-4096,4096]^10, default_rng(2026)) born on the device
+    in the reference's stream; support, coefficients and lattices drawn from
+    the same generator; all 2^26 hit counts bit-identical (sha256), detected
+    indices identical, coefficients within 1e-10."""
+    import hashlib
+    import json
+
+    from conftest import golden
+
+    pkg, port = cuda, oracle_lib
+    g = golden("cfg4_full.npz")
+    d, N, n, s = 10, 4096, 1 << 26, 10_000
+    rng = np.random.default_rng(2026)
+    G = pkg.random_box_device(pkg.Box(d, -N, N), n, rng)
+    assert rng.bit_generator.state == json.loads(str(g["rng_state_after_gamma"]))
+    elems = G.elems
+    assert np.array_equal(elems[g["gamma_pos"]], g["gamma_rows"])
+    assert hashlib.sha256(elems.tobytes()).hexdigest() == str(g["gamma_sha256"])
+    I = pkg.random_subset(G, s, rng)
+    assert hashlib.sha256(np.ascontiguousarray(I.elems).tobytes()).hexdigest()[:16] == \
+        str(g["support_digest"])
+    coeffs = rng.uniform(1, 10, s) * np.exp(1j * rng.uniform(0, 2 * np.pi, s))
+    assert np.array_equal(coeffs, g["coeffs_true"])
+    cfg = pkg.draw_config(G, s, 0.1, rng=rng)
+    assert cfg.shared_M == int(g["M"]) and np.array_equal(cfg.zmat(), g["zmat"])
+    # the reference's lattice samples (bincount + ifft, polyeval.py:78-87)
+    samples = [port.sample_lattice_structured(I.elems, coeffs, cfg.zmat()[l], cfg.shared_M)
+               for l in range(cfg.L)]
+    assert hashlib.sha256(np.ascontiguousarray(np.array(samples)).tobytes()).hexdigest()[:16] \
+        == str(g["samples_digest"])
+    res = pkg.detect_and_compute(samples, cfg, G)
+    assert hashlib.sha256(np.ascontiguousarray(res.hits, dtype=np.int64).tobytes()
+                          ).hexdigest() == str(g["hits_sha256"])
+    assert np.array_equal(res.detected_idx, g["idx"])
+    co = g["coeffs"]
+    assert np.max(np.abs(res.coeffs - co)) <= 1e-10 * np.max(np.abs(co))
+    assert res.theta_zero == pytest.approx(float(g["theta0"]), rel=1e-14)

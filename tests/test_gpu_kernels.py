@@ -255,17 +255,30 @@ def test_device_canonicalisation_matches_host(cuda, case):
     assert len(S) == got.shape[0]
 
 
-def test_random_box_device(cuda):
+@pytest.mark.parametrize("d,lo,hi,count", [
+    (3, -2, 2, 100),            # 125 points: duplicates, top-up rounds, Floyd choice
+    (10, -4096, 4096, 1 << 16),  # config-4 box: one round, native tail shuffle
+    (4, -40, 40, 40_000),        # duplicates AND the tail-shuffle regime
+    (2, -(1 << 40), 1 << 40, 5000),  # range beyond 32-bit words: numpy's own draw
+    (5, 0, 0, 1),                # a one-point box
+])
+def test_random_box_device_is_the_reference_stream(cuda, d, lo, hi, count):
+    """Device-born Gamma == _random_from_box (freqset.py:266-280) row for row,
+    and the generator is left in numpy's exact state (later draws agree)."""
+    import workloads
+
     pkg = cuda
-    box = pkg.Box(3, -2, 2)  # 125 points: forces re-draws and a random drop
-    S = pkg.random_box_device(box, 100, seed=5)
-    e = S.elems
-    assert e.shape == (100, 3) and np.all(e >= -2) and np.all(e <= 2)
-    assert np.array_equal(e, np.unique(e, axis=0))
-    big = pkg.random_box_device(pkg.Box(10, -4096, 4096), 1 << 16, seed=9)
-    assert len(big) == 1 << 16
-    b = big.elems
-    assert np.array_equal(b, np.unique(b, axis=0)) and b.min() >= -4096 and b.max() <= 4096
+    g1 = np.random.default_rng(d * 1000 + count)
+    g1.random(3)  # leave a buffered 32-bit word half the time
+    g1.integers(0, 7)
+    g2 = np.random.default_rng(d * 1000 + count)
+    g2.random(3)
+    g2.integers(0, 7)
+    want = workloads.rows_from_box(d, lo, hi, count, g1)
+    got = pkg.random_box_device(pkg.Box(d, lo, hi), count, g2)
+    assert np.array_equal(got.elems, want)
+    assert g1.bit_generator.state == g2.bit_generator.state
+    assert np.array_equal(g1.integers(0, 1 << 40, size=9), g2.integers(0, 1 << 40, size=9))
 
 
 @pytest.mark.parametrize("L", [1, 7, 31, 33, 47, 63, 65])
@@ -400,3 +413,33 @@ def test_eval_lines_matches_dense_nodes(cuda):
     _native.call("sfftb_eval_lines", _dev.ptr(sup_d), s, d, _dev.ptr(c_d), _dev.ptr(b_d),
                  d * r, K, r, _dev.ptr(got), _dev.stream())
     assert np.array_equal(_dev.download(got), _dev.download(want))
+
+
+def test_hash_without_host_bound_mixed_rows(cuda, oracle_lib):
+    """A large host FreqSet with no memoised bound: the hash picks the 32-bit
+    or the exact 64-bit residue chain per warp from the rows themselves
+    (kbound = -1, csrc/hash.cu AUTO); a few huge coordinates force the wide
+    chain on their warps only.  Bit-exact against the C oracle."""
+    import torch
+
+    import paper_2006_13053_b200 as pkg
+    from paper_2006_13053_b200 import _dev, _engine
+
+    rng = np.random.default_rng(11)
+    n, d, M, L = 300_000, 10, 103307, 47
+    rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+    wide = rng.choice(n, size=50, replace=False)
+    rows[wide, 3] = rng.integers(-(1 << 62), 1 << 62, size=50)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    gh = rng.normal(size=(L, M)) + 1j * rng.normal(size=(L, M))
+    gh[rng.random(size=(L, M)) < 0.9] = 0.0
+    samples = _dev.upload(np.fft.ifft(gh, axis=1) * M)
+    G = pkg.FreqSet(d, rows)  # canonical order, no bound memoised
+    assert pkg.detect._kbound(G) == -1
+    srt = G.elems
+    b = _engine.detect_batch(samples, M, _dev.upload(z), 1, L, G.device(), -1, 0.5,
+                             theta0=torch.full((1,), 1e-9, dtype=torch.float64,
+                                               device="cuda"), want_hits=True)
+    ghat = _dev.download(b.ghat)
+    want_h, _ = oracle_lib.gather_c(srt % M, z, M, ghat, 1e-9, L / 2, True)
+    assert np.array_equal(_dev.download(b.hits), want_h)
