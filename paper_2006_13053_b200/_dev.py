@@ -7,6 +7,8 @@ the Python side.
 
 from __future__ import annotations
 
+import os
+import threading
 import warnings
 
 import numpy as np
@@ -14,18 +16,20 @@ import torch
 
 from . import _native
 
-import os
-
 _PINNED_SMALL = os.environ.get("SFFTB_PINNED_SMALL", "1") == "1"
 _CHECKED = False
-_SCOPE = None  # (device, stream handle) pinned by stream_scope()
+# (device, stream handle) pinned by stream_scope(), per calling thread: the
+# reference's kernels are reentrant and called from worker threads
+# (analysis.py:271-274), so each thread keeps its own current stream.
+_TLS = threading.local()
 
 
 def device():
     """The CUDA device; raises if there is none (no CPU fallback exists)."""
     global _CHECKED
-    if _SCOPE is not None:
-        return _SCOPE[0]
+    sc = getattr(_TLS, "scope", None)
+    if sc is not None:
+        return sc[0]
     if not _CHECKED:
         if not torch.cuda.is_available():
             raise RuntimeError(
@@ -38,8 +42,9 @@ def device():
 
 def stream():
     """cudaStream_t of the current torch stream, as an int for ctypes."""
-    if _SCOPE is not None:
-        return _SCOPE[1]
+    sc = getattr(_TLS, "scope", None)
+    if sc is not None:
+        return sc[1]
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -48,16 +53,14 @@ class stream_scope:
     (saves a torch query per launch on the driver's hot loop)."""
 
     def __enter__(self):
-        global _SCOPE
-        self._prev = _SCOPE
-        if _SCOPE is None:
+        self._prev = getattr(_TLS, "scope", None)
+        if self._prev is None:
             dev = device()
-            _SCOPE = (dev, torch.cuda.current_stream(dev).cuda_stream)
+            _TLS.scope = (dev, torch.cuda.current_stream(dev).cuda_stream)
         return self
 
     def __exit__(self, *exc):
-        global _SCOPE
-        _SCOPE = self._prev
+        _TLS.scope = self._prev
         return False
 
 

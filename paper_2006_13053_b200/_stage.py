@@ -119,6 +119,17 @@ def arena():
 
 
 def release():
+    """Drop the thread's arena.  Work an early return left queued (spectra
+    of the next stage on the side / sampler streams, detection on det_stream)
+    may still write into its buffers, which were allocated on the caller's
+    stream: drain every stream of this thread before the caching allocator
+    can hand that memory out again."""
+    if getattr(_LOCAL, "arena", None) is not None:
+        torch.cuda.current_stream().synchronize()
+        for kind in ("side", "samp", "det"):
+            st = (getattr(_LOCAL, kind, None) or {}).get(torch.cuda.current_device())
+            if st is not None:
+                st.synchronize()
     _LOCAL.arena = None
 
 
