@@ -11,16 +11,23 @@ B200 arm, one JSON line on rank 0:
                polynomial already in HBM; lower is better.
   * e2e     -- the same through the public API from host arrays: upload of
                the polynomial, sfft(), support/coefficients back on the host.
-  * hashing -- config 4: |Gamma| = 2^26 candidates in [-4096,4096]^10 (HBM
-               resident), s=1e4, L=47, M=103307: candidates hashed per
-               second by the hashing kernel and by the whole detection call,
-               with its roofline; plus an e2e through detect_and_compute from
-               pinned host rows.
+  * hashing -- config 4: |Gamma| = 2^26 candidates in [-4096,4096]^10, the
+               reference's seeded Gamma (generated in HBM in its RNG stream),
+               s=1e4, L=47, M=103307: candidates hashed per second by the
+               hashing kernel and by the whole detection call, every hit
+               count checked against the reference's own run
+               (tests/golden/cfg4_full.npz); e2e through detect_and_compute
+               from a plain host FreqSet over pinned rows.  With N > 1 ranks
+               one Gamma is sharded (shard.detect_and_compute_sharded).
   * roofline -- the hashing kernel vs measured HBM bandwidth (the metric's
                "vs HBM roofline"); roofline_sfft -- the dominant kernel of
                the reconstruction step.
-  * cpu_baseline -- the CPU oracle / the reference's compiled kernel on this
-               host's cores over a bounded sample, scaled to the unit.
+  * configs -- SURVEY 8(d)'s rows for configs 1, 2, 3, 5: entry-point time,
+               phase breakdown, dominant kernel vs roofline, same-run CPU.
+  * cpu_baseline -- the algorithm-matched CPU reference (the reference's
+               driver, structured sampler, pocketfft and compiled gather on
+               all host threads) run to completion and timed; the as-shipped
+               dense run beside it, bounded and flagged as extrapolated.
 Timing: CUDA events on the launching (current torch) stream, W untimed
 warm-up steps, L2 flushed (256 MB write) between timed steps, max over
 ranks; nvidia-smi clocks sampled during the timed region.
@@ -170,6 +177,35 @@ def predicted_sample_count(w):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+def sfft_profile(step, flush=None):
+    """One instrumented reconstruction: device time per entry point and per
+    stage phase ('stage:<phase>', CUDA events on the launch streams), plus
+    the (G, L, M, fused) shape of every stage call that runs transforms."""
+    import torch
+
+    from paper_2006_13053_b200 import _native, _stage
+
+    shapes = []
+    orig_run = _stage.run
+
+    def run_rec(desc, stream=None):
+        if desc.phase in (0, 1, 4):  # the calls that run transforms
+            shapes.append((desc.G, desc.L, desc.M, bool(desc.fused)))
+        return orig_run(desc, stream)
+
+    if flush is not None:
+        flush_l2(flush)
+    torch.cuda.synchronize()
+    _stage.run = run_rec
+    try:
+        with _native.Timeline() as tl:
+            step()
+        raw = tl.ms()
+    finally:
+        _stage.run = orig_run
+    return {k: (sum(v), len(v)) for k, v in raw.items()}, raw, shapes
+
+
 def run_sfft_arm(args, world, rank):
     import torch
 
@@ -213,29 +249,7 @@ def run_sfft_arm(args, world, rank):
               "sample_count_predicted": predicted_sample_count(w),
               "stages": len(res.stage_log)}
 
-    # per-entry-point / per-stage-phase device times of one instrumented step
-    # (dominant kernel), with the shapes of every stage call
-    from paper_2006_13053_b200 import _stage
-
-    shapes = []
-    orig_run = _stage.run
-
-    def run_rec(desc, stream=None):
-        if desc.phase in (0, 1, 4):  # the calls that run transforms
-            shapes.append((desc.G, desc.L, desc.M, bool(desc.fused)))
-        return orig_run(desc, stream)
-
-    flush_l2(flush)
-    torch.cuda.synchronize()
-    _stage.run = run_rec
-    try:
-        with _native.Timeline() as tl:
-            step()
-        raw = tl.ms()
-    finally:
-        _stage.run = orig_run
-    per = {k: (sum(v), len(v)) for k, v in raw.items()}
-    per_list = {k: v for k, v in raw.items()}
+    per, per_list, shapes = sfft_profile(step, flush)
 
     # e2e: host arrays in, host results out, through the public API
     e2e_times = []
@@ -261,55 +275,76 @@ def run_sfft_arm(args, world, rank):
             "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "workload": w}
 
 
-def device_gamma(n, d, N, seed):
-    """2^26-scale candidate set generated in HBM by the package's own
-    kernels: uniform rows of [-N, N]^d (Philox stream), canonicalised
-    (lexicographic radix sort + de-dup, csrc/canon.cu).  Returns (FreqSet,
-    generation ms)."""
+CFG4_SEED = 2026  # tests/golden/cfg4_full.npz: the reference's own run at this seed
+
+
+def cfg4_instance(n, d, N, s, seed):
+    """Config 4 as the reference builds it: Gamma = 2^26
+    distinct rows of [-N, N]^d in the reference's default_rng(seed) stream,
+    born in HBM (csrc/boxgen.cu + canon.cu: identical rows to
+    freqset._random_from_box, freqset.py:266-280); support = random_subset
+    of Gamma, |c| ~ U[1,10] e^{i U[0,2pi)}, draw_config(Gamma, s, 0.1) --
+    every draw from the same generator, in the reference's order.
+    Returns (G, support FreqSet, coeffs, config, generation ms)."""
     import torch
 
     import paper_2006_13053_b200 as pkg
 
+    rng = np.random.default_rng(seed)
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
-    G = pkg.random_box_device(pkg.Box(d, -N, N), n, seed)
+    G = pkg.random_box_device(pkg.Box(d, -N, N), n, rng)
     b.record()
     torch.cuda.synchronize()
-    return G, a.elapsed_time(b)
+    gen_ms = a.elapsed_time(b)
+    pick = np.sort(rng.choice(len(G), size=s, replace=False))  # random_subset's draw
+    I = G.take(torch.as_tensor(pick, device="cuda"))
+    coeffs = rng.uniform(1, 10, s) * np.exp(1j * rng.uniform(0, 2 * np.pi, s))
+    cfg = pkg.draw_config(G, s, 0.1, rng=rng)
+    return G, I, pick, coeffs, cfg, gen_ms
 
 
 def run_hash_arm(args, world, rank):
+    """Config 4: fixed-Gamma detection of 2^26 HBM-resident candidates.
+    N = 1: detect_and_compute on all rows.  N > 1: one Gamma sharded across
+    the ranks (strong scaling): shard.detect_and_compute_sharded -- lattice-
+    sharded DFTs, bitmap + spectra all-gathers over NCCL, row-sharded
+    hashing, merged detections."""
+    import hashlib
+
     import torch
 
     import paper_2006_13053_b200 as pkg
-    from oracle import port
     from paper_2006_13053_b200 import _dev, _native
+    from paper_2006_13053_b200.shard import detect_and_compute_sharded, shard_bounds
 
     n, d, N, s = args.hash_rows, 10, 4096, 10_000
-    G, gen_ms = device_gamma(n, d, N, 4242 + rank)
-    rows = G.device()
-    G.memo("bounds", lambda: np.array([[-N, N]] * d, dtype=np.int64))  # known by construction
-    rng = np.random.default_rng(2026 + rank)
-    sup_idx = np.sort(rng.choice(n, size=s, replace=False))
-    coeffs = workloads.mag_phase_coeffs(s, rng)
-    I = G.take(sup_idx)
-    poly = pkg.SparsePoly(I, coeffs)
-    cfg = pkg.draw_config(G, s, 0.1, rng=rng)
+    G, I, pick, coeffs, cfg, gen_ms = cfg4_instance(n, d, N, s, CFG4_SEED)
     M, L = cfg.shared_M, cfg.L
-    orc = pkg.oracle_from_poly(poly)
+    orc = pkg.oracle_from_poly(pkg.SparsePoly(I, coeffs))
     samples = orc.sample_lattices_device(cfg.zmat_device(), M,
                                          torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
-                                         1, L, d)
-    samples = samples.contiguous()
+                                         1, L, d).contiguous()
+    rows_all = G.device()
+    lo, hi = shard_bounds(n, world, rank)
+    if world > 1:
+        Gs = pkg.FreqSet.from_device(d, rows_all[lo:hi].contiguous())
+        zero = pkg.default_zero_test(samples)
 
-    def step():
-        return pkg.detect_and_compute(samples, cfg, G)
+        def step():
+            gidx, gco, res = detect_and_compute_sharded(samples, cfg, Gs, lo, zero=zero)
+            return gidx, gco, res
+    else:
+        Gs = G
+
+        def step():
+            res = pkg.detect_and_compute(samples, cfg, G)
+            return res.detected_idx, res.coeffs, res
 
     for _ in range(args.warmup):
-        res = step()
-        res.detected_idx  # noqa: B018
+        step()
     torch.cuda.synchronize()
     times, hash_ms, path_ms = [], [], []
     with ClockSampler(torch.cuda.current_device()) as clk:
@@ -320,7 +355,7 @@ def run_hash_arm(args, world, rank):
             b = torch.cuda.Event(enable_timing=True)
             with _native.Timeline() as tl:
                 a.record()
-                res = step()
+                idx, co, res = step()
                 b.record()
             per = tl.ms()
             times.append(a.elapsed_time(b))
@@ -329,52 +364,92 @@ def run_hash_arm(args, world, rank):
                 "sfftb_nonzero_bitmap", "sfftb_hash_hits", "sfftb_compact_mask",
                 "sfftb_medians")))
     clocks = clk.summary()
-    idx = res.detected_idx
-    parity = {"detected_equals_support": bool(np.array_equal(idx, sup_idx)),
-              "coeff_max_rel_err_vs_truth": float(np.max(np.abs(res.coeffs - coeffs))
+    parity = {"detected_equals_support": bool(np.array_equal(idx, pick)),
+              "coeff_max_rel_err_vs_truth": float(np.max(np.abs(co - coeffs))
                                                   / np.max(np.abs(coeffs)))}
-    # bit-exact hits on a random sample of rows against the C oracle
-    samp = np.sort(rng.choice(n, size=1 << 16, replace=False))
-    samp_t = torch.as_tensor(samp, device="cuda")
-    rows_h = _dev.download(rows.index_select(0, samp_t))
-    b = pkg.detect._gather(samples, cfg, G, pkg.ZeroTest(res.theta_zero), False)
-    ghat = _dev.download(b.ghat)
-    want, _ = port.gather_c(rows_h % M, cfg.zmat(), M, ghat, res.theta_zero, L / 2, False)
-    got = _dev.download(b.hits)[samp]
-    parity["sampled_hits_bitexact_vs_oracle"] = bool(np.array_equal(got, want))
-    parity["sampled_rows"] = int(samp.size)
-    del b
+    # the reference's own run of this instance (tests/golden/make_golden.py
+    # gen_cfg4_full): every row's hit count (sha256 over all 2^26), the
+    # detected indices and coefficients
+    gold = None
+    try:
+        gold = np.load(os.path.join(ROOT, "tests", "golden", "cfg4_full.npz"))
+    except OSError:
+        pass
+    if gold is not None and n == 1 << 26 and world == 1:
+        hits = res.hits
+        parity["hits_bitexact_all_rows"] = (
+            hashlib.sha256(np.ascontiguousarray(hits, dtype=np.int64).tobytes()).hexdigest()
+            == str(gold["hits_sha256"]))
+        parity["hits_rows_compared"] = int(hits.size)
+        parity["detected_idx_equals_reference"] = bool(np.array_equal(idx, gold["idx"]))
+        parity["coeff_max_rel_err_vs_reference"] = float(
+            np.max(np.abs(co - gold["coeffs"])) / np.max(np.abs(gold["coeffs"])))
+        parity["gamma_equals_reference"] = bool(np.array_equal(
+            _dev.download(rows_all[torch.as_tensor(gold["gamma_pos"], device="cuda")]),
+            gold["gamma_rows"]))
+        parity["reference"] = "tests/golden/cfg4_full.npz (the reference's own run, seed 2026)"
+        del hits
+    elif world > 1 and rank == 0:
+        parity["sharded"] = f"{world} ranks, merged detections"
 
-    # e2e: pinned host rows -> detect_and_compute (H2D inside) -> results to host
-    host = torch.empty((n, d), dtype=torch.int64, pin_memory=True)
-    host.copy_(rows)
+    # CPU sample for the reference's gather, and the spectra it reads
+    from paper_2006_13053_b200 import _engine
+
+    ghat, theta0, _ = _engine.spectra(samples, M, 1, L,
+                                      torch.full((1,), res.theta_zero, dtype=torch.float64,
+                                                 device="cuda"))
+    ghat_h = _dev.download(ghat)
+    rows_h = _dev.download(rows_all[:1 << 20])
+    del ghat
+
+    # e2e: a plain host FreqSet from pinned rows (no bounds, no memo) through
+    # detect_and_compute: chunked H2D overlapped with hashing, results to host
+    host = torch.empty((hi - lo, d), dtype=torch.int64, pin_memory=True)
+    host.copy_(rows_all[lo:hi])
     hnp = host.numpy()
     e2e = []
     d2h = 0
     nrep = max(1, min(args.steps, 3))
     for rep in range(nrep + 1):  # rep 0 warms the pinned result buffers (untimed)
+        barrier(world)
         torch.cuda.synchronize()
         Gh = pkg.FreqSet(d, hnp, _sorted=True)
-        Gh.memo("bounds", lambda: np.array([[-N, N]] * d, dtype=np.int64))
         a = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         a.record()
-        r2 = pkg.detect_and_compute(samples, cfg, Gh)
-        out = (r2.hits, r2.detected_idx, r2.coeffs)
+        if world > 1:
+            gi, gc, r2 = detect_and_compute_sharded(samples, cfg, Gh, lo)
+            out = (r2.hits, gi, gc)
+        else:
+            r2 = pkg.detect_and_compute(samples, cfg, Gh)
+            out = (r2.hits, r2.detected_idx, r2.coeffs)
         e.record()
         torch.cuda.synchronize()
         if rep:
             e2e.append(a.elapsed_time(e))
         d2h = sum(x.nbytes for x in out)
         del Gh, r2, out
+    # the same H2D alone (pinned, one stream): the PCIe floor of the e2e
+    dst = torch.empty((hi - lo, d), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    a.record()
+    dst.copy_(host, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    h2d_ms = a.elapsed_time(e)
+    del dst, host
     W = int(_native.lib().sfftb_bitmap_words(M))
-    return {"n": n, "d": d, "L": L, "M": M, "s": s, "W": W, "n_det": int(idx.size),
+    return {"n": n, "n_local": hi - lo, "d": d, "L": L, "M": M, "s": s, "W": W,
+            "n_det": int(idx.size),
             "ms": max_over_ranks(statistics.mean(times), world),
             "hash_ms": max_over_ranks(statistics.mean(hash_ms), world),
             "path_ms": max_over_ranks(statistics.mean(path_ms), world),
             "clocks": clocks, "parity": parity, "gamma_generation_ms": gen_ms,
-            "e2e_ms": max_over_ranks(statistics.mean(e2e), world), "h2d": n * d * 8,
-            "d2h": d2h, "rows_host_sample": rows_h[:1 << 20], "ghat": ghat,
+            "e2e_ms": max_over_ranks(statistics.mean(e2e), world),
+            "h2d_ms": max_over_ranks(h2d_ms, world), "h2d": (hi - lo) * d * 8,
+            "d2h": d2h, "rows_host_sample": rows_h, "ghat": ghat_h,
             "zmat": cfg.zmat(), "theta0": res.theta_zero}
 
 
@@ -404,9 +479,29 @@ class _BudgetExceeded(Exception):
     pass
 
 
-def cpu_sfft_bounded(w, budget_s, workers):
-    """The oracle's sfft (dense sampling, as the reference ships it) run for
-    `budget_s` seconds, extrapolated by sample count to the full run."""
+def cpu_sfft_structured(w, workers):
+    """The algorithm-matched CPU reference, run to completion and timed: the
+    reference's sfft driver (dimincr.py:195-256, restated in oracle/port.py)
+    with the reference's own structured lattice sampler (bincount + numpy
+    ifft, polyeval.py:78-87) and numpy's pocketfft for every detection DFT
+    (dft.py:27), the reference's compiled detect_gather (oracle/_ref, built
+    from _core.pyx) for the hashing; lattices sampled and transformed on
+    `workers` threads.  Returns (seconds, samples, support size)."""
+    from oracle import port
+
+    orc = port.PolyOracle(w.support, w.coeffs, mode="structured", sigma=w.sigma,
+                          noise_seed=w.noise_seed)
+    t0 = time.perf_counter()
+    res = port.sfft(orc, port.Box(w.d, w.lo, w.hi), w.s, w.delta, w.seed, theta=w.theta,
+                    r=w.r, gather_backend="reference" if _ref_core() else "port",
+                    workers=workers)
+    return time.perf_counter() - t0, int(res[2]), int(len(res[0]))
+
+
+def cpu_sfft_dense_bounded(w, budget_s, workers):
+    """The reference as shipped (dense evaluate_many sampling, polyeval.py:
+    66-75, threaded over `workers` cores) for `budget_s` seconds, then
+    EXTRAPOLATED by sample count to the full run (a full run is ~8 min)."""
     from oracle import port
 
     dense = _ThreadedDense(workers)
@@ -431,8 +526,10 @@ def cpu_sfft_bounded(w, budget_s, workers):
     elapsed = time.perf_counter() - t0
     total = predicted_sample_count(w)
     est = elapsed if finished else elapsed * total / max(orc.count, 1)
-    return est, {"samples_done": int(orc.count), "samples_total": total,
-                 "elapsed_s": elapsed, "finished": finished}
+    return {"value": round(est, 3), "unit": "s", "extrapolated": not finished,
+            "fraction_run": round(orc.count / total, 5), "samples_done": int(orc.count),
+            "samples_total": total, "elapsed_s": round(elapsed, 2), "cores": workers,
+            "what": "reference sfft as shipped: dense evaluate_many sampling"}
 
 
 def _ref_core():
@@ -506,7 +603,7 @@ def _imad_bound(h):
     pk = _pipe_peaks()
     if not pk:
         return {}
-    pairs = h["n"] * h["L"]
+    pairs = h.get("n_local", h["n"]) * h["L"]
     floor_ms = pairs * 12 / (pk["imad_lanes_per_clk_per_sm"] * pk["sms"]
                              * pk["clock_mhz"] * 1e6) * 1e3
     return {"int_pipe": {"imad_per_pair": 12, "floor_ms": round(floor_ms, 3),
@@ -520,7 +617,8 @@ def _imad_bound(h):
 def roofline_hash(h, peak, src):
     """Algorithmic bytes of one hashing launch: rows (n*8d) + int64 hits
     (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8)."""
-    bytes_ = h["n"] * 8 * h["d"] + h["n"] * 8 + h["L"] * h["W"] * 4 + h["n"] // 8
+    n = h.get("n_local", h["n"])  # this rank's rows (all rows at N = 1)
+    bytes_ = n * 8 * h["d"] + n * 8 + h["L"] * h["W"] * 4 + n // 8
     ach = bytes_ / (h["hash_ms"] * 1e-3) / 1e9
     tr = measured_traffic("hash_rows")
     traffic = None
@@ -597,6 +695,11 @@ def roofline_sfft(r, peak, src):
     return out
 
 
+WORKLOAD = ("d10_s1000: sfft over [-32,32]^10, s=1000 random frequencies, |c|~U[1,10], r=5, "
+            "theta=1e-12, delta=0.9, polynomial seed 2006, sfft seed 7 (BASELINE config-2 "
+            "generator at the metric's s=1000)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -604,11 +707,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--hash-rows", type=int, default=1 << 26)
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0,
+                    help="seconds of the dense as-shipped CPU run before extrapolating")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
-                    help="skip the per-config entry-point times (configs 1, 2, 3, 5)")
+                    help="skip the per-config measurements (configs 1, 2, 3, 5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local = dist_env()
@@ -632,9 +736,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "d10_s1000: sfft over [-32,32]^10, s=1000 random frequencies, "
-                               "|c|~U[1,10], r=5, theta=1e-12, delta=0.9, seed 7 "
-                               "(BASELINE config-2 generator at the metric's s=1000)",
+        "config": {"workload": WORKLOAD,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": "flushed (256 MB write) between timed steps",
                    "value_semantics": "seconds per reconstruction (replicas: step time / N)"},
@@ -650,37 +752,49 @@ def main():
         out["roofline"] = rl
         out["hashing"] = {
             "workload": f"cfg4: |Gamma|=2^{int(math.log2(h['n']))} rows of [-4096,4096]^10 in "
-                        f"HBM, s=1e4, L={h['L']}, M={h['M']}",
-            "value": round(world * h["n"] / (h["hash_ms"] * 1e-3), 1), "unit": "candidates/s",
-            "value_semantics": "all ranks' candidates (one 2^26 set per rank) / max kernel time",
+                        f"HBM (the reference's default_rng({CFG4_SEED}) stream), s=1e4, "
+                        f"L={h['L']}, M={h['M']}",
+            "value": round(h["n"] / (h["hash_ms"] * 1e-3), 1), "unit": "candidates/s",
+            "value_semantics": ("one Gamma sharded over the ranks (strong scaling): all "
+                                "candidates / max over ranks of the hashing kernel time")
+            if world > 1 else "candidates / hashing kernel time",
             "hash_kernel_ms": round(h["hash_ms"], 4),
             "detect_and_compute_ms": round(h["ms"], 3),
             "detect_candidates_per_s": round(h["n"] / (h["ms"] * 1e-3), 1),
             "gather_path_ms": round(h["path_ms"], 4),
             "gather_path_gbs_survey_bytes": round(
-                (h["n"] * 8 * h["d"] + h["n"] * 8 + h["L"] * h["M"] * 16 + h["n_det"] * 24)
-                / (h["path_ms"] * 1e-3) / 1e9, 1),
+                (h["n_local"] * 8 * h["d"] + h["n_local"] * 8 + h["L"] * h["M"] * 16
+                 + h["n_det"] * 24) / (h["path_ms"] * 1e-3) / 1e9, 1),
             "parity": h["parity"], "clocks": h["clocks"],
             "gamma_generation_ms": round(h["gamma_generation_ms"], 2),
-            "gamma_generation_note": "device Philox rows + canonicalisation (csrc/canon.cu); "
-                                     "reference host Gamma generation 432.6 s (SURVEY 8(d))",
-            "e2e": {"value": round(world * h["n"] / (h["e2e_ms"] * 1e-3), 1),
+            "gamma_generation_note": "device generation in the reference's PCG64 stream "
+                                     "(csrc/boxgen.cu) + canonicalisation (csrc/canon.cu); "
+                                     "reference host generation 432.6 s (SURVEY 8(d))",
+            "e2e": {"value": round(h["n"] / (h["e2e_ms"] * 1e-3), 1),
                     "unit": "candidates/s",
                     "ms": round(h["e2e_ms"], 2), "h2d_bytes_per_step": h["h2d"],
-                    "d2h_bytes_per_step": h["d2h"]},
+                    "d2h_bytes_per_step": h["d2h"],
+                    "h2d_alone_ms": round(h["h2d_ms"], 2),
+                    "e2e_over_h2d": round(h["e2e_ms"] / h["h2d_ms"], 3),
+                    "input": "plain host FreqSet over pinned rows (no bounds, no memo)"},
         }
     if rank == 0 and world == 1 and not args.no_configs:
-        out["other_configs"] = all_configs()
+        out["configs"] = all_configs(peak, src, workers, cpu=not args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
-        est, info = cpu_sfft_bounded(r["workload"], args.cpu_budget, workers)
+        w = r["workload"]
+        secs, samples, nsup = cpu_sfft_structured(w, workers)
+        dense = cpu_sfft_dense_bounded(w, args.cpu_budget, workers)
         out["cpu_baseline"] = {
-            "value": round(est, 3), "unit": "s", "cores": workers,
-            "kind": "reference" if _ref_core() else "port",
-            "sample": (f"oracle/port sfft with dense sampling (the reference's as-shipped "
-                       f"evaluate_many) threaded over {workers} cores, gather by "
-                       f"{'the reference compiled _core' if _ref_core() else 'oracle C'}; "
-                       f"ran {info['elapsed_s']:.1f}s = {info['samples_done']} of "
-                       f"{info['samples_total']} samples, extrapolated by sample count"),
+            "value": round(secs, 3), "unit": "s", "cores": workers, "kind": "port",
+            "extrapolated": False,
+            "sample": (f"the whole metric instance, run to completion and timed: oracle/port "
+                       f"sfft driver with the reference's structured lattice sampler "
+                       f"(bincount + numpy ifft) and numpy pocketfft DFTs on {workers} "
+                       f"threads, gather by "
+                       f"{'the reference compiled _core (oracle/_ref)' if _ref_core() else 'oracle C'}"
+                       f"; {samples} samples, support {nsup}"),
+            "algorithm_matched": True,
+            "dense_as_shipped": dense,
         }
         if h is not None:
             rate, kind, hi = cpu_hash_bounded(h["rows_host_sample"], h["zmat"], h["M"],
@@ -697,27 +811,39 @@ def main():
         dist.destroy_process_group()
 
 
-def all_configs(reps=3):
-    """Entry-point device time of the other BASELINE configs on this GPU
-    (median of `reps` after one warm-up; parity = exact support for the
-    exact-sparse configs, planted support for config 1)."""
+def _timed(fn, reps=3):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    ts, out = [], None
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), out
+
+
+def _phases(per):
+    ph = {k[len("stage:"):]: round(v[0], 3) for k, v in per.items() if k.startswith("stage:")}
+    rest = {k: round(v[0], 3) for k, v in per.items()
+            if not k.startswith("stage:") and k != "sfftb_sfft_stage"}
+    return ph, rest
+
+
+def all_configs(peak, src, workers, cpu=True):
+    """SURVEY 8(d)'s per-config rows on this GPU: device time of the entry
+    point (median of 3 after a warm-up), its phase breakdown from one
+    instrumented run, the dominant kernel against its roofline, and the
+    algorithm-matched CPU reference on the same inputs in the same run."""
     import torch
 
     import paper_2006_13053_b200 as pkg
-
-    def timed(fn):
-        fn()
-        torch.cuda.synchronize()
-        ts, out = [], None
-        for _ in range(reps):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            out = fn()
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts), out
+    from oracle import port
 
     out = {}
     for name in ("config2", "config3", "config5"):
@@ -725,14 +851,35 @@ def all_configs(reps=3):
         poly = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
         box = pkg.Box(w.d, w.lo, w.hi)
         params = pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
-        ms, res = timed(lambda: pkg.sfft(pkg.oracle_from_poly(
-            poly, noise_sigma=w.sigma, noise_seed=w.noise_seed), box, params, seed=w.seed))
+
+        def step():
+            return pkg.sfft(pkg.oracle_from_poly(poly, noise_sigma=w.sigma,
+                                                 noise_seed=w.noise_seed),
+                            box, params, seed=w.seed)
+
+        ms, res = _timed(step)
+        per, per_list, shapes = sfft_profile(step)
+        ph, rest = _phases(per)
+        rl = roofline_sfft({"ms": ms, "per_entry": per, "per_list": per_list,
+                            "shapes": shapes}, peak, src)
         ent = {"entry": "sfft", "ms": round(ms, 3), "samples": res.sample_count,
-               "support": len(res.support)}
+               "support": len(res.support), "stages": len(res.stage_log),
+               "phases_ms": ph, "other_entry_points_ms": rest,
+               "dominant": {k: rl.get(k) for k in ("kernel", "ms_total", "share_of_step",
+                                                    "achieved", "unit", "frac", "fp64_tflops",
+                                                    "fp64_frac")}}
         if w.sigma == 0:
             ent["exact_support"] = bool(np.array_equal(
                 res.support.elems, w.support[np.lexsort(w.support.T[::-1])]))
+        if cpu:
+            secs, samples, nsup = cpu_sfft_structured(w, workers)
+            ent["cpu"] = {"value": round(secs, 3), "unit": "s", "cores": workers,
+                          "kind": "port", "algorithm_matched": True,
+                          "same_samples": samples == res.sample_count,
+                          "same_support_size": nsup == len(res.support)}
         out[w.name] = ent
+
+    # config 1: fixed Gamma, launch-latency bound
     w = workloads.config1()
     G = pkg.FreqSet(w.d, w.gamma, _sorted=True)
     cfg = pkg.draw_config(G, w.s, 0.1, rng=w.rng)
@@ -740,39 +887,68 @@ def all_configs(reps=3):
     smp = orc.sample_lattices_device(cfg.zmat_device(), cfg.shared_M,
                                      torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
                                      1, cfg.L, w.d).contiguous()
-    ms, det = timed(lambda: pkg.detect_and_compute(smp, cfg, G).detected_idx)
-    out["cfg1"] = {"entry": "detect_and_compute", "ms": round(ms, 3),
-                   "detected_equals_support": bool(np.array_equal(det,
-                                                                  np.sort(w.support_idx)))}
+    ms, det = _timed(lambda: pkg.detect_and_compute(smp, cfg, G).detected_idx)
+    from paper_2006_13053_b200 import _native
+
+    torch.cuda.synchronize()
+    with _native.Timeline() as tl:
+        pkg.detect_and_compute(smp, cfg, G).detected_idx  # noqa: B018
+    per = {k: round(sum(v) * 1e3, 2) for k, v in tl.ms().items()}
+    n, d, L, M = len(G), w.d, cfg.L, cfg.shared_M
+    bytes_ = n * (8 * d + 8) + L * M * 16
+    ent = {"entry": "detect_and_compute", "us": round(ms * 1e3, 1),
+           "candidates_per_s": round(n / (ms * 1e-3), 1),
+           "detected_equals_support": bool(np.array_equal(det, np.sort(w.support_idx))),
+           "breakdown_us": per,
+           "roofline": {"bound": "launch latency", "algorithmic_bytes": bytes_,
+                        "achieved_gbs": round(bytes_ / (ms * 1e-3) / 1e9, 2), "peak": peak,
+                        "frac": round(bytes_ / (ms * 1e-3) / 1e9 / peak, 5),
+                        "launches": len(tl.records)}}
+    if cpu:
+        smp_h = [s for s in smp.cpu().numpy()]
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            port.detect_and_compute(smp_h, M, cfg.zmat(), w.gamma,
+                                    gather_backend="reference" if _ref_core() else "port")
+            ts.append(time.perf_counter() - t0)
+        ent["cpu"] = {"value": round(min(ts) * 1e6, 1), "unit": "us", "cores": 1,
+                      "kind": "port", "what": "detect_and_compute on the host (pocketfft DFTs "
+                      "+ the reference's compiled gather), best of 3"}
+    out["cfg1"] = ent
     return out
 
 
 def reference_arm(args, rank, world, workers):
-    """CPU reference arm: the reference's path on this host's cores."""
+    """CPU reference arm on this host's cores, same workload as our arm:
+    each step runs the algorithm-matched reference sfft on the metric
+    instance to completion (cpu_sfft_structured), timed; the as-shipped
+    dense run is reported beside it (bounded, extrapolated, flagged)."""
     if rank != 0:
         return
     w = workloads.metric_config()
     vals = []
-    info = None
-    budget = max(2.0, args.cpu_budget / 2.5)
     for k in range(args.warmup + args.steps):
-        est, info = cpu_sfft_bounded(w, budget, workers)
+        secs, samples, nsup = cpu_sfft_structured(w, workers)
         if k >= args.warmup:
-            vals.append(est)
+            vals.append(secs)
     value = statistics.mean(vals)
-    kind = "reference" if _ref_core() else "port"
-    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "s",
+    dense = cpu_sfft_dense_bounded(w, max(2.0, args.cpu_budget / 2), workers)
+    kind = "port"
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(value * 1e3, 1), "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "d10_s1000: sfft over [-32,32]^10, s=1000 random "
-                                  "frequencies, r=5, theta=1e-12, delta=0.9, seed 7"},
-           "cpu_baseline": {"value": round(value, 3), "unit": "s", "cores": workers, "kind": kind,
-                            "sample": (f"per step: oracle/port sfft (dense sampling as the "
-                                       f"reference ships it, {workers} threads) run "
-                                       f"{budget:.0f}s = {info['samples_done']} of "
-                                       f"{info['samples_total']} samples, extrapolated")},
-           "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0,
+           "config": {"workload": WORKLOAD},
+           "cpu_baseline": {"value": round(value, 4), "unit": "s", "cores": workers, "kind": kind,
+                            "extrapolated": False, "algorithm_matched": True,
+                            "sample": (f"per step: the whole metric instance ({samples} samples, "
+                                       f"support {nsup}) through oracle/port's sfft driver with "
+                                       f"the reference's structured sampler, numpy pocketfft "
+                                       f"and the reference's compiled gather on {workers} "
+                                       f"threads, run to completion")},
+           "dense_as_shipped": dense,
+           "e2e": {"value": round(value, 4), "unit": "s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

@@ -276,6 +276,18 @@ int sfftb_topk_grid(const int64_t *idx, const double *coeffs, const int64_t *cou
                     int64_t *kidx, double *kcoeffs, int64_t *kcounts, void *ws,
                     void *stream);
 
+/* Step-1 selection (step1_components, dimincr.py:122-152) for nlines = d*r
+ * coordinate lines of K estimates each (est (nlines, K) complex128 row-major,
+ * line q = (t, i) = divmod(q, r)): per line the values v of vals (nv,
+ * ascending) ranked by (|est[q][v mod K]| descending, v ascending), the first
+ * s_local with magnitude >= theta kept (kept[q] = their count); present
+ * (d, nv) int32 = 1 where any line of coordinate t kept vals[j] (the
+ * np.union1d over i).  nv <= 8192.  Replaces the host lexsort of
+ * dimincr.py:143-146. */
+int sfftb_step1_select(const double *est, int64_t nlines, int64_t K,
+                       const int64_t *vals, int64_t nv, int64_t r, int64_t s_local,
+                       double theta, int32_t *present, int64_t *kept, void *stream);
+
 /* Set mask bit i for every listed index (group union, dimincr.py:239-240). */
 int sfftb_mark_indices(const int64_t *idx, const int64_t *counts, int64_t G,
                        int64_t cap, uint32_t *mask, int64_t n, void *stream);

@@ -381,6 +381,20 @@ class PolyOracle:
         self.count += X.shape[0]
         return self._noise(evaluate_dense(self.support, self.coeffs, X))
 
+    def sample_lattices_tail(self, zmat, M, tail, workers=1):
+        """sample_lattice_tail for every row of zmat, in order; the structured
+        noise-free evaluations run on `workers` threads (the noise stream and
+        the counter still advance lattice by lattice)."""
+        if self.mode == "dense" or workers <= 1:
+            return [self.sample_lattice_tail(z, M, tail) for z in zmat]
+        vals = _pmap(lambda z: sample_lattice_structured(self.support, self.coeffs, z, M, tail),
+                     list(zmat), workers)
+        out = []
+        for v in vals:
+            self.count += M
+            out.append(self._noise(v))
+        return out
+
     def sample_lattice_tail(self, z, M, tail):
         """Samples at [j z/M mod 1 | tail], j < M (dimincr.py:186-191)."""
         if self.mode == "dense":
@@ -406,15 +420,27 @@ def zero_threshold(samples):
     return max(1e-12, 1e-10 * mid)
 
 
-def ghat_matrix(samples, M):
+def _pmap(fn, items, workers):
+    """list(map(fn, items)), on a thread pool when workers > 1 (numpy's FFT
+    and bincount release the GIL; results keep the input order)."""
+    items = list(items)
+    if workers <= 1 or len(items) < 2:
+        return [fn(x) for x in items]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(min(workers, len(items))) as ex:
+        return list(ex.map(fn, items))
+
+
+def ghat_matrix(samples, M, workers=1):
     """_ghat_list + np.vstack (detect.py:98-109, :132)."""
-    rows = []
-    for s in samples:
+    def one(s):
         s = np.asarray(s, dtype=np.complex128)
         if s.shape != (M,):
             raise OracleParameterError("sample vector length does not match M")
-        rows.append(dft_normalized(s))
-    return np.vstack(rows)
+        return dft_normalized(s)
+
+    return np.vstack(_pmap(one, samples, workers))
 
 
 def gather(samples, M, zmat, elems, theta0, nu, want_medians,
@@ -425,7 +451,7 @@ def gather(samples, M, zmat, elems, theta0, nu, want_medians,
         raise OracleParameterError("sample count does not match L")
     if not d * (M - 1) ** 2 < 2 ** 62:
         raise OracleParameterError("lattice size too large for int64 residues")
-    g = ghat_matrix(samples, M)
+    g = ghat_matrix(samples, M, workers)
     thr = nu * L
     em = np.asarray(elems, np.int64) % M
     if gather_backend == "reference":
@@ -594,7 +620,10 @@ def sfft(oracle, gamma, s, delta, seed, s_local=None, theta=1e-12, r=None,
 
     def detect_on(J, sparsity, s_tilde, budget, tail, rng, ls):
         M, zmat = draw_config(J, sparsity, budget, rng, c=c, L_scale=ls)
-        samples = [oracle.sample_lattice_tail(z, M, tail) for z in zmat]
+        if hasattr(oracle, "sample_lattices_tail"):
+            samples = oracle.sample_lattices_tail(zmat, M, tail, workers)
+        else:
+            samples = [oracle.sample_lattice_tail(z, M, tail) for z in zmat]
         _, idx, coeffs, _ = detect_topk(samples, M, zmat, J, s_tilde, theta, **kw)
         return idx, coeffs, M, zmat.shape[0]
 

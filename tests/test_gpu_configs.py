@@ -6,7 +6,7 @@
   through numpy's pocketfft like the reference).  Supports, sample counts and
   stage logs must be identical; coefficients within rel-l2 1e-10.
 * config 4 shape (fixed Gamma, d=10, [-2^12, 2^12]^10): 2^20 rows here (the
-  full 2^26 is checked by bench.py's sampled bit-exact hits); hits,
+  full 2^26 is checked below against the reference run and by bench.py); hits,
   detected indices bit-exact, medians within 1e-10.
 
 These run the oracle on the host for up to a minute each (``slow``).

@@ -165,3 +165,30 @@ def test_sfft_few_dims_vs_oracle(cuda, oracle_lib, d, r, sigma):
     if sigma == 0:
         order = np.lexsort(w.support.T[::-1])
         assert np.array_equal(res.support.elems, w.support[order])
+
+
+@pytest.mark.parametrize("d,N,n,s", [(6, 16, 200_000, 30), (7, 12, 120_000, 20)])
+def test_sfft_freqset_gamma_vs_oracle(cuda, oracle_lib, d, N, n, s):
+    """sfft over an explicit candidate set (a FreqSet, not a Box): every
+    pairing stage filters by the prefix projection P_{0..t}(Gamma)
+    (dimincr.py:155-175, freqset.py:139-142) on the device.  Supports, sample
+    counts and stage logs identical to the oracle's; coefficients 1e-10."""
+    pkg, port = cuda, oracle_lib
+    rng = np.random.default_rng(1000 + d)
+    gamma = workloads.rows_from_box(d, -N, N, n, rng)
+    idx = np.sort(rng.choice(gamma.shape[0], size=s, replace=False))
+    sup = gamma[idx]
+    co = workloads.mag_phase_coeffs(s, rng)
+    G = pkg.FreqSet(d, gamma, _sorted=True)
+    p = pkg.SparsePoly(pkg.FreqSet(d, sup, _sorted=True), co)
+    res = pkg.sfft(pkg.oracle_from_poly(p), G, pkg.SfftParams(s, 0.9, r=2), seed=11)
+    ref = port.sfft(port.PolyOracle(sup, co, mode="structured"), gamma, s, 0.9, 11, r=2)
+    assert np.array_equal(res.support.elems, ref[0])
+    assert np.array_equal(res.support.elems, sup)
+    assert res.sample_count == ref[2]
+    got = [(e["stage"], e["t"], e["i"], e["candidates"], e["kept"], e["samples"])
+           for e in res.stage_log]
+    want = [(e["stage"], e["t"], e["i"], e["candidates"], e["kept"], e["samples"])
+            for e in ref[3]]
+    assert got == want
+    assert workloads.rel_l2(res.coeffs, ref[1]) <= 1e-10
