@@ -443,3 +443,41 @@ def test_hash_without_host_bound_mixed_rows(cuda, oracle_lib):
     ghat = _dev.download(b.ghat)
     want_h, _ = oracle_lib.gather_c(srt % M, z, M, ghat, 1e-9, L / 2, True)
     assert np.array_equal(_dev.download(b.hits), want_h)
+
+
+@pytest.mark.parametrize("K,nv,r,s_local,theta", [(65, 65, 5, 2000, 1e-12), (129, 129, 3, 40, 0.5),
+                                                 (64, 33, 2, 7, 0.0), (1000, 1000, 4, 100, 0.2)])
+def test_step1_select_matches_reference_lexsort(cuda, K, nv, r, s_local, theta):
+    """sfftb_step1_select == step1_components' selection (dimincr.py:143-146):
+    per line the s_local largest |est[v mod K]| (ties: smaller v first),
+    >= theta, union over the r lines of each coordinate -- with planted exact
+    magnitude ties and values below theta."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    pkg = cuda
+    rng = np.random.default_rng(K + nv)
+    d = 3
+    nl = d * r
+    est = rng.standard_normal((nl, K)) + 1j * rng.standard_normal((nl, K))
+    est[:, ::5] = est[:, 1:2]  # exact ties
+    est[:, 3::7] *= 1e-3       # small values
+    vals = np.sort(rng.choice(np.arange(-K // 2, K // 2 + K), size=nv, replace=False))
+    off = (d * nv + 1) // 2 * 2
+    res = _dev.empty((off + 2 * nl,), torch.int32)
+    _native.call("sfftb_step1_select", _dev.ptr(_dev.upload(est)), nl, K,
+                 _dev.ptr(_dev.upload(vals)), nv, r, s_local, theta, _dev.ptr(res),
+                 res[off:].data_ptr(), _dev.stream())
+    arr = _dev.download(res)
+    present = arr[:d * nv].reshape(d, nv) != 0
+    kept = arr[off:].view(np.int64)
+    for t in range(d):
+        union = np.zeros(0, np.int64)
+        for i in range(r):
+            mags = np.abs(est[t * r + i][vals % K])
+            order = np.lexsort((vals, -mags))[:s_local]
+            order = order[mags[order] >= theta]
+            assert kept[t * r + i] == order.size
+            union = np.union1d(union, vals[order])
+        assert np.array_equal(vals[present[t]], union)
