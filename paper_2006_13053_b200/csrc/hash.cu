@@ -1015,7 +1015,10 @@ __global__ void lattice_values_kernel(const int64_t* __restrict__ elems, int d,
 // vals (n, L) the hits count #{l: |v_l| > theta} with |.| = hypot (np.abs) and,
 // for rows with hits >= thr, np.median of the real and imaginary parts: the
 // middle element (odd L) or the mean of the two middle elements (even L).
-// One warp per row; values staged in shared memory, stable ranks.
+// One warp per row; values staged in shared memory (L <= 128) or read from
+// the row itself in global memory (any L: the reference's numpy fallback,
+// _kernels/__init__.py:62, serves every L > _MAX_COMPILED_L = 128), stable
+// ranks.
 __global__ void __launch_bounds__(256)
     rows_hits_medians_kernel(const double2* __restrict__ vals, int64_t n, int L, double theta,
                              double thr, int want_medians, int64_t* __restrict__ hits,
@@ -1024,24 +1027,26 @@ __global__ void __launch_bounds__(256)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool staged = L <= 128;
     for (int64_t i = gw; i < n; i += nw) {
         int h = 0;
         for (int l = lane; l < L; l += 32) {
             const double2 v = vals[i * L + l];
-            sv[wib][l] = v;
+            if (staged) sv[wib][l] = v;
             h += hypot(v.x, v.y) > theta;
         }
         for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
         __syncwarp();
+        const double2* row = staged ? sv[wib] : vals + i * L;
         double2 m = make_double2(0.0, 0.0);
         if (want_medians && (double)h >= thr) {
             const int lo = (L - 1) / 2, hi = L / 2;
             double lo_re = 0.0, hi_re = 0.0, lo_im = 0.0, hi_im = 0.0;
             for (int l = lane; l < L; l += 32) {
-                const double2 v = sv[wib][l];
+                const double2 v = row[l];
                 int rr = 0, ri = 0;
                 for (int j = 0; j < L; ++j) {
-                    const double2 o = sv[wib][j];
+                    const double2 o = row[j];
                     rr += (o.x < v.x) || (o.x == v.x && j < l);
                     ri += (o.y < v.y) || (o.y == v.y && j < l);
                 }
@@ -1609,7 +1614,7 @@ extern "C" int sfftb_threshold_mask(const int64_t* hits, int64_t n, double thr, 
 extern "C" int sfftb_rows_hits_medians(const double* vals, int64_t n, int64_t L, double theta,
                                        double thr, int want_medians, int64_t* hits,
                                        double* medians, void* stream) {
-    SFFTB_REQUIRE(n >= 0 && L >= 1 && L <= 128, "rows_hits_medians: 1 <= L <= 128");
+    SFFTB_REQUIRE(n >= 0 && L >= 1 && L < (int64_t(1) << 30), "rows_hits_medians: bad L");
     if (n == 0) return SFFTB_OK;
     rows_hits_medians_kernel<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(
         (const double2*)vals, n, (int)L, theta, thr, want_medians, hits, (double2*)medians);

@@ -158,6 +158,10 @@ extern "C" int sfftb_rows_injective_mod(const int64_t* elems, int64_t n, int64_t
     return sfftb_injective_mod_dev((const int64_t*)de, n, d, p, injective, st);
 }
 
+// Largest lattice count the reference's compiled gather serves
+// (_kernels/__init__.py:26 _MAX_COMPILED_L); beyond it the numpy path applies.
+static constexpr int64_t kMaxCompiledL = 128;
+
 extern "C" int sfftb_detect_gather(const int64_t* elems, int64_t n, int64_t d,
                                    const int64_t* zmat, int64_t L, int64_t M, const double* ghat,
                                    double theta, double hit_threshold, int want_medians,
@@ -167,7 +171,6 @@ extern "C" int sfftb_detect_gather(const int64_t* elems, int64_t n, int64_t d,
         set_error("medians require an odd lattice count");
         return SFFTB_EINVAL;
     }
-    SFFTB_REQUIRE(L <= 128 || !want_medians, "detect_gather: medians need L <= 128");
     if (n == 0) return SFFTB_OK;
     cudaStream_t st = cudaStreamPerThread;
     // detected iff (double)hits >= hit_threshold  <=>  hits >= ceil(thr)
@@ -202,6 +205,34 @@ extern "C" int sfftb_detect_gather(const int64_t* elems, int64_t n, int64_t d,
                                    st));
     SFFTB_CUDA(cudaMemcpyAsync(dth, &theta, sizeof(double), cudaMemcpyHostToDevice, st));
     int rc;
+    if (L > kMaxCompiledL) {
+        // the reference's numpy path for L > _MAX_COMPILED_L (_kernels/__init__.py:62,
+        // fallback.py:106-131): per row the L values ghat[l, r_l], hits by
+        // np.abs (hypot) > theta, np.median of real and imaginary parts; rows
+        // in chunks of <= 256 MB of values
+        const int64_t chunk = std::max<int64_t>(1, ((int64_t)256 << 20) / (16 * L));
+        void *dv, *dm;
+        SFFTB_CUDA(b.alloc(&dv, sizeof(double2) * std::min(n, chunk) * L));
+        SFFTB_CUDA(b.alloc(&dm, sizeof(double2) * n));
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int64_t cn = std::min(chunk, n - c0);
+            rc = sfftb_lattice_values((const int64_t*)de + c0 * d, d, (const int64_t*)dz, L, M,
+                                      (const double*)dg, nullptr, cn, (double*)dv, st);
+            if (rc) return rc;
+            rc = sfftb_rows_hits_medians((const double*)dv, cn, L, theta, hit_threshold,
+                                         want_medians, (int64_t*)dhits + c0,
+                                         (double*)((double2*)dm + c0), st);
+            if (rc) return rc;
+        }
+        SFFTB_CUDA(cudaMemcpyAsync(hits, dhits, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+        if (want_medians)
+            SFFTB_CUDA(cudaMemcpyAsync(medians, dm, sizeof(double2) * n, cudaMemcpyDeviceToHost,
+                                       st));
+        else
+            memset(medians, 0, sizeof(double) * 2 * n);
+        SFFTB_CUDA(cudaStreamSynchronize(st));
+        return SFFTB_OK;
+    }
     if (L > 0) {
         rc = sfftb_nonzero_bitmap((const double*)dg, 1, L, M, (const double*)dth,
                                   (uint32_t*)dbits, st);

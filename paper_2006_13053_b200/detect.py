@@ -195,10 +195,17 @@ def _theta_tensor(theta):
     return torch.full((1,), float(theta), dtype=torch.float64, device=_dev.device())
 
 
+# the reference dispatcher serves L <= 128 with its compiled gather and larger
+# L with the numpy fallback (_kernels/__init__.py:26,62): |v| by hypot, np.median
+MAX_COMPILED_L = 128
+
+
 def _gather(samples, config, gamma, zero, want_medians, want_hits=True):
     """Device detection for one configuration -> engine Batch (G = 1)."""
     M = config.shared_M
-    if M is None:
+    if M is None or config.L > MAX_COMPILED_L:
+        # distinct lattice sizes, or more lattices than the reference's
+        # compiled gather serves: the reference's numpy semantics
         return _gather_mixed(samples, config, gamma, zero, want_medians)
     if not gamma.dim * (M - 1) ** 2 < 2**62:
         raise ParameterError("lattice size too large for int64 residues")

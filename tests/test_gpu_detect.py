@@ -284,3 +284,36 @@ def test_streamed_upload_matches_resident(cuda, monkeypatch):
     assert np.array_equal(got.detected_idx, want.detected_idx)
     assert np.array_equal(got.coeffs, want.coeffs)
     assert np.array_equal(got.detected_idx, sup)
+
+
+@pytest.mark.parametrize("L", [129, 131, 201])
+def test_more_than_128_lattices_numpy_semantics(cuda, oracle_lib, L):
+    """L > _MAX_COMPILED_L (=128): the reference dispatcher takes its numpy
+    fallback (_kernels/__init__.py:62, fallback.py:106-131) -- hits by
+    np.abs (hypot) > theta, np.median of the real and imaginary parts.  The
+    plugin and detect_and_compute follow it (oracle: port.gather_mixed)."""
+    pkg, port = cuda, oracle_lib
+    rng = np.random.default_rng(L)
+    M, d, n = 211, 4, 5000
+    elems = workloads.rows_from_box(d, -40, 40, n, rng)
+    zmat = rng.integers(0, M, size=(L, d))
+    ghat = rng.standard_normal((L, M)) + 1j * rng.standard_normal((L, M))
+    ghat[:, rng.random(M) < 0.7] = 0.0
+    theta = 0.5
+    hits, med = pkg._kernels.detect_gather(elems % M, zmat, M, ghat, theta, L / 2, True)
+    # fallback semantics restated
+    vals = np.stack([ghat[l][port.residues(elems, zmat[l], M)] for l in range(L)], axis=1)
+    want_hits = np.sum(np.abs(vals) > theta, axis=1)
+    det = want_hits >= L / 2
+    want_med = np.zeros(n, np.complex128)
+    want_med[det] = np.median(vals[det].real, axis=1) + 1j * np.median(vals[det].imag, axis=1)
+    assert np.array_equal(hits, want_hits)
+    assert det.any()
+    assert np.array_equal(med, want_med)
+    # the public entry point on a shared-M configuration with L lattices
+    cfg = _config(pkg, zmat, M)
+    samples = [np.fft.ifft(g) * M for g in ghat]
+    S = pkg.FreqSet(d, elems, _sorted=True)
+    res = pkg.detect_and_compute(samples, cfg, S)
+    h2, _, _ = port.gather_mixed(samples, [M] * L, zmat, elems, res.theta_zero, 0.5, True)
+    assert np.array_equal(res.hits, h2)
