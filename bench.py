@@ -135,7 +135,8 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t[0])
 
@@ -713,6 +714,9 @@ def main():
     ap.add_argument("--no-hash", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config measurements (configs 1, 2, 3, 5)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--one-device", action="store_true",
+                    help="all ranks on cuda:0 (functional check of N > 1 with gloo)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local = dist_env()
@@ -723,11 +727,17 @@ def main():
 
     import torch
 
-    torch.cuda.set_device(local)
+    # --dist-backend gloo --one-device: every rank on cuda:0 with host-side
+    # collectives -- a functional check of the N > 1 paths on a 1-GPU box
+    # (timings from it are not scaling numbers)
+    torch.cuda.set_device(0 if args.one_device else local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     peak, src = hbm_peak()
     r = run_sfft_arm(args, world, rank)
     h = None if args.no_hash else run_hash_arm(args, world, rank)
