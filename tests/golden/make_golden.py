@@ -522,13 +522,72 @@ def gen_cfg4_full():
              ref_seconds=np.array([t_gen, t_cfg, t_det]))
 
 
+class _LatticeShimOracle(rpe.SamplingOracle):
+    """The reference's SamplingOracle with a structured fast path for the
+    node sets its sfft driver builds (SURVEY App. A "shimmed reference,
+    structured sampler"): a node set [(j z mod M)/M | tail], j < M, is
+    recognised exactly (the leading columns equal lattice_nodes bit for bit)
+    and evaluated as bins + inverse FFT with the tail's anchor phase
+    (oracle/port.py sample_lattice_structured, the restatement of
+    polyeval.py:78-87 that the B200 sampler implements); every other node set
+    (step 1's coordinate lines) goes through the reference's evaluate_many.
+    Harness noise per call as _NoisyFn.  Counters advance as the reference's."""
+
+    def __init__(self, p, support, coeffs, sigma=0.0, noise_seed=0):
+        super().__init__(lambda X: rpe.evaluate_many(p, X), p.dim)
+        object.__setattr__(self, "_extra", (support, coeffs, sigma, noise_seed, [0]))
+
+    __slots__ = ("_extra",)
+
+    def sample_many(self, X):
+        support, coeffs, sigma, nseed, calls = self._extra
+        X = np.asarray(X, dtype=np.float64)
+        self.count += X.shape[0]
+        M = X.shape[0]
+        t = 0
+        while t < X.shape[1] and X[0, t] == 0.0:
+            t += 1
+        vals = None
+        if t >= 1 and M >= 2:
+            z = np.rint(X[1, :t] * M).astype(np.int64)
+            nodes = (np.arange(M, dtype=np.int64)[:, None] * z % M) / M
+            tail = X[0, t:]
+            if np.array_equal(X[:, :t], nodes) and np.all(X[:, t:] == tail):
+                vals = port.sample_lattice_structured(support, coeffs, z, M, tail)
+        if vals is None:
+            vals = np.asarray(self.fn(X), dtype=np.complex128)
+        if sigma > 0:
+            vals = vals + port.noise_for_call(nseed, calls[0], M, sigma)
+        calls[0] += 1
+        return vals
+
+
+def gen_sfft_fullsize():
+    """The metric instance, config 3 and config 5 at full size through the
+    reference's own sfft driver and detection (compiled gather), with the
+    structured sampler shim above: the fixtures the full-size GPU runs and
+    oracle/port.sfft are pinned to."""
+    for name in ("metric_config", "config3", "config5"):
+        w = getattr(workloads, name)()
+        I = rfs.FreqSet(w.d, w.support, _sorted=True)
+        p = rpe.SparsePoly(I, w.coeffs)
+        oracle = _LatticeShimOracle(p, w.support, w.coeffs, w.sigma, w.noise_seed)
+        params = rdim.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
+        t0 = time.perf_counter()
+        res = rdim.sfft(oracle, ClampedBox(w.d, w.lo, w.hi), params, seed=w.seed)
+        dt = time.perf_counter() - t0
+        print(f"{name}: reference sfft (structured shim) {dt:.1f}s, "
+              f"{len(res.support)} found, {res.sample_count} samples")
+        save_sfft(f"sfft_ref_{w.name}", w, res, dt)
+
+
 GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
        "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
        "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale,
-       "cfg4_full": gen_cfg4_full}
-SLOW = {"cfg4_full"}
+       "cfg4_full": gen_cfg4_full, "sfft_fullsize": gen_sfft_fullsize}
+SLOW = {"cfg4_full", "sfft_fullsize"}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or [k for k in GEN if k not in SLOW]

@@ -1,4 +1,5 @@
-"""Full-size parity of the BASELINE configs against the CPU oracle.
+"""Full-size parity of the BASELINE configs against the reference's own
+runs (tests/golden/sfft_ref_*.npz, cfg4_full.npz) and the CPU oracle.
 
 * sfft configs (the metric instance d=10/s=1000, config 3 d=20, config 5
   noisy d=9): GPU ``sfft`` vs ``oracle.port.sfft`` with the structured
@@ -114,3 +115,25 @@ def test_config4_full_size_vs_reference_golden(cuda, oracle_lib):
     co = g["coeffs"]
     assert np.max(np.abs(res.coeffs - co)) <= 1e-10 * np.max(np.abs(co))
     assert res.theta_zero == pytest.approx(float(g["theta0"]), rel=1e-14)
+
+
+@pytest.mark.parametrize("name", ["metric_config", "config3", "config5"])
+def test_sfft_fullsize_vs_reference_golden(cuda, name):
+    """GPU sfft against the reference's own driver + detection at full size
+    (structured samples; tests/golden/sfft_ref_*.npz): supports, sample
+    counts and stage logs identical, coefficients within rel-l2 1e-10."""
+    from conftest import golden
+
+    pkg = cuda
+    w = getattr(workloads, name)()
+    g = golden(f"sfft_ref_{w.name}.npz")
+    p = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
+    orc = pkg.oracle_from_poly(p, noise_sigma=w.sigma, noise_seed=w.noise_seed)
+    res = pkg.sfft(orc, pkg.Box(w.d, w.lo, w.hi),
+                   pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r), seed=w.seed)
+    assert np.array_equal(res.support.elems, g["support"])
+    assert res.sample_count == int(g["sample_count"])
+    flat = [[e["stage"], str(e["t"]), str(e["i"]), str(e["candidates"]), str(e["kept"]),
+             str(e["samples"])] for e in res.stage_log]
+    assert flat == g["stage_log"].tolist()
+    assert workloads.rel_l2(res.coeffs, g["coeffs"]) <= 1e-10

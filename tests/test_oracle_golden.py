@@ -151,3 +151,22 @@ def test_sfft_cfg2_structured_vs_reference(oracle_lib):
                           theta=w.theta, r=w.r)
     _check_sfft(res, g, 1e-12)
     assert np.array_equal(res[0], w.support)
+
+
+@pytest.mark.parametrize("name", ["metric_config", "config3", "config5"])
+def test_sfft_fullsize_structured_vs_reference(oracle_lib, name):
+    """The metric instance (d=10, s=1000), config 3 (d=20, 76.5 M samples) and
+    config 5 (noisy, top-k truncation at every stage) at full size: the
+    oracle's sfft against the reference's own driver and detection run on
+    the same structured samples (tests/golden/make_golden.py
+    gen_sfft_fullsize).  Supports, sample counts and stage logs exact;
+    coefficients to roundoff.  This pins the oracle the full-size GPU tests
+    (tests/test_gpu_configs.py) compare against."""
+    w = getattr(workloads, name)()
+    g = golden(f"sfft_ref_{w.name}.npz")
+    assert np.array_equal(w.support, g["true_support"])
+    orc = oracle_lib.PolyOracle(w.support, w.coeffs, mode="structured", sigma=w.sigma,
+                                noise_seed=w.noise_seed)
+    res = oracle_lib.sfft(orc, oracle_lib.Box(w.d, w.lo, w.hi), w.s, w.delta, w.seed,
+                          theta=w.theta, r=w.r, workers=8)
+    _check_sfft(res, g, 1e-12)
