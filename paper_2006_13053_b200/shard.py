@@ -93,8 +93,11 @@ def _all_gather_padded(local, per, world, group, async_op=False):
         send = local if local.shape[0] == per else torch.cat(
             [local, local.new_zeros((per - local.shape[0],) + shape[1:])])
         out = torch.empty((world * per,) + shape[1:], dtype=local.dtype, device=local.device)
-        work = dist.all_gather_into_tensor(out, send.contiguous(), group=group,
-                                           async_op=async_op)
+        # NCCL moves real words: complex blocks travel as their float64 pairs
+        src, dst = send.contiguous(), out
+        if src.is_complex():
+            src, dst = torch.view_as_real(src), torch.view_as_real(out)
+        work = dist.all_gather_into_tensor(dst, src, group=group, async_op=async_op)
         return out, work
     send = torch.zeros(shape, dtype=local.dtype)
     send[:local.shape[0]] = local.cpu()
