@@ -22,6 +22,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "median_nets.cuh"
 
 namespace sfftb {
 
@@ -995,6 +996,70 @@ __global__ void __launch_bounds__(256) medians2_pairs_kernel(
     }
 }
 
+// Thread-pair per detected row on pair tables, L odd <= 63: lane pair (2i,
+// 2i + 1) takes the real and the imaginary part of work item i, gathers its
+// L values in lattice order into registers and selects the median with the
+// pruned network of median_nets.cuh (DSETP/FSEL comparators, no ranks, no
+// shared memory).  Min/max networks agree bit for bit with the reference's
+// stable insertion sort (_core.pyx:151-161) except when -0.0 and +0.0 are
+// both present; a component holding a zero takes that insertion sort
+// itself, in lattice order.
+template <int L>
+__global__ void __launch_bounds__(256) medians_net_pairs_kernel(
+    int G, int64_t M, const double2* __restrict__ ghat, const int64_t* __restrict__ idx,
+    const int64_t* __restrict__ counts, int64_t cap, double2* __restrict__ coeffs,
+    PairTables pt) {
+    __shared__ int64_t cnt_s[32];
+    const bool cnt_in_smem = G <= 32;
+    if (cnt_in_smem && threadIdx.x < G) cnt_s[threadIdx.x] = counts[threadIdx.x];
+    __syncthreads();
+    const int64_t* cnt = cnt_in_smem ? cnt_s : counts;
+    int64_t total = 0;
+    for (int g = 0; g < G; ++g) total += cnt[g];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w2 < 2 * total;
+         w2 += stride) {
+        const int64_t w = w2 >> 1;
+        const int comp = (int)(w2 & 1);
+        int g = 0;
+        int64_t k = w;
+        while (k >= cnt[g]) k -= cnt[g++];
+        const int64_t row = idx[(int64_t)g * cap + k];
+        const uint32_t q = (uint32_t)row / (uint32_t)pt.n2;
+        const uint32_t i2 = (uint32_t)(row - (int64_t)q * pt.n2);
+        double a[L];
+        bool zero = false;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            const uint32_t gl = (uint32_t)(g * L + l);
+            uint32_t r32 = (uint32_t)__ldg(pt.P + gl * (uint32_t)pt.n1 + q) +
+                           (uint32_t)__ldg(pt.V + gl * (uint32_t)pt.n2 + i2);
+            if (r32 >= (uint32_t)M) r32 -= (uint32_t)M;
+            a[l] = __ldg(reinterpret_cast<const double*>(ghat + gl * (uint32_t)M + r32) + comp);
+            zero |= a[l] == 0.0;
+        }
+        double m;
+        if (!zero) {
+            m = median_net<L>(a);
+        } else {  // signed zeros: the reference's insertion sort, in lattice order
+            double t[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) t[l] = a[l];
+            for (int i = 1; i < L; ++i) {
+                const double v = t[i];
+                int j = i;
+                while (j > 0 && t[j - 1] > v) {
+                    t[j] = t[j - 1];
+                    --j;
+                }
+                t[j] = v;
+            }
+            m = t[L >> 1];
+        }
+        reinterpret_cast<double*>(coeffs + (int64_t)g * cap + k)[comp] = m;
+    }
+}
+
 __global__ void lattice_values_kernel(const int64_t* __restrict__ elems, int d,
                                       const int64_t* __restrict__ zmat, int L, int64_t M,
                                       const double2* __restrict__ ghat,
@@ -1702,7 +1767,32 @@ int medians_pairs_launch(const int32_t* P, const int32_t* V, int64_t n1, int64_t
                                      (const double2*)ghat, idx, counts, cap, (double2*)coeffs,
                                      pt);
     };
-    if (L <= 32)
+    // pair-table medians by selection network (medians_net_pairs_kernel):
+    // config 5 8.62 -> 7.75 ms, the metric instance unchanged (A/B on one box,
+    // profiles/r02/ab_mednet.txt); SFFTB_MEDNET=0 restores the rank kernels,
+    // 1 uses the network for dense detections only
+    static const int mednet = [] {
+        const char* e = getenv("SFFTB_MEDNET");
+        return e ? atoi(e) : 2;
+    }();
+    if (small && L <= 63 && mednet > 0 && (mednet > 1 || dense)) {
+        const int nb = num_sms() * 8;
+        switch (L) {
+#define SFFTB_MN(LL)                                                                        \
+    case LL:                                                                                \
+        medians_net_pairs_kernel<LL><<<nb, 256, 0, st>>>((int)G, M, (const double2*)ghat, \
+                                                         idx, counts, cap,                \
+                                                         (double2*)coeffs, pt);           \
+        break;
+            SFFTB_MN(1) SFFTB_MN(3) SFFTB_MN(5) SFFTB_MN(7) SFFTB_MN(9) SFFTB_MN(11)
+            SFFTB_MN(13) SFFTB_MN(15) SFFTB_MN(17) SFFTB_MN(19) SFFTB_MN(21) SFFTB_MN(23)
+            SFFTB_MN(25) SFFTB_MN(27) SFFTB_MN(29) SFFTB_MN(31) SFFTB_MN(33) SFFTB_MN(35)
+            SFFTB_MN(37) SFFTB_MN(39) SFFTB_MN(41) SFFTB_MN(43) SFFTB_MN(45) SFFTB_MN(47)
+            SFFTB_MN(49) SFFTB_MN(51) SFFTB_MN(53) SFFTB_MN(55) SFFTB_MN(57) SFFTB_MN(59)
+            SFFTB_MN(61) SFFTB_MN(63)
+#undef SFFTB_MN
+        }
+    } else if (L <= 32)
         small ? go(medians_kernel<1, true, true>) : go(medians_kernel<1, true>);
     else if (L <= 64)
     {

@@ -481,3 +481,42 @@ def test_step1_select_matches_reference_lexsort(cuda, K, nv, r, s_local, theta):
             assert kept[t * r + i] == order.size
             union = np.union1d(union, vals[order])
         assert np.array_equal(vals[present[t]], union)
+
+
+@pytest.mark.parametrize("L,G", [(3, 2), (31, 5), (39, 5), (41, 2), (63, 1)])
+def test_network_medians_ties_and_signed_zeros_bitexact(cuda, L, G):
+    """Pair-table medians by selection network (medians_net_pairs_kernel) with
+    heavy ties and +0.0/-0.0 mixes (rows holding a zero take the insertion
+    sort in lattice order) == the generic medians (sfftb_medians, bit-exact
+    to the reference's insertion sort) on the materialised J."""
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _engine, _native
+
+    rng = np.random.default_rng(100 + L)
+    M, t, n1, n2 = 101, 2, 40, 9
+    prefix = np.unique(rng.integers(-30, 31, size=(n1, t)), axis=0)
+    n1 = prefix.shape[0]
+    vals = np.unique(rng.integers(-30, 31, size=n2))
+    n2 = vals.size
+    pre_d, vals_d = _dev.upload(prefix), _dev.upload(vals)
+    J = _engine.pair_product(pre_d, vals_d)
+    n = n1 * n2
+    z = _dev.upload(rng.integers(0, M, size=(G * L, t + 1)))
+    st = _dev.stream()
+    P = _dev.empty((G * L * n1,), torch.int32)
+    V = _dev.empty((G * L * n2,), torch.int32)
+    _native.call("sfftb_pair_residues", _dev.ptr(pre_d), n1, t, _dev.ptr(vals_d), n2, _dev.ptr(z),
+                 G * L, M, _dev.ptr(P), _dev.ptr(V), st)
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 2.5, 0.0, -0.0, 0.5])
+    gh = rng.choice(pool, size=(G * L, M)) + 1j * rng.choice(pool, size=(G * L, M))
+    gh[0] = rng.normal(size=M) + 1j * rng.normal(size=M)  # some rows without zeros
+    ghat = _dev.upload(gh.astype(np.complex128))
+    idx = _dev.upload(np.concatenate([np.arange(n) for _ in range(G)]))
+    cnt = _dev.upload(np.full(G, n, dtype=np.int64))
+    o1, o2 = _dev.empty((G * n,), torch.complex128), _dev.empty((G * n,), torch.complex128)
+    _native.call("sfftb_medians", _dev.ptr(J), t + 1, _dev.ptr(z), G, L, M, _dev.ptr(ghat),
+                 _dev.ptr(idx), _dev.ptr(cnt), n, _dev.ptr(o1), st)
+    _native.call("sfftb_medians_pairs", _dev.ptr(P), _dev.ptr(V), n1, n2, G, L, M,
+                 _dev.ptr(ghat), _dev.ptr(idx), _dev.ptr(cnt), n, _dev.ptr(o2), st)
+    assert np.array_equal(_dev.download(o1).view(np.int64), _dev.download(o2).view(np.int64))

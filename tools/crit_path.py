@@ -2,7 +2,7 @@
 the detection stream (before every phase-2 call) or on the spectra stream
 (before every phase-4 call) and report how the step time moves.  A slope
 near the number of stages means that chain is critical; near 0, slack.
-    python tools/crit_path.py"""
+    python tools/crit_path.py [workload name, default metric_config]"""
 import os
 import statistics
 import sys
@@ -14,7 +14,7 @@ import paper_2006_13053_b200 as pkg  # noqa: E402
 from paper_2006_13053_b200 import _stage  # noqa: E402
 import workloads  # noqa: E402
 
-w = workloads.metric_config()
+w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "metric_config")()
 box = pkg.Box(w.d, w.lo, w.hi)
 params = pkg.SfftParams(w.s, w.delta, theta=w.theta, r=w.r)
 poly = pkg.SparsePoly(pkg.FreqSet(w.d, w.support, _sorted=True), w.coeffs)
@@ -37,7 +37,8 @@ def make(phase_target, us):
 
 
 def step():
-    return pkg.sfft(pkg.oracle_from_poly(poly), box, params, seed=w.seed)
+    return pkg.sfft(pkg.oracle_from_poly(poly, noise_sigma=w.sigma, noise_seed=w.noise_seed),
+                    box, params, seed=w.seed)
 
 
 def timeit(reps=7):
