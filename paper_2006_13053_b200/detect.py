@@ -115,8 +115,10 @@ class DetectionResult:
 
 # ---------------------------------------------------------------------------
 
-def _stack_samples(samples, config):
-    """Validated (L, M) complex128 CUDA tensor (detect.py:98-109 checks)."""
+def _stack_samples(samples, config, deferred=False):
+    """Validated (L, M) complex128 CUDA tensor (detect.py:98-109 checks).
+    With ``deferred`` the finiteness check is returned as a device flag
+    instead of being read here: (tensor, flag or None)."""
     L = config.L
     if isinstance(samples, torch.Tensor):
         if samples.ndim != 2 or samples.shape[0] != L:
@@ -136,8 +138,11 @@ def _stack_samples(samples, config):
                     f"sample vector of length {s.shape} does not match M={lat.M}")
             rows.append(s)
         if config.shared_M is None:
-            return [_dev.upload(r).reshape(1, -1) for r in rows]
+            t = [_dev.upload(r).reshape(1, -1) for r in rows]
+            return (t, None) if deferred else t
         t = _dev.upload(np.vstack(rows))
+    if deferred:
+        return t, torch.isfinite(torch.view_as_real(t)).all()
     if not bool(torch.isfinite(torch.view_as_real(t)).all()):
         raise ParameterError("samples contain NaN or Inf")
     return t
@@ -282,8 +287,43 @@ def _result_from_batch(gamma, b, theta0, with_coeffs):
     return DetectionResult(gamma, b.hits, idx, coeffs, theta0)
 
 
+def _detect_async(samples, config, gamma, zero, want_medians):
+    """The shared-M detection with ONE host synchronisation: the finiteness
+    check, the zero test and the whole chain are enqueued back to back, then
+    (finite flag, theta0, detected count) come back in one read.  None when
+    the call takes another path (distinct lattice sizes, L > 128, a large
+    host-resident candidate set that streams its upload)."""
+    M = config.shared_M
+    if M is None or config.L > MAX_COMPILED_L:
+        return None
+    host = gamma._host if gamma._dev is None else None
+    if host is not None and host.nbytes >= STREAM_UPLOAD_BYTES:
+        return None
+    t, fin = _stack_samples(samples, config, deferred=True)
+    if not gamma.dim * (M - 1) ** 2 < 2**62:
+        raise ParameterError("lattice size too large for int64 residues")
+    if config.dim != gamma.dim:
+        raise ParameterError("candidate set/lattice dimension mismatch")
+    L = config.L
+    theta = _engine.zero_thresholds(t, 1, L, M) if zero is None else \
+        _theta_tensor(zero.theta_zero)
+    b = _engine.detect_batch(t, M, config.zmat_device(), 1, L, gamma.device(), _kbound(gamma),
+                             config.nu, theta0=theta, want_medians=want_medians, want_hits=True)
+    small = torch.stack([fin.to(torch.float64), theta.reshape(-1)[0],
+                         b.counts.reshape(-1)[0].to(torch.float64)])
+    f, th, cnt = _dev.download(small).tolist()
+    if f != 1.0:
+        raise ParameterError("samples contain NaN or Inf")
+    cnt = int(cnt)
+    coeffs = b.coeffs[:cnt] if want_medians else None
+    return DetectionResult(gamma, b.hits, b.idx[:cnt], coeffs, th)
+
+
 def detect_frequencies(samples, config, gamma, zero=None):
     """Alg. 1: keep k when its nonzero count reaches nu*L (detect.py:149-155)."""
+    res = _detect_async(samples, config, gamma, zero, False)
+    if res is not None:
+        return res
     t = _stack_samples(samples, config)
     if zero is None:
         zero = _zero_from_device(t)
@@ -297,6 +337,9 @@ def detect_and_compute(samples, config, gamma, zero=None):
         raise ParameterError("coefficient computation requires nu = 1/2")
     if config.L % 2 == 0:
         raise ParameterError("coefficient computation requires odd L")
+    res = _detect_async(samples, config, gamma, zero, True)
+    if res is not None:
+        return res
     t = _stack_samples(samples, config)
     if zero is None:
         zero = _zero_from_device(t)
