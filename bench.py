@@ -637,15 +637,15 @@ def fft_flops(N):
 
 def bluestein_N(M):
     """The library's convolution length (csrc/fft.cu bluestein_N): the
-    smallest power of two >= max(2M-1, 256), or 192*{128, 256} when that is
-    smaller and above the single-CTA sizes."""
+    smallest power of two >= max(2M-1, 256), or 192*{128, 256} (four-step) /
+    9*2^k (single CTA) when that is smaller."""
     N = 256
     while N < 2 * M - 1:
         N *= 2
-    if N > 8192:
-        for c in (24576, 49152):
-            if c >= 2 * M - 1 and c < N:
-                return c
+    cands = (24576, 49152) if N > 8192 else (576, 1152, 2304, 4608)
+    for c in cands:
+        if c >= 2 * M - 1 and c < N:
+            return c
     return N
 
 

@@ -33,6 +33,7 @@ namespace sfftb {
 struct BluesteinPlan {
     int64_t M = 0;
     int N = 0, N1 = 0, N2 = 0, logN = 0;
+    int P9 = 0;  // single-CTA mixed length N = 9 * P9 (P9 a power of two), else 0
     double2* chirp = nullptr;  // M
     double2* bhat = nullptr;   // N (natural if N <= 8192, else [k2][k1] = B^[k2 + N2 k1])
     double2* tw_hi = nullptr;  // N/64 : e^{-2 pi i 64k/N}
@@ -58,11 +59,19 @@ static int bluestein_log(int64_t M) {
 // and, above the single-CTA sizes, the mixed-radix 192 * {128, 256} of the
 // register four-step kernels (N = 3 * 2^k: 25% fewer bytes per pass than the
 // next power of two for M in (8192, 12288] and (16384, 24576]).
+// Within the single-CTA sizes the smallest 9 * 2^k >= max(2M-1, 576) is used
+// when it is below the power of two (bluestein_small9: M = 2069 -> 4608
+// instead of 8192, M = 1039 -> 2304 instead of 4096).
 static int64_t bluestein_N(int64_t M) {
     const int64_t pow2 = int64_t(1) << bluestein_log(M);
     if (pow2 > (int64_t(1) << kSmallMaxLog)) {
         for (int64_t c : {int64_t(24576), int64_t(49152)})
             if (c >= 2 * M - 1 && c < pow2) return c;
+    } else {
+        static const bool off = getenv("SFFTB_NO_SMALL9") != nullptr;  // A/B only
+        if (!off)
+            for (int64_t c : {int64_t(576), int64_t(1152), int64_t(2304), int64_t(4608)})
+                if (c >= 2 * M - 1 && c < pow2) return c;
     }
     return pow2;
 }
@@ -98,6 +107,37 @@ static void host_fft_ld(std::vector<long double>& re, std::vector<long double>& 
                 re[i + k] += tr;
                 im[i + k] += ti;
             }
+    }
+}
+
+// Forward DFT of any length 2^a 3^b in long double by recursive radix-2/3
+// decimation in time (plan construction only).
+static void host_fft23_ld(std::vector<long double>& re, std::vector<long double>& im) {
+    const size_t n = re.size();
+    if (n == 1) return;
+    const size_t R = (n % 2 == 0) ? 2 : 3, m = n / R;
+    std::vector<long double> r[3], i[3];
+    for (size_t q = 0; q < R; ++q) {
+        r[q].resize(m);
+        i[q].resize(m);
+        for (size_t j = 0; j < m; ++j) {
+            r[q][j] = re[R * j + q];
+            i[q][j] = im[R * j + q];
+        }
+        host_fft23_ld(r[q], i[q]);
+    }
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (size_t k = 0; k < n; ++k) {
+        long double sr = 0.0L, si = 0.0L;
+        for (size_t q = 0; q < R; ++q) {
+            const long double a = -2.0L * PI * (long double)((q * k) % n) / (long double)n;
+            const long double c = cosl(a), sn = sinl(a);
+            const long double xr = r[q][k % m], xi = i[q][k % m];
+            sr += xr * c - xi * sn;
+            si += xr * sn + xi * c;
+        }
+        re[k] = sr;
+        im[k] = si;
     }
 }
 
@@ -139,7 +179,9 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
     p->N = (int)bluestein_N(M);
     const bool mixed = (p->N & (p->N - 1)) != 0;
     p->logN = mixed ? 0 : lg;
-    if (mixed) {
+    if (mixed && p->N <= (1 << kSmallMaxLog)) {
+        p->P9 = p->N / 9;  // bluestein_small9
+    } else if (mixed) {
         p->N1 = 192;
         p->N2 = p->N / 192;
     } else if (lg > kSmallMaxLog) {
@@ -179,7 +221,9 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
         long double a = -2.0L * PI * (64.0L * k) / N;
         thi[k] = make_double2((double)cosl(a), (double)sinl(a));
     }
-    if (mixed)
+    if (p->P9)
+        host_fft23_ld(br, bi);
+    else if (mixed)
         host_fft3_ld(br, bi);
     else
         host_fft_ld(br, bi);
@@ -188,6 +232,8 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
         if (p->N1) {  // B^[k2 + N2 k1] stored at [k2][k1]
             const int k2 = k % p->N2, k1 = k / p->N2;
             dst = k2 * p->N1 + k1;
+        } else if (p->P9) {  // B^[k1 + 9 k2] stored at [k1][k2] (bluestein_small9)
+            dst = (k % 9) * p->P9 + k / 9;
         }
         bh[dst] = make_double2((double)(br[k] / N), (double)(bi[k] / N));
     }
@@ -324,6 +370,111 @@ __global__ void __launch_bounds__(N / 16) bluestein_small(DftArgs a) {
     double2* y = a.y + b * a.ys;
     for (int h = tid; h < a.M; h += T) {
         double2 v = cmul(a.chirp[h], smem[pad16(h)]);
+        y[h] = cscale(conj_if<INV>(v), a.scale);
+    }
+}
+
+// e^{-+2 pi i m/9}, m in {1, 2, 4} (the products b c of the 3 x 3 split)
+template <bool INV>
+__device__ __forceinline__ double2 w9(int m) {
+    double2 w;
+    switch (m) {
+        case 1: w = make_double2(0.76604444311897803520, -0.64278760968653932632); break;
+        case 2: w = make_double2(0.17364817766693034885, -0.98480775301220805936); break;
+        default: w = make_double2(-0.93969262078590838405, -0.34202014332566873304); break;
+    }
+    if (INV) w.y = -w.y;
+    return w;
+}
+
+// 9-point DFT, natural order: n = 3a + b, k = c + 3d,
+// X[c + 3d] = sum_b w3^{bd} w9^{bc} sum_a x[3a + b] w3^{ac}.
+template <bool INV>
+__device__ __forceinline__ void dft9(double2 (&v)[9]) {
+    double2 y[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        double2 p = v[b], q = v[3 + b], r = v[6 + b];
+        dft3<INV>(p, q, r);
+        y[b][0] = p;
+        y[b][1] = b ? cmul(q, w9<INV>(b)) : q;
+        y[b][2] = b ? cmul(r, w9<INV>(2 * b)) : r;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double2 p = y[0][c], q = y[1][c], r = y[2][c];
+        dft3<INV>(p, q, r);
+        v[c] = p;
+        v[c + 3] = q;
+        v[c + 6] = r;
+    }
+}
+
+// Single-CTA Bluestein for N = 9 P (P a power of two, 64..512): with
+// j = P r + p and k = k1 + 9 k2,
+//   X[k1 + 9 k2] = sum_p w_P^{p k2} [w_N^{p k1} sum_r x[P r + p] w_9^{r k1}],
+// so the data live as 9 sub-arrays of P (sub-array r holds x[P r + .]): a
+// 9-point DFT down every column p with the twiddle w_N^{p k1}, then 9
+// concurrent P-point Stockham FFTs (fft_smem, P/16 threads each) leave
+// X[k1 + 9 k2] at sub-array k1, position k2 -- the layout B^ is stored in.
+// The inverse runs the same steps backwards and ends in natural order.
+template <int P, bool INV>
+__global__ void __launch_bounds__(9 * P / 16) bluestein_small9(DftArgs a) {
+    extern __shared__ double2 smem[];
+    constexpr int N = 9 * P, T = N / 16, SUB = P + P / 16, TPF = P / 16;
+    double2* hi = smem + 9 * SUB;
+    double2* lo = hi + N / 64;
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    stage(hi, a.tw_hi, N / 64);
+    stage(lo, a.tw_lo, 64);
+    const double2* x = a.x + b * a.xs;
+    for (int i = tid; i < N; i += T) {
+        double2 v = make_double2(0.0, 0.0);
+        if (i < a.M) v = cmul(conj_if<INV>(x[i]), a.chirp[i]);
+        smem[(i / P) * SUB + pad16(i % P)] = v;
+    }
+    __syncthreads();
+    const TwTwoLevel twN{hi, lo, 1};
+    const TwTwoLevel twP{hi, lo, 9};
+    double2* sub = smem + (tid / TPF) * SUB;
+    const int tpf = tid % TPF;
+    // forward: radix 9 down the columns, twiddle w_N^{p k1}
+    for (int p = tid; p < P; p += T) {
+        double2 v[9];
+#pragma unroll
+        for (int r = 0; r < 9; ++r) v[r] = smem[r * SUB + pad16(p)];
+        dft9<false>(v);
+#pragma unroll
+        for (int k1 = 0; k1 < 9; ++k1)
+            smem[k1 * SUB + pad16(p)] = (k1 && p) ? cmul(v[k1], twN.template get<false>(p * k1))
+                                                  : v[k1];
+    }
+    __syncthreads();
+    fft_smem<P, false>(sub, tpf, twP);
+    for (int i = tid; i < N; i += T) {
+        const int k1 = i / P, k2 = i % P;
+        double2* e = smem + k1 * SUB + pad16(k2);
+        *e = cmul(*e, a.bhat[i]);
+    }
+    __syncthreads();
+    // inverse: P-point IFFTs, twiddle w_N^{-p k1}, radix 9 back to natural order
+    fft_smem<P, true>(sub, tpf, twP);
+    for (int p = tid; p < P; p += T) {
+        double2 v[9];
+#pragma unroll
+        for (int k1 = 0; k1 < 9; ++k1) {
+            const double2 u = smem[k1 * SUB + pad16(p)];
+            v[k1] = (k1 && p) ? cmul(u, twN.template get<true>(p * k1)) : u;
+        }
+        dft9<true>(v);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) smem[r * SUB + pad16(p)] = v[r];
+    }
+    __syncthreads();
+    double2* y = a.y + b * a.ys;
+    for (int h = tid; h < a.M; h += T) {
+        double2 v = cmul(a.chirp[h], smem[(h / P) * SUB + pad16(h % P)]);
         y[h] = cscale(conj_if<INV>(v), a.scale);
     }
 }
@@ -935,6 +1086,28 @@ static int launch_small(const DftArgs& a, int64_t batch, cudaStream_t st) {
     return SFFTB_OK;
 }
 
+template <int P, bool INV>
+static int launch_small9(const DftArgs& a, int64_t batch, cudaStream_t st) {
+    constexpr int N = 9 * P;
+    const size_t sm = sizeof(double2) * (9 * (P + P / 16) + N / 64 + 64);
+    SFFTB_CUDA(allow_smem(bluestein_small9<P, INV>, sm));
+    bluestein_small9<P, INV><<<(unsigned)batch, N / 16, sm, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+template <bool INV>
+static int small9_dispatch(int P, const DftArgs& a, int64_t batch, cudaStream_t st) {
+    switch (P) {
+        case 64: return launch_small9<64, INV>(a, batch, st);
+        case 128: return launch_small9<128, INV>(a, batch, st);
+        case 256: return launch_small9<256, INV>(a, batch, st);
+        case 512: return launch_small9<512, INV>(a, batch, st);
+    }
+    set_error("internal: bad 9 * 2^k Bluestein size");
+    return SFFTB_EINVAL;
+}
+
 template <bool INV>
 static int small_dispatch(int lg, const DftArgs& a, int64_t batch, cudaStream_t st) {
     switch (lg) {
@@ -1128,6 +1301,9 @@ extern "C" int sfftb_dft(const double* x, int64_t x_stride, double* y, int64_t y
     a.tw_n2 = p->tw_n2;
     a.work = (double2*)ws;
     a.hi_in_smem = p->N / 64 <= 2048;  // <= 32 KB of shared memory
+    if (p->P9)
+        return inverse ? small9_dispatch<true>(p->P9, a, batch, st)
+                       : small9_dispatch<false>(p->P9, a, batch, st);
     if (p->N <= (1 << kSmallMaxLog))
         return inverse ? small_dispatch<true>(p->logN, a, batch, st)
                        : small_dispatch<false>(p->logN, a, batch, st);
