@@ -207,7 +207,18 @@ int stage_detect(const sfftb_stage_t* a, void* stream, const Marks& mark) {
                                cudaMemcpyDeviceToHost, st));
 
     // union of the kept indices (ascending)
-    if (a->umask) {
+    if (a->umask && G == 1) {
+        // one group: its kept indices are already the ascending union (the
+        // top-s emits in candidate order) -- two copies instead of mark +
+        // compaction on the latency-bound tail stages
+        const int64_t keep = std::min<int64_t>(cap, std::max<int64_t>(a->s_tilde, 1));
+        SFFTB_CUDA(cudaMemcpyAsync(a->uidx, a->kidx, (size_t)keep * sizeof(int64_t),
+                                   cudaMemcpyDeviceToDevice, st));
+        SFFTB_CUDA(cudaMemcpyAsync(a->ucount, a->kcounts, sizeof(int64_t),
+                                   cudaMemcpyDeviceToDevice, st));
+        SFFTB_CUDA(cudaMemcpyAsync(a->host_counts + G, a->ucount, sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, st));
+    } else if (a->umask) {
         const int64_t nwords = (n + 31) / 32 > 0 ? (n + 31) / 32 : 1;
         SFFTB_CUDA(cudaMemsetAsync(a->umask, 0, (size_t)nwords * sizeof(uint32_t), st));
         SFFTB_TRY(sfftb_mark_indices(a->kidx, a->kcounts, G, cap, a->umask, n, stream));
