@@ -1,7 +1,10 @@
-"""Multi-rank fixed-Gamma path on CPU: world_size 2 over gloo.
+"""Multi-rank fixed-Gamma MERGE logic on CPU: world_size 2 over gloo.
 
-Each rank runs the CPU oracle on its contiguous shard (standing in for its
-GPU) and merges with paper_2006_13053_b200.shard; the merged result must equal
+The product path (lattice-sharded DFTs, bitmap and spectra all-gathers,
+row-sharded hashing on the device) is tested on the GPU in
+tests/test_gpu_shard_threads.py.  Here, with no GPU, each rank runs the CPU
+oracle on its contiguous shard (standing in for its device) and merges with
+paper_2006_13053_b200.shard.merge_detections; the merged result must equal
 the single-process detection exactly (indices) and bitwise (coefficients).
 """
 
