@@ -108,3 +108,25 @@ def test_pair_candidates_capacity_and_restriction(cuda):
     want = rows[[tuple(r) in pool for r in rows]]
     assert np.array_equal(J.elems, want)
     assert len(J) < len(prev) * len(vals)
+
+
+@pytest.mark.parametrize("n", [0, 1, 33])
+def test_tiny_and_empty_candidate_sets(cuda, oracle_lib, n):
+    """Empty and tiny candidate sets through the single-sync detection path:
+    the same hits / detections as the oracle (detect.py:158-169)."""
+    pkg, port = cuda, oracle_lib
+    rng = np.random.default_rng(40 + n)
+    d, M, L = 3, 101, 7
+    gamma = np.unique(rng.integers(-20, 21, size=(n, d)), axis=0) if n else \
+        np.zeros((0, d), np.int64)
+    cfg = _cfg(pkg, M, L, d, seed=n)
+    smp = [rng.standard_normal(M) + 1j * rng.standard_normal(M) for _ in range(L)]
+    G = pkg.FreqSet(d, gamma, _sorted=True)
+    res = pkg.detect_and_compute(smp, cfg, G)
+    hits, idx, co, th = port.detect_and_compute(smp, M, cfg.zmat(), gamma)
+    assert res.theta_zero == pytest.approx(th, rel=1e-14)
+    assert np.array_equal(res.hits, hits)
+    assert np.array_equal(res.detected_idx, idx)
+    assert len(res.coeffs) == len(co)
+    if len(co):
+        assert np.max(np.abs(res.coeffs - co)) <= 1e-10 * max(1.0, np.max(np.abs(co)))
