@@ -66,7 +66,23 @@ class SparsePoly:
     def device(self):
         """(support int64 (s, d), coeffs complex128 (s,)) on the device."""
         if self._dev is None:
-            self._dev = (self.support.device(), _dev.upload(self.coeffs))
+            sup = self.support
+            if sup._dev is not None:
+                self._dev = (sup.device(), _dev.upload(self.coeffs))
+            else:
+                # host support: rows and coefficients travel as ONE staged
+                # buffer and one host-to-device copy (the polynomial upload
+                # opens every end-to-end reconstruction)
+                s, d = len(self), self.dim
+                rows = np.ascontiguousarray(sup.elems, dtype=np.int64).reshape(s, d)
+                co = np.ascontiguousarray(self.coeffs, dtype=np.complex128)
+                off = s * d + (s * d) % 2  # coefficients 16-byte aligned
+                buf = np.zeros(off + 2 * s, dtype=np.int64)
+                buf[:s * d] = rows.reshape(-1)
+                buf[off:] = co.view(np.int64)
+                dev = _dev.upload(buf)
+                sup._dev = dev[:s * d].view(s, d)
+                self._dev = (sup._dev, dev[off:].view(torch.complex128))
         return self._dev
 
 
