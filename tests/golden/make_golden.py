@@ -581,12 +581,59 @@ def gen_sfft_fullsize():
         save_sfft(f"sfft_ref_{w.name}", w, res, dt)
 
 
+def gen_sfft_freqset():
+    """sfft over explicit candidate sets (FreqSet Gamma, the pairing filtered
+    by the prefix projections, dimincr.py:155-175) through the reference's own
+    driver, with the structured-sampler shim; two shapes."""
+    out = {}
+    for d, N, n, s in ((6, 16, 200_000, 30), (7, 12, 120_000, 20)):
+        rng = np.random.default_rng(1000 + d)
+        gamma = workloads.rows_from_box(d, -N, N, n, rng)
+        idx = np.sort(rng.choice(gamma.shape[0], size=s, replace=False))
+        sup = gamma[idx]
+        co = workloads.mag_phase_coeffs(s, rng)
+        G = rfs.FreqSet(d, gamma, _sorted=True)
+        p = rpe.SparsePoly(rfs.FreqSet(d, sup, _sorted=True), co)
+        oracle = _LatticeShimOracle(p, sup, co)
+        t0 = time.perf_counter()
+        res = rdim.sfft(oracle, G, rdim.SfftParams(s, 0.9, r=2), seed=11)
+        dt = time.perf_counter() - t0
+        log = [[e["stage"], e["t"], e["i"], e["candidates"], e["kept"], e["samples"]]
+               for e in res.stage_log]
+        key = f"d{d}"
+        out[key + "_support"] = res.support.elems
+        out[key + "_coeffs"] = res.coeffs
+        out[key + "_count"] = np.array(res.sample_count)
+        out[key + "_log"] = np.array(log, dtype=object).astype(str)
+        out[key + "_gamma_digest"] = np.array(digest(gamma))
+        print(f"freqset d={d}: {dt:.1f}s, {len(res.support)} found")
+    # a hyperbolic cross (the reference's hc_enumerate builds it)
+    rng = np.random.default_rng(77)
+    G = rfs.hyperbolic_cross(4, 40)
+    gamma = np.ascontiguousarray(G.elems)
+    idx = np.sort(rng.choice(gamma.shape[0], size=16, replace=False))
+    sup = gamma[idx]
+    co = workloads.mag_phase_coeffs(16, rng)
+    p = rpe.SparsePoly(rfs.FreqSet(4, sup, _sorted=True), co)
+    res = rdim.sfft(_LatticeShimOracle(p, sup, co), G, rdim.SfftParams(16, 0.9, r=2), seed=5)
+    log = [[e["stage"], e["t"], e["i"], e["candidates"], e["kept"], e["samples"]]
+           for e in res.stage_log]
+    out["hc_gamma_digest"] = np.array(digest(gamma))
+    out["hc_support"] = res.support.elems
+    out["hc_coeffs"] = res.coeffs
+    out["hc_count"] = np.array(res.sample_count)
+    out["hc_log"] = np.array(log, dtype=object).astype(str)
+    print(f"hyperbolic cross d=4 N=40 (|Gamma| = {gamma.shape[0]}): {len(res.support)} found")
+    save_npz("sfft_freqset", **out)
+
+
 GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
        "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
        "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale,
-       "cfg4_full": gen_cfg4_full, "sfft_fullsize": gen_sfft_fullsize}
+       "cfg4_full": gen_cfg4_full, "sfft_fullsize": gen_sfft_fullsize,
+       "sfft_freqset": gen_sfft_freqset}
 SLOW = {"cfg4_full", "sfft_fullsize"}
 
 if __name__ == "__main__":

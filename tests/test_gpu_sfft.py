@@ -192,3 +192,37 @@ def test_sfft_freqset_gamma_vs_oracle(cuda, oracle_lib, d, N, n, s):
             for e in ref[3]]
     assert got == want
     assert workloads.rel_l2(res.coeffs, ref[1]) <= 1e-10
+    # and against the reference's own run of the same instance
+    g = golden("sfft_freqset.npz")
+    key = f"d{d}"
+    assert np.array_equal(res.support.elems, g[key + "_support"])
+    assert res.sample_count == int(g[key + "_count"])
+    flat = [[e["stage"], str(e["t"]), str(e["i"]), str(e["candidates"]), str(e["kept"]),
+             str(e["samples"])] for e in res.stage_log]
+    assert flat == g[key + "_log"].tolist()
+    assert workloads.rel_l2(res.coeffs, g[key + "_coeffs"]) <= 1e-10
+
+
+def test_sfft_hyperbolic_cross_vs_reference(cuda):
+    """sfft over a hyperbolic cross (hc_enumerate, freqset.py:222-245) against
+    the reference's own run: the candidate set, supports, sample counts,
+    stage logs and coefficients."""
+    import hashlib
+
+    pkg = cuda
+    g = golden("sfft_freqset.npz")
+    G = pkg.hyperbolic_cross(4, 40)
+    gamma = np.ascontiguousarray(G.elems)
+    assert hashlib.sha256(gamma.tobytes()).hexdigest()[:16] == str(g["hc_gamma_digest"])
+    rng = np.random.default_rng(77)
+    idx = np.sort(rng.choice(gamma.shape[0], size=16, replace=False))
+    sup = gamma[idx]
+    co = workloads.mag_phase_coeffs(16, rng)
+    p = pkg.SparsePoly(pkg.FreqSet(4, sup, _sorted=True), co)
+    res = pkg.sfft(pkg.oracle_from_poly(p), G, pkg.SfftParams(16, 0.9, r=2), seed=5)
+    assert np.array_equal(res.support.elems, g["hc_support"])
+    assert res.sample_count == int(g["hc_count"])
+    flat = [[e["stage"], str(e["t"]), str(e["i"]), str(e["candidates"]), str(e["kept"]),
+             str(e["samples"])] for e in res.stage_log]
+    assert flat == g["hc_log"].tolist()
+    assert workloads.rel_l2(res.coeffs, g["hc_coeffs"]) <= 1e-10

@@ -170,3 +170,24 @@ def test_sfft_fullsize_structured_vs_reference(oracle_lib, name):
     res = oracle_lib.sfft(orc, oracle_lib.Box(w.d, w.lo, w.hi), w.s, w.delta, w.seed,
                           theta=w.theta, r=w.r, workers=8)
     _check_sfft(res, g, 1e-12)
+
+
+@pytest.mark.parametrize("d,N,n,s", [(6, 16, 200_000, 30), (7, 12, 120_000, 20)])
+def test_sfft_freqset_gamma_vs_reference(oracle_lib, d, N, n, s):
+    """sfft over an explicit candidate set (FreqSet Gamma): the oracle against
+    the reference's own run (tests/golden/sfft_freqset.npz)."""
+    g = golden("sfft_freqset.npz")
+    key = f"d{d}"
+    rng = np.random.default_rng(1000 + d)
+    gamma = workloads.rows_from_box(d, -N, N, n, rng)
+    idx = np.sort(rng.choice(gamma.shape[0], size=s, replace=False))
+    sup = gamma[idx]
+    co = workloads.mag_phase_coeffs(s, rng)
+    res = oracle_lib.sfft(oracle_lib.PolyOracle(sup, co, mode="structured"), gamma, s, 0.9, 11,
+                          r=2)
+    assert np.array_equal(res[0], g[key + "_support"])
+    assert res[2] == int(g[key + "_count"])
+    flat = [[e["stage"], str(e["t"]), str(e["i"]), str(e["candidates"]), str(e["kept"]),
+             str(e["samples"])] for e in res[3]]
+    assert flat == g[key + "_log"].tolist()
+    assert workloads.rel_l2(res[1], g[key + "_coeffs"]) <= 1e-12
