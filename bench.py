@@ -564,16 +564,17 @@ def cpu_hash_bounded(rows_host, zmat, M, ghat, theta0, workers, budget_s=8.0):
 # ---------------------------------------------------------------------------
 
 def measured_traffic(kernel):
-    """DRAM bytes per launch from the committed ncu capture
-    (profiles/r01/traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                        "traffic.json")
-    try:
-        with open(path) as f:
-            ent = json.load(f)[kernel]
-        return ent
-    except (OSError, KeyError, ValueError):
-        return None
+    """DRAM bytes per launch from the newest committed ncu capture
+    (profiles/r02/traffic.json, else r01), or None."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", rnd,
+                            "traffic.json")
+        try:
+            with open(path) as f:
+                return json.load(f)[kernel]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def _pipe_peaks():
