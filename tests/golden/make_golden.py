@@ -627,13 +627,45 @@ def gen_sfft_freqset():
     save_npz("sfft_freqset", **out)
 
 
+def gen_fixed_noisy():
+    """Fixed-Gamma detection on noisy samples at 2 x 10^4 candidates: many false
+    detections, so detect_topk truncates and postprocess_r1l refines
+    crowded residues (reference detect.py:158-228, compiled gather)."""
+    rng = np.random.default_rng(4242)
+    d, N, n, s = 5, 20, 20_000, 40
+    gamma = workloads.rows_from_box(d, -N, N, n, rng)
+    G = rfs.FreqSet(d, gamma, _sorted=True)
+    idx = np.sort(rng.choice(n, size=s, replace=False))
+    co = workloads.mag_phase_coeffs(s, rng)
+    p = rpe.SparsePoly(rfs.FreqSet(d, gamma[idx], _sorted=True), co)
+    cfg = rlat.draw_config(G, s, 0.1, rng=rng)
+    oracle = rpe.oracle_from_poly(p)
+    samples = [oracle.sample_lattice(lat) + 0.3 * (rng.standard_normal(lat.M)
+                                                   + 1j * rng.standard_normal(lat.M))
+               for lat in cfg.lattices]
+    res = rdetect.detect_and_compute(samples, cfg, G)
+    topk = rdetect.detect_topk(samples, cfg, G, s, 0.5)
+    post = rdetect.postprocess_r1l(res, samples, cfg)
+    fr = rdetect.detect_frequencies(samples, cfg, G)
+    hits = np.ascontiguousarray(res.hits, dtype=np.int64)
+    print(f"fixed noisy: M={cfg.shared_M} L={len(cfg.lattices)} detected {len(res.detected_idx)}, "
+          f"top-s {len(topk.detected_idx)}, post {len(post.detected_idx)}")
+    save_npz("fixed_noisy", gamma_digest=np.array(digest(gamma)), support_idx=idx,
+             coeffs_true=co, M=np.array(cfg.shared_M),
+             zmat=np.vstack([lat.z for lat in cfg.lattices]), samples=np.array(samples),
+             hits_sha256=np.array(hashlib.sha256(hits.tobytes()).hexdigest()),
+             idx=res.detected_idx, coeffs=res.coeffs, theta0=np.array(res.theta_zero),
+             topk_idx=topk.detected_idx, topk_coeffs=topk.coeffs,
+             post_idx=post.detected_idx, post_coeffs=post.coeffs, freq_idx=fr.detected_idx)
+
+
 GEN = {"gather": gen_gather, "injective": gen_injective, "hc": gen_hc,
        "lattice": gen_lattice, "dft": gen_dft, "sampling": gen_sampling,
        "tiny_detect": gen_tiny_detect, "cfg1": gen_cfg1,
        "sfft_small": gen_sfft_small, "sfft_cfg2": gen_sfft_cfg2,
        "analysis": gen_analysis, "f10": gen_f10, "fullscale": gen_fullscale,
        "cfg4_full": gen_cfg4_full, "sfft_fullsize": gen_sfft_fullsize,
-       "sfft_freqset": gen_sfft_freqset}
+       "sfft_freqset": gen_sfft_freqset, "fixed_noisy": gen_fixed_noisy}
 SLOW = {"cfg4_full", "sfft_fullsize"}
 
 if __name__ == "__main__":

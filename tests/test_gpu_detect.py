@@ -317,3 +317,33 @@ def test_more_than_128_lattices_numpy_semantics(cuda, oracle_lib, L):
     res = pkg.detect_and_compute(samples, cfg, S)
     h2, _, _ = port.gather_mixed(samples, [M] * L, zmat, elems, res.theta_zero, 0.5, True)
     assert np.array_equal(res.hits, h2)
+
+
+def test_noisy_fixed_gamma_vs_reference(cuda):
+    """Noisy samples on 2 x 10^4 candidates (tests/golden/fixed_noisy.npz, the
+    reference's own run): every candidate detected, so detect_topk truncates
+    and postprocess_r1l refines crowded residues.  Hits bit-exact (sha256),
+    detected / kept indices exact, coefficients within 1e-10."""
+    import hashlib
+
+    pkg = cuda
+    g = golden("fixed_noisy.npz")
+    rng = np.random.default_rng(4242)
+    gamma = workloads.rows_from_box(5, -20, 20, 20_000, rng)
+    assert hashlib.sha256(np.ascontiguousarray(gamma).tobytes()).hexdigest()[:16] == \
+        str(g["gamma_digest"])
+    G = pkg.FreqSet(5, gamma, _sorted=True)
+    cfg = _config(pkg, g["zmat"], int(g["M"]))
+    smp = list(g["samples"])
+    res = pkg.detect_and_compute(smp, cfg, G)
+    assert hashlib.sha256(np.ascontiguousarray(res.hits, dtype=np.int64).tobytes()).hexdigest() \
+        == str(g["hits_sha256"])
+    assert np.array_equal(res.detected_idx, g["idx"])
+    assert np.max(np.abs(res.coeffs - g["coeffs"])) <= 1e-10 * np.max(np.abs(g["coeffs"]))
+    top = pkg.detect_topk(smp, cfg, G, 40, 0.5)
+    assert_topk_equivalent(top.detected_idx, g["topk_idx"], g["idx"], g["coeffs"])
+    post = pkg.postprocess_r1l(res, smp, cfg)
+    assert np.array_equal(post.detected_idx, g["post_idx"])
+    assert np.max(np.abs(post.coeffs - g["post_coeffs"])) <= 1e-10 * np.max(np.abs(g["post_coeffs"]))
+    fr = pkg.detect_frequencies(smp, cfg, G)
+    assert np.array_equal(fr.detected_idx, g["freq_idx"])

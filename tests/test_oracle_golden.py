@@ -191,3 +191,24 @@ def test_sfft_freqset_gamma_vs_reference(oracle_lib, d, N, n, s):
              str(e["samples"])] for e in res[3]]
     assert flat == g[key + "_log"].tolist()
     assert workloads.rel_l2(res[1], g[key + "_coeffs"]) <= 1e-12
+
+
+def test_fixed_noisy_vs_reference(oracle_lib):
+    """The oracle on the reference's noisy fixed-Gamma run (every candidate
+    detected; top-s truncation; R1L refinement on crowded residues)."""
+    import hashlib
+
+    g = golden("fixed_noisy.npz")
+    rng = np.random.default_rng(4242)
+    gamma = workloads.rows_from_box(5, -20, 20, 20_000, rng)
+    M, z, smp = int(g["M"]), g["zmat"], list(g["samples"])
+    hits, idx, co, th = oracle_lib.detect_and_compute(smp, M, z, gamma)
+    assert hashlib.sha256(np.ascontiguousarray(hits).tobytes()).hexdigest() == \
+        str(g["hits_sha256"])
+    assert np.array_equal(idx, g["idx"]) and np.array_equal(co, g["coeffs"])
+    assert th == float(g["theta0"])
+    _, ti, tc, _ = oracle_lib.detect_topk(smp, M, z, gamma, 40, 0.5)
+    assert np.array_equal(ti, g["topk_idx"]) and np.array_equal(tc, g["topk_coeffs"])
+    pi, pc = oracle_lib.postprocess_r1l(gamma[idx], co, idx, smp, M, z, th)
+    assert np.array_equal(pi, g["post_idx"])
+    assert np.max(np.abs(pc - g["post_coeffs"])) <= 1e-13 * np.max(np.abs(g["post_coeffs"]))
