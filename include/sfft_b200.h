@@ -288,6 +288,20 @@ int sfftb_step1_select(const double *est, int64_t nlines, int64_t K,
                        const int64_t *vals, int64_t nv, int64_t r, int64_t s_local,
                        double theta, int32_t *present, int64_t *kept, void *stream);
 
+/* detect_frequencies / detect_and_compute (detect.py:149-169) on device
+ * buffers in one call: samples (L, M) complex128, rows (n, d) int64, zmat
+ * (L, d).  theta_in: device theta0, or NULL for the default zero test
+ * (detect.py:42-53).  Outputs: hits (n), idx (n) ascending with counts[0]
+ * entries, coeffs (n) medians of the detected rows when want_medians,
+ * theta_out (1), bad (1) = 1 when the samples hold NaN or Inf (detect.py:
+ * 98-109; the caller raises).  ws: sfftb_detect_dev_workspace_bytes(L, M, n). */
+int64_t sfftb_detect_dev_workspace_bytes(int64_t L, int64_t M, int64_t n);
+int sfftb_detect_dev(const double *samples, int64_t L, int64_t M, const int64_t *rows,
+                     int64_t n, int64_t d, const int64_t *zmat, const double *theta_in,
+                     int64_t kbound, int64_t min_hits, int want_medians, int64_t *hits,
+                     int64_t *idx, int64_t *counts, double *coeffs, double *theta_out,
+                     int32_t *bad, void *ws, void *stream);
+
 /* Set mask bit i for every listed index (group union, dimincr.py:239-240). */
 int sfftb_mark_indices(const int64_t *idx, const int64_t *counts, int64_t G,
                        int64_t cap, uint32_t *mask, int64_t n, void *stream);

@@ -88,6 +88,9 @@ _SIGS = {
     "sfftb_postprocess_r1l": (_int, [_p, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _dbl, _p, _p,
                                      _p, _p]),
     "sfftb_compact_mask_cap": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
+    "sfftb_detect_dev_workspace_bytes": (_i64, [_i64, _i64, _i64]),
+    "sfftb_detect_dev": (_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i64, _i64, _int, _p, _p,
+                                _p, _p, _p, _p, _p, _p]),
     "sfftb_step1_select": (_int, [_p, _i64, _i64, _p, _i64, _i64, _i64, _dbl, _p, _p, _p]),
     "sfftb_rows_in_sorted": (_int, [_p, _i64, _i64, _p, _i64, _p, _p]),
     "sfftb_alias_classify": (_int, [_p, _p, _p, _i64, _i64, _p, _dbl, _p, _p, _p]),

@@ -115,7 +115,7 @@ class DetectionResult:
 
 # ---------------------------------------------------------------------------
 
-def _stack_samples(samples, config, deferred=False):
+def _stack_samples(samples, config, deferred=False, check=True):
     """Validated (L, M) complex128 CUDA tensor (detect.py:98-109 checks).
     With ``deferred`` the finiteness check is returned as a device flag
     instead of being read here: (tensor, flag or None)."""
@@ -142,7 +142,7 @@ def _stack_samples(samples, config, deferred=False):
             return (t, None) if deferred else t
         t = _dev.upload(np.vstack(rows))
     if deferred:
-        return t, torch.isfinite(torch.view_as_real(t)).all()
+        return t, (torch.isfinite(torch.view_as_real(t)).all() if check else None)
     if not bool(torch.isfinite(torch.view_as_real(t)).all()):
         raise ParameterError("samples contain NaN or Inf")
     return t
@@ -299,24 +299,33 @@ def _detect_async(samples, config, gamma, zero, want_medians):
     host = gamma._host if gamma._dev is None else None
     if host is not None and host.nbytes >= STREAM_UPLOAD_BYTES:
         return None
-    t, fin = _stack_samples(samples, config, deferred=True)
+    t = _stack_samples(samples, config, deferred=True, check=False)[0]
     if not gamma.dim * (M - 1) ** 2 < 2**62:
         raise ParameterError("lattice size too large for int64 residues")
     if config.dim != gamma.dim:
         raise ParameterError("candidate set/lattice dimension mismatch")
-    L = config.L
-    theta = _engine.zero_thresholds(t, 1, L, M) if zero is None else \
-        _theta_tensor(zero.theta_zero)
-    b = _engine.detect_batch(t, M, config.zmat_device(), 1, L, gamma.device(), _kbound(gamma),
-                             config.nu, theta0=theta, want_medians=want_medians, want_hits=True)
-    small = torch.stack([fin.to(torch.float64), theta.reshape(-1)[0],
-                         b.counts.reshape(-1)[0].to(torch.float64)])
-    f, th, cnt = _dev.download(small).tolist()
-    if f != 1.0:
+    L, n, d = config.L, len(gamma), gamma.dim
+    rows = gamma.device()
+    lib = _native.lib()
+    ws = _dev.workspace(lib.sfftb_detect_dev_workspace_bytes(L, M, n))
+    hits = _dev.empty((max(n, 1),), torch.int64)
+    idx = _dev.empty((max(n, 1),), torch.int64)
+    coeffs = _dev.empty((max(n, 1),), torch.complex128) if want_medians else None
+    small = _dev.empty((3,), torch.int64)  # count | theta0 (f64) | non-finite flag (i32)
+    theta_in = None if zero is None else _theta_tensor(zero.theta_zero)
+    # the whole chain in one C call (csrc/detect_dev.cu), one read-back
+    _native.call("sfftb_detect_dev", _dev.ptr(t), L, M, _dev.ptr(rows), n, d,
+                 _dev.ptr(config.zmat_device()), _dev.ptr(theta_in), int(_kbound(gamma)),
+                 _engine.min_hits_for(config.nu, L), int(bool(want_medians)), _dev.ptr(hits),
+                 _dev.ptr(idx), small.data_ptr(), _dev.ptr(coeffs), small[1:].data_ptr(),
+                 small[2:].data_ptr(), _dev.ptr(ws), _dev.stream())
+    host = _dev.download(small)
+    if int(host[2]) & 0xFFFFFFFF:
         raise ParameterError("samples contain NaN or Inf")
-    cnt = int(cnt)
-    coeffs = b.coeffs[:cnt] if want_medians else None
-    return DetectionResult(gamma, b.hits, b.idx[:cnt], coeffs, th)
+    cnt = int(host[0])
+    th = float(host[1:2].view(np.float64)[0])
+    return DetectionResult(gamma, hits[:n], idx[:cnt],
+                           coeffs[:cnt] if want_medians else None, th)
 
 
 def detect_frequencies(samples, config, gamma, zero=None):
