@@ -176,6 +176,10 @@ int sfftb_hash_hits(const int64_t *elems, int64_t n, int64_t d,
  * reset (reset != 0 zeroes the counter); synchronous, for tests. */
 int64_t sfftb_hash_tc_recomputed(int reset);
 
+/* The same counter of the rolling tensor-core kernel (csrc/hash_roll.cu): rows
+ * with a coordinate outside [-2^13, 2^13) that took its exact 64-bit path. */
+int64_t sfftb_hash_roll_recomputed(int reset);
+
 /*
  * Ascending indices of set bits per group: idx[g*n + k], counts[g].
  * ws: sfftb_compact_workspace_bytes(G, n).

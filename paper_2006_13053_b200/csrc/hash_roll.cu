@@ -1,0 +1,716 @@
+// K3 on the tensor cores, second design ("rolling" kernel): candidate residues
+// k . z mod M as an exact u8 x u8 -> s32 GEMM whose A operand (the candidate
+// rows) lives in TENSOR MEMORY, and the per-lattice nonzero bitmaps streamed
+// through shared memory in lattice groups while ~6000 rows stay resident.
+// Same semantics as hash_rows (hash.cu): the reference's per-candidate loop of
+// _core.pyx:185-197 (residue, |ghat| > theta probe, hits >= nu*L).
+//
+// Why this shape.  The CUDA-core kernel spends 10 IMADs per (row, lattice) on
+// the dot product (IMAD-pipe floor 2.08 ms at config 4) and re-streams the
+// 607 KB of bitmaps per 2048-row tile (L2 -> SM ingress).  Here
+//  * a row is packed ONCE into 2d+2 bytes (u = k + 2^13 = a + 128 b, limbs a, b
+//    < 128, a constant 1 and an out-of-range flag) and stored by its loader
+//    thread into TMEM (tcgen05.st): 8 columns hold a 128-row tile, 50 tiles
+//    (6400 rows) stay resident in 400 of the 512 columns;
+//  * one tcgen05.mma (kind::i8, A from TMEM, B = the base-256 limbs of the
+//    per-lattice coefficients z_j 128^p mod M in shared memory) gives, for a
+//    128-row tile and a group of 5 lattices, three s32 partial sums per (row,
+//    lattice): x = v0 + 256 v1 + 65536 v2 == k.z (mod M), x < 2^32;
+//  * the epilogue reduces x with ONE multiply-high (q = umulhi(x, 2^32/M) is
+//    floor(x/M) or one less, so x - qM < M + ext with ext = ceil(M x_max /
+//    2^32)) and probes a bitmap whose first ext bits are repeated after bit
+//    M, built in shared memory after the bulk copy lands;
+//  * bitmaps arrive by 1-D bulk copies, one group (5 lattices) per step,
+//    double buffered; a step applies its group to every resident tile.  Tiles
+//    are organised in NG cohorts (NG = groups per pass): at step s the cohort
+//    s mod NG is reborn with fresh rows and every cohort sees the groups in
+//    rotated order, so loading, hashing and retiring all overlap and each
+//    group of bitmaps is brought in once per ~6400 rows instead of once per
+//    2048.
+//
+// Warp roles (832 threads, one CTA per SM): warp 0 bitmap producer (+ TMEM
+// allocation), warp 1 MMA issuer, warps 2-9 row loaders (two per TMEM lane
+// quadrant), warps 10-25 epilogue (four groups of four quadrant warps).
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace sfftb {
+
+namespace roll {
+
+constexpr int kThreads = 832;
+constexpr int kTile = 128;
+constexpr int kLG = 5;          // lattices per group (15 of the 16 MMA columns)
+constexpr int kNC = 16;         // MMA N
+constexpr int kACols = 8;       // TMEM columns of one A tile (K = 32 bytes)
+constexpr int kMaxTA = 56;      // resident tiles
+constexpr int kMaxND = 16;      // accumulator buffers
+constexpr int kMinND = 4;
+constexpr int kLoaders = 8;
+constexpr int kEpiWarp0 = 2 + kLoaders;
+constexpr int64_t kOffset = 8192;  // u = k + kOffset must lie in [0, 2^14)
+
+struct Args {
+    const int64_t* elems;
+    int64_t n;
+    const int64_t* zmat;  // (L, d)
+    int L, NG, SP, TA, ND;
+    uint32_t M, negM, magic;
+    const uint32_t* bits;  // (L, W)
+    int W;                 // words per lattice in global memory
+    int ext_words;         // words rewritten/appended from word M >> 5 on
+    uint32_t S2;           // shared-memory stride per lattice bitmap (power of two)
+    int64_t ntiles;
+    int64_t min_hits;
+    int64_t* hits64;   // may be null
+    uint32_t* detmask;
+    unsigned long long* recomputed;
+    int32_t* dbg;  // diagnostics: the 128 x 16 accumulators of tile 0, step 0
+};
+
+// ---- PTX helpers (shared-window addresses) ----
+__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32_t bytes,
+                                           uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t desc = 0;
+    desc |= (uint64_t)((addr >> 4) & 0x3FFF);
+    desc |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    desc |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    desc |= (uint64_t)1 << 46;
+    return desc;
+}
+// D[tmem] = A[tmem] * B[smem], u8 x u8 -> s32, no accumulate
+__device__ __forceinline__ void umma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                           uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+                 : "=r"(p));
+    return p != 0;
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Exact hits of one row from global memory (a coordinate outside the limb range).
+__device__ int exact_row_hits(const Args& a, int d, int64_t row) {
+    int h = 0;
+    for (int l = 0; l < a.L; ++l) {
+        uint64_t acc = 0;
+        for (int j = 0; j < d; ++j) {
+            int64_t e = a.elems[row * d + j] % (int64_t)a.M;
+            if (e < 0) e += a.M;
+            int64_t z = a.zmat[(int64_t)l * d + j] % (int64_t)a.M;
+            if (z < 0) z += a.M;
+            acc = (acc + (uint64_t)e * (uint64_t)z) % a.M;
+        }
+        const uint32_t r = (uint32_t)acc;
+        h += (a.bits[(int64_t)l * a.W + (r >> 5)] >> (r & 31)) & 1u;
+    }
+    return h;
+}
+
+// Shared-memory map: byte offsets from the dynamic base (the two bitmap ring
+// slots follow at the next S2-aligned address).
+struct Smem {
+    uint32_t bm_raw, bm_full, bm_empty, d_full, d_empty, a_full, a_empty, tmem_holder;
+    uint32_t bop, hits, stage, end;
+};
+__host__ __device__ inline Smem smem_map(int NG, int TA, int RS) {
+    Smem s;
+    uint32_t o = 0;
+    s.bm_raw = o;   o += 16;
+    s.bm_full = o;  o += 16;
+    s.bm_empty = o; o += 16;
+    s.d_full = o;   o += 8u * kMaxND;
+    s.d_empty = o;  o += 8u * kMaxND;
+    s.a_full = o;   o += 8u * kMaxTA;
+    s.a_empty = o;  o += 8u * kMaxTA * 4;
+    s.tmem_holder = o; o += 16;
+    o = (o + 127u) & ~127u;
+    s.bop = o;      o += (uint32_t)NG * 512u;           // B operand: NG x [2][16][16 B]
+    s.hits = o;     o += (uint32_t)TA * kTile;          // u8 running hit counts
+    o = (o + 15u) & ~15u;
+    s.stage = o;    o += (uint32_t)kLoaders * 32u * RS * 4u;  // loader transposition
+    s.end = (o + 15u) & ~15u;
+    return s;
+}
+
+// One step's canonical item order, shared by the MMA issuer and the epilogue:
+// cohorts from the oldest (age NG-1, retiring) to the newborn (age 0).
+#define ROLL_FOR_ITEMS(s_, ...)                                                       \
+    for (int age = a.NG - 1; age >= 0; --age) {                                       \
+        const int64_t b = (int64_t)(s_) - age;                                        \
+        if (b < 0 || b >= nb) continue;                                               \
+        const int c = (int)(b % a.NG);                                                \
+        for (int k = 0; k < a.SP; ++k) {                                              \
+            const int64_t j = b * a.SP + k;                                           \
+            if (j >= my_tiles) break;                                                 \
+            const int slot = c * a.SP + k;                                            \
+            __VA_ARGS__                                                               \
+            if (++buf == a.ND) {                                                      \
+                buf = 0;                                                              \
+                ++round;                                                              \
+            }                                                                         \
+        }                                                                             \
+    }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    constexpr int H = D / 2;        // 16-byte chunks (coordinate pairs) per row
+    constexpr int RS = H | 1;       // odd row stride of the transposition buffer
+    const uint32_t raw = smem_addr(smem_raw);
+    const Smem S = smem_map(a.NG, a.TA, RS);
+    const uint32_t ring0 = (raw + S.end + a.S2 - 1u) & ~(a.S2 - 1u);
+    const uint32_t ring_bytes = (uint32_t)kLG * a.S2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t cta = blockIdx.x, ncta = gridDim.x;
+    const int64_t my_tiles = a.ntiles > cta ? (a.ntiles - 1 - cta) / ncta + 1 : 0;
+    const int64_t nb = (my_tiles + a.SP - 1) / a.SP;             // births
+    const int64_t nsteps = nb > 0 ? nb + a.NG - 1 : 0;
+    const int dcol0 = a.TA * kACols;
+
+    // ---- setup ----
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            bar_init(raw + S.bm_raw + 8u * i, 1);
+            bar_init(raw + S.bm_full + 8u * i, 1);
+            bar_init(raw + S.bm_empty + 8u * i, 16);
+        }
+        for (int i = 0; i < a.ND; ++i) {
+            bar_init(raw + S.d_full + 8u * i, 1);
+            bar_init(raw + S.d_empty + 8u * i, 4);
+        }
+        for (int i = 0; i < a.TA; ++i) {
+            bar_init(raw + S.a_full + 8u * i, 4);
+            for (int q = 0; q < 4; ++q) bar_init(raw + S.a_empty + 8u * (i * 4 + q), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         raw + S.tmem_holder)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // B operand of group g: [2 K-chunks][16 columns][16 B]; column 3i + limb
+    // for lattice g*kLG + i, column 15 = the out-of-range flag.  K bytes:
+    // 4p + e = coordinate 2p + (e >> 1), limb weight (e & 1) ? 128 : 1;
+    // 2D = the constant (k = u - kOffset); 2D + 1 = the flag.
+    for (uint32_t e4 = threadIdx.x; e4 < (uint32_t)a.NG * 128u; e4 += blockDim.x) {
+        uint32_t word = 0;
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t idx = e4 * 4 + t;
+            const int g = (int)(idx / 512u);
+            const uint32_t in = idx % 512u;
+            const int col = (int)((in / 16u) % 16u);
+            const int kb = (int)(in / 256u) * 16 + (int)(in % 16u);
+            uint32_t v = 0;
+            const int i = col / 3, limb = col % 3;
+            const int l = g * kLG + i;
+            if (col < 3 * kLG && l < a.L) {
+                uint64_t c = 0;
+                bool have = false;
+                if (kb < 2 * D) {
+                    int64_t z = a.zmat[(int64_t)l * D + (kb >> 1)] % (int64_t)a.M;
+                    if (z < 0) z += a.M;
+                    c = ((uint64_t)z * ((kb & 1) ? 128u : 1u)) % a.M;
+                    have = true;
+                } else if (kb == 2 * D) {
+                    uint64_t zs = 0;
+                    for (int j = 0; j < D; ++j) {
+                        int64_t z = a.zmat[(int64_t)l * D + j] % (int64_t)a.M;
+                        if (z < 0) z += a.M;
+                        zs += (uint64_t)z;
+                    }
+                    const uint64_t t2 = ((zs % a.M) * (uint64_t)(kOffset % (int64_t)a.M)) % a.M;
+                    c = (a.M - t2) % a.M;
+                    have = true;
+                }
+                if (have) v = (uint32_t)(c >> (8 * limb)) & 255u;
+            } else if (col == 15 && kb == 2 * D + 1) {
+                v = 1u;
+            }
+            word |= v << (8 * t);
+        }
+        *reinterpret_cast<uint32_t*>(smem_raw + S.bop + e4 * 4) = word;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + S.tmem_holder);
+
+    if (warp == 0) {
+        // ================= bitmap producer =================
+        const uint32_t wbytes = (uint32_t)a.W * 4u;
+        const int wM = (int)(a.M >> 5), sh = (int)(a.M & 31u);
+        auto issue = [&](int64_t s) {
+            const int ring = (int)(s & 1);
+            const int l0 = (int)(s % a.NG) * kLG;
+            const int cnt = min(a.L, l0 + kLG) - l0;
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t bar = raw + S.bm_raw + 8u * ring;
+                bar_expect_tx(bar, wbytes * (uint32_t)cnt);
+                for (int i = 0; i < cnt; ++i)
+                    bulk_g2s_a(ring0 + (uint32_t)ring * ring_bytes + (uint32_t)i * a.S2,
+                               a.bits + (int64_t)(l0 + i) * a.W, wbytes, bar);
+            }
+        };
+        // bits [M, M + 32 ext_words) := bits [0, 32 ext_words) of every lattice
+        auto extend = [&](int64_t s) {
+            const int ring = (int)(s & 1);
+            const int l0 = (int)(s % a.NG) * kLG;
+            const int cnt = min(a.L, l0 + kLG) - l0;
+            bar_wait(raw + S.bm_raw + 8u * ring, (uint32_t)((s >> 1) & 1));
+            uint32_t* base = reinterpret_cast<uint32_t*>(smem_raw + (ring0 - raw) +
+                                                         (uint32_t)ring * ring_bytes);
+            const int per = a.ext_words + 1;
+            for (int e = lane; e < cnt * per; e += 32) {
+                uint32_t* bm = base + (size_t)(e / per) * (a.S2 / 4);
+                const int w = e % per;
+                uint32_t v;
+                if (sh == 0) {
+                    v = w < a.ext_words ? bm[w] : 0u;
+                } else {
+                    const uint32_t lo = w == 0 ? (bm[wM] & ((1u << sh) - 1u)) : (bm[w - 1] >> (32 - sh));
+                    const uint32_t hi = w < a.ext_words ? (bm[w] << sh) : 0u;
+                    v = lo | hi;
+                }
+                bm[wM + w] = v;
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(raw + S.bm_full + 8u * ring);
+        };
+        if (nsteps > 0) issue(0);
+        if (nsteps > 1) issue(1);
+        if (nsteps > 0) extend(0);
+        for (int64_t s = 0; s < nsteps; ++s) {
+            if (s + 1 < nsteps) extend(s + 1);
+            if (s + 2 < nsteps) {
+                bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1), (uint32_t)((s >> 1) & 1));
+                issue(s + 2);
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        const bool leader = elect_one();
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
+        int buf = 0;
+        int64_t round = 0;
+        for (int64_t s = 0; s < nsteps; ++s) {
+            const uint64_t bdesc =
+                umma_desc(raw + S.bop + (uint32_t)(s % a.NG) * 512u, 256u, 128u);
+            ROLL_FOR_ITEMS(s, {
+                if (round >= 1)
+                    bar_wait(raw + S.d_empty + 8u * buf, (uint32_t)((round - 1) & 1));
+                if (age == 0)
+                    bar_wait(raw + S.a_full + 8u * slot, (uint32_t)((b / a.NG) & 1));
+                tc_fence_after();
+                if (leader) {
+                    umma_i8_ts(tmem + (uint32_t)(dcol0 + kNC * buf),
+                               tmem + (uint32_t)(slot * kACols), bdesc, idesc);
+                    umma_commit(raw + S.d_full + 8u * buf);
+                }
+                __syncwarp();
+            })
+        }
+    } else if (warp < kEpiWarp0) {
+        // ================= row loaders =================
+        const int q = warp & 3;              // TMEM lane quadrant of this warp
+        const int hsel = (warp - 2) >> 2;    // tiles k = hsel (mod 2) of every birth
+        uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + S.stage) + (warp - 2) * 32 * RS;
+        const int4* gbase = reinterpret_cast<const int4*>(a.elems);
+        // item = (birth b, tile k); rows [t*128 + q*32, +32) of tile t = cta + (b*SP + k)*ncta
+        auto item_rows = [&](int64_t b, int k) -> int64_t {
+            return ((cta + (b * a.SP + k) * ncta) * kTile + q * 32);
+        };
+        auto valid_item = [&](int64_t b, int k) -> bool {
+            return b < nb && (b * a.SP + k) < my_tiles;
+        };
+        auto advance = [&](int64_t& b, int& k) {
+            k += 2;
+            if (k >= a.SP) {
+                k = hsel;
+                ++b;
+            }
+        };
+        auto load = [&](int4 (&rawv)[H], int64_t b, int k) {
+            const int64_t r0 = item_rows(b, k);
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const int ch = lane + 32 * i;
+                const int64_t row = r0 + ch / H;
+                rawv[i] = row < a.n ? __ldg(gbase + r0 * H + ch) : make_int4(0, 0, 0, 0);
+            }
+        };
+        auto prefetch = [&](int64_t b, int k) {
+            const char* p = reinterpret_cast<const char*>(a.elems) + item_rows(b, k) * (8 * D);
+            if (lane * 128 < 32 * 8 * D && item_rows(b, k) + 32 <= a.n) prefetch_l2(p + lane * 128);
+        };
+        int64_t b = 0;
+        int k = hsel;
+        if (k >= a.SP) b = nb;  // SP == 1: the second loader of each quadrant idles
+        int4 cur[H], nxt[H];
+        if (valid_item(b, k)) load(cur, b, k);
+        {
+            int64_t pb = b;
+            int pk = k;
+            for (int i = 0; i < 3; ++i) {
+                advance(pb, pk);
+                if (valid_item(pb, pk)) prefetch(pb, pk);
+            }
+        }
+        while (valid_item(b, k)) {
+            int64_t b2 = b;
+            int k2 = k;
+            advance(b2, k2);
+            const bool more = valid_item(b2, k2);
+            if (more) load(nxt, b2, k2);
+            {
+                int64_t pb = b2;
+                int pk = k2;
+                advance(pb, pk);
+                advance(pb, pk);
+                advance(pb, pk);
+                if (valid_item(pb, pk)) prefetch(pb, pk);
+            }
+            // pack: one 32-bit word per coordinate pair
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const int ch = lane + 32 * i;
+                const uint64_t u0 =
+                    (uint64_t)(((int64_t)(uint32_t)cur[i].x | ((int64_t)cur[i].y << 32)) + kOffset);
+                const uint64_t u1 =
+                    (uint64_t)(((int64_t)(uint32_t)cur[i].z | ((int64_t)cur[i].w << 32)) + kOffset);
+                const uint32_t l0 = (uint32_t)u0, l1 = (uint32_t)u1;
+                uint32_t w = (l0 & 127u) | (((l0 >> 7) & 127u) << 8) | ((l1 & 127u) << 16) |
+                             (((l1 >> 7) & 127u) << 24);
+                if ((u0 | u1) >> 14) w |= 0x80u;
+                stg[(ch / H) * RS + (ch % H)] = w;
+            }
+            __syncwarp();
+            uint32_t r[8];
+            uint32_t bad = 0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                if (p < H) {
+                    const uint32_t w = stg[lane * RS + p];
+                    bad |= w & 0x80u;
+                    r[p] = w & ~0x80u;
+                } else {
+                    r[p] = 0u;
+                }
+            }
+            // K = 2D: the constant 1; K = 2D + 1: the flag
+            if (H < 8) r[H] = 1u | (bad ? 0x100u : 0u);
+            __syncwarp();
+            const int slot = (int)(b % a.NG) * a.SP + k;
+            const int64_t beta = b / a.NG;
+            if (beta >= 1)
+                bar_wait(raw + S.a_empty + 8u * (slot * 4 + q), (uint32_t)((beta - 1) & 1));
+            tc_fence_after();
+            tmem_st8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(slot * kACols), r);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(raw + S.a_full + 8u * slot);
+            b = b2;
+            k = k2;
+            if (more) {
+#pragma unroll
+                for (int i = 0; i < H; ++i) cur[i] = nxt[i];
+            }
+        }
+    } else {
+        // ================= epilogue =================
+        const int ew = warp - kEpiWarp0;
+        const int grp = ew >> 2;
+        const int q = warp & 3;
+        const uint32_t M = a.M, negM = a.negM, magic = a.magic;
+        uint8_t* hs = smem_raw + S.hits;
+        int buf = 0;
+        int64_t round = 0;
+        for (int64_t s = 0; s < nsteps; ++s) {
+            const int ring = (int)(s & 1);
+            const int l0 = (int)(s % a.NG) * kLG;
+            const int lcg = min(a.L, l0 + kLG) - l0;
+            uint32_t lb[kLG];
+#pragma unroll
+            for (int i = 0; i < kLG; ++i)
+                lb[i] = ring0 + (uint32_t)ring * ring_bytes + (uint32_t)i * a.S2;
+            bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1));
+            ROLL_FOR_ITEMS(s, {
+                if (((c + k) & 3) == grp) {
+                    bar_wait(raw + S.d_full + 8u * buf, (uint32_t)(round & 1));
+                    tc_fence_after();
+                    uint32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * buf), v);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
+                    if (a.dbg && s == 0 && j == 0 && cta == 0) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
+                    }
+                    uint32_t bacc = 0;
+#pragma unroll
+                    for (int i = 0; i < kLG; ++i) {
+                        if (i < lcg) {
+                            uint32_t x = (v[3 * i + 1] << 8) + v[3 * i];
+                            x = (v[3 * i + 2] << 16) + x;
+                            const uint32_t qq = __umulhi(x, magic);
+                            uint32_t r;
+                            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(qq), "r"(negM), "r"(x));
+                            uint32_t w;
+                            asm volatile("{\n\t.reg .u32 t;\n\t"
+                                         "shr.u32 t, %1, 3;\n\t"
+                                         "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
+                                         "ld.shared.u32 %0, [t];\n\t}"
+                                         : "=r"(w)
+                                         : "r"(r), "r"(lb[i]));
+                            bacc = __funnelshift_r(bacc, __funnelshift_r(w, w, r), 1);
+                        }
+                    }
+                    const int hidx = slot * kTile + q * 32 + lane;
+                    uint32_t h = __popc(bacc);
+                    if (age != 0) h += hs[hidx];
+                    if (age == a.NG - 1) {
+                        const int64_t t = cta + j * ncta;
+                        const int64_t row0 = t * kTile + q * 32;
+                        const int64_t row = row0 + lane;
+                        const bool valid = row < a.n;
+                        int64_t hits = (int64_t)h;
+                        if (v[15] != 0u && valid) {
+                            hits = exact_row_hits(a, D, row);
+                            atomicAdd(a.recomputed, 1ull);
+                        }
+                        const unsigned det =
+                            __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
+                        if (valid && a.hits64) a.hits64[row] = hits;
+                        if (lane == 0 && row0 < a.n) a.detmask[row0 >> 5] = det;
+                        if (lane == 0) bar_arrive(raw + S.a_empty + 8u * (slot * 4 + q));
+                    } else {
+                        hs[hidx] = (uint8_t)h;
+                    }
+                }
+            })
+            __syncwarp();
+            if (lane == 0) bar_arrive(raw + S.bm_empty + 8u * ring);
+        }
+        (void)M;
+    }
+
+    // ---- teardown ----
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
+static unsigned long long* recomputed_counter() {
+    static unsigned long long* p = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaMalloc(&p, sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(p, 0, sizeof(unsigned long long));
+        else
+            p = nullptr;
+    });
+    return p;
+}
+
+template <int D>
+static int launch_d(Args& a, uint32_t smem, int grid, cudaStream_t st) {
+    auto kern = hash_roll_kernel<D>;
+    SFFTB_CUDA(smem_opt_in(kern, smem));
+    kern<<<grid, kThreads, smem, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+}  // namespace roll
+
+// Returns 1 when the rolling tensor-core kernel handled the call, 0 when the
+// shape is outside it (the caller takes the other kernels), < 0 = -status.
+int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat, int64_t L,
+                   int64_t M, const uint32_t* bits, int64_t min_hits, int64_t* hits64,
+                   uint32_t* detmask, cudaStream_t st) {
+    using namespace roll;
+    {
+        const char* e = getenv("SFFTB_HASH_ROLL");
+        if (!e || e[0] != '1') return 0;
+    }
+    const char* mr = getenv("SFFTB_HASH_ROLL_MINROWS");
+    const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 18;
+    if (n < min_rows || n > ((int64_t)1 << 40) || L < 1 || L > 255 || M < 64 ||
+        M >= ((int64_t)1 << 24))
+        return 0;
+    if (d != 4 && d != 6 && d != 8 && d != 10 && d != 12 && d != 14) return 0;
+    if (((uintptr_t)elems & 15) != 0 || ((uintptr_t)bits & 15) != 0) return 0;
+    // x = sum of 2d limb products + the constant, must stay below 2^32
+    const __int128 xmax = ((__int128)(2 * d) * 127 + 1) * (M - 1);
+    if (xmax >= ((__int128)1 << 32)) return 0;
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    // q = umulhi(x, floor(2^32/M)) >= floor(x/M) - 1, and is one short only
+    // when x mod M < M x / 2^32: residues land in [0, M + ext)
+    const int64_t ext = (int64_t)(((__int128)M * xmax) >> 32) + 2;
+    const int64_t ext_words = (ext + 31) / 32 + 1;
+    if (ext_words >= (M >> 5)) return 0;
+    const int64_t need_words = (M >> 5) + ext_words + 2;
+    uint32_t S2 = 64;
+    while ((int64_t)S2 < std::max(need_words, W) * 4) S2 <<= 1;
+    const int NG = (int)((L + kLG - 1) / kLG);
+    int SP = (512 - kMinND * kNC) / kACols / NG;
+    if (SP < 1) return 0;
+    SP = std::min(SP, 8);
+    const int TA = NG * SP;
+    const int ND = std::min(kMaxND, (512 - TA * kACols) / kNC);
+    const int RS = (int)(d / 2) | 1;
+    const Smem S = smem_map(NG, TA, RS);
+    const uint32_t smem = S.end + S2 + 2u * kLG * S2;
+    static int prop_smem = 0;
+    if (prop_smem == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&prop_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (prop_smem <= 0) prop_smem = 232448;
+    }
+    if (smem > (uint32_t)prop_smem) return 0;
+    unsigned long long* rec = recomputed_counter();
+    if (!rec) return 0;
+
+    Args a;
+    a.elems = elems;
+    a.n = n;
+    a.zmat = zmat;
+    a.L = (int)L;
+    a.NG = NG;
+    a.SP = SP;
+    a.TA = TA;
+    a.ND = ND;
+    a.M = (uint32_t)M;
+    a.negM = 0u - (uint32_t)M;
+    a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
+    a.bits = bits;
+    a.W = (int)W;
+    a.ext_words = (int)ext_words;
+    a.S2 = S2;
+    a.ntiles = (n + kTile - 1) / kTile;
+    a.min_hits = min_hits;
+    a.hits64 = hits64;
+    a.detmask = detmask;
+    a.recomputed = rec;
+    a.dbg = nullptr;
+    static int32_t* dbg = nullptr;
+    if (getenv("SFFTB_HASH_ROLL_DUMP")) {
+        if (!dbg) SFFTB_CUDA(cudaMalloc(&dbg, 128 * 16 * sizeof(int32_t)));
+        SFFTB_CUDA(cudaMemsetAsync(dbg, 0xFF, 128 * 16 * sizeof(int32_t), st));
+        a.dbg = dbg;
+    }
+    int grid = num_sms();
+    if (const char* e = getenv("SFFTB_HASH_ROLL_GRID")) grid = std::max(1, atoi(e));
+    grid = (int)std::min<int64_t>(grid, a.ntiles);
+    if (getenv("SFFTB_HASH_ROLL_DEBUG"))
+        fprintf(stderr, "hash_roll: d=%d L=%d NG=%d SP=%d TA=%d ND=%d S2=%u ext_words=%d smem=%u grid=%d\n",
+                (int)d, (int)L, NG, SP, TA, ND, S2, (int)ext_words, smem, grid);
+    int rc = SFFTB_EINVAL;
+    switch (d) {
+        case 4: rc = launch_d<4>(a, smem, grid, st); break;
+        case 6: rc = launch_d<6>(a, smem, grid, st); break;
+        case 8: rc = launch_d<8>(a, smem, grid, st); break;
+        case 10: rc = launch_d<10>(a, smem, grid, st); break;
+        case 12: rc = launch_d<12>(a, smem, grid, st); break;
+        case 14: rc = launch_d<14>(a, smem, grid, st); break;
+    }
+    if (a.dbg && rc == SFFTB_OK) {
+        static int32_t h[128 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int r : {0, 1, 33, 127}) {
+            fprintf(stderr, "roll dbg row %3d:", r);
+            for (int i = 0; i < 16; ++i) fprintf(stderr, " %d", h[r * 16 + i]);
+            fprintf(stderr, "\n");
+        }
+    }
+    return rc == SFFTB_OK ? 1 : -rc;
+}
+
+}  // namespace sfftb
+
+// Rows the rolling tensor-core hash sent to its exact 64-bit path (a
+// coordinate outside [-2^13, 2^13)) since the last reset.
+extern "C" int64_t sfftb_hash_roll_recomputed(int reset) {
+    unsigned long long* p = sfftb::roll::recomputed_counter();
+    if (!p) return -1;
+    unsigned long long v = 0;
+    if (cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (reset) cudaMemset(p, 0, sizeof(v));
+    return (int64_t)v;
+}
