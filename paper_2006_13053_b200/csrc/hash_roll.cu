@@ -48,10 +48,11 @@ constexpr int kLG = 5;          // lattices per group (15 of the 16 MMA columns)
 constexpr int kNC = 16;         // MMA N
 constexpr int kACols = 8;       // TMEM columns of one A tile (K = 32 bytes)
 constexpr int kMaxTA = 56;      // resident tiles
-constexpr int kMaxND = 16;      // accumulator buffers
-constexpr int kMinND = 4;
+constexpr int kMaxND = 8;       // accumulator buffers (one cohort each)
+constexpr int kMaxNG = 14;
 constexpr int kLoaders = 8;
 constexpr int kEpiWarp0 = 2 + kLoaders;
+constexpr int kEpiWarps = 16;
 constexpr int64_t kOffset = 8192;  // u = k + kOffset must lie in [0, 2^14)
 
 struct Args {
@@ -70,6 +71,7 @@ struct Args {
     uint32_t* detmask;
     unsigned long long* recomputed;
     int32_t* dbg;  // diagnostics: the 128 x 16 accumulators of tile 0, step 0
+    long long* prof;  // diagnostics: cycle counters of CTA 0 (SFFTB_HASH_ROLL_PROF)
 };
 
 // ---- PTX helpers (shared-window addresses) ----
@@ -154,7 +156,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 }
 
 // Exact hits of one row from global memory (a coordinate outside the limb range).
-__device__ int exact_row_hits(const Args& a, int d, int64_t row) {
+__device__ __noinline__ int exact_row_hits(const Args& a, int d, int64_t row) {
     int h = 0;
     for (int l = 0; l < a.L; ++l) {
         uint64_t acc = 0;
@@ -185,8 +187,8 @@ __host__ __device__ inline Smem smem_map(int NG, int TA, int RS) {
     s.bm_empty = o; o += 16;
     s.d_full = o;   o += 8u * kMaxND;
     s.d_empty = o;  o += 8u * kMaxND;
-    s.a_full = o;   o += 8u * kMaxTA;
-    s.a_empty = o;  o += 8u * kMaxTA * 4;
+    s.a_full = o;   o += 8u * kMaxNG;
+    s.a_empty = o;  o += 8u * kMaxNG;
     s.tmem_holder = o; o += 16;
     o = (o + 127u) & ~127u;
     s.bop = o;      o += (uint32_t)NG * 512u;           // B operand: NG x [2][16][16 B]
@@ -197,26 +199,40 @@ __host__ __device__ inline Smem smem_map(int NG, int TA, int RS) {
     return s;
 }
 
+#define ROLL_T(acc, ...)                         \
+    do {                                         \
+        if (PROF) {                              \
+            const long long t0_ = clock64();     \
+            __VA_ARGS__;                         \
+            acc += clock64() - t0_;              \
+        } else {                                 \
+            __VA_ARGS__;                         \
+        }                                        \
+    } while (0)
+
 // One step's canonical item order, shared by the MMA issuer and the epilogue:
-// cohorts from the oldest (age NG-1, retiring) to the newborn (age 0).
+// cohorts from the oldest (age NG-1, retiring) to the newborn (age 0).  An
+// item is a whole cohort (SP tiles, one accumulator buffer of 16 SP columns).
 #define ROLL_FOR_ITEMS(s_, ...)                                                       \
-    for (int age = a.NG - 1; age >= 0; --age) {                                       \
-        const int64_t b = (int64_t)(s_) - age;                                        \
-        if (b < 0 || b >= nb) continue;                                               \
-        const int c = (int)(b % a.NG);                                                \
-        for (int k = 0; k < a.SP; ++k) {                                              \
-            const int64_t j = b * a.SP + k;                                           \
-            if (j >= my_tiles) break;                                                 \
-            const int slot = c * a.SP + k;                                            \
-            __VA_ARGS__                                                               \
-            if (++buf == a.ND) {                                                      \
-                buf = 0;                                                              \
-                ++round;                                                              \
+    {                                                                                 \
+        int c = cold; /* cohort of age NG-1 */                                        \
+        for (int age = a.NG - 1; age >= 0; --age) {                                   \
+            const int b = (s_) - age;                                                 \
+            if (b >= 0 && b < nb) {                                                   \
+                const int ntile = min(a.SP, my_tiles - b * a.SP);                     \
+                __VA_ARGS__                                                           \
+                if (++buf == a.ND) {                                                  \
+                    buf = 0;                                                          \
+                    round ^= 1u;                                                      \
+                    first_round = false;                                              \
+                }                                                                     \
             }                                                                         \
+            if (++c == a.NG) c = 0;                                                   \
         }                                                                             \
+        if (++cold == a.NG) cold = 0;                                                 \
     }
 
-template <int D>
+template <int D, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     constexpr int H = D / 2;        // 16-byte chunks (coordinate pairs) per row
@@ -227,25 +243,26 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     const uint32_t ring_bytes = (uint32_t)kLG * a.S2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t cta = blockIdx.x, ncta = gridDim.x;
-    const int64_t my_tiles = a.ntiles > cta ? (a.ntiles - 1 - cta) / ncta + 1 : 0;
-    const int64_t nb = (my_tiles + a.SP - 1) / a.SP;             // births
-    const int64_t nsteps = nb > 0 ? nb + a.NG - 1 : 0;
+    const int my_tiles = a.ntiles > cta ? (int)((a.ntiles - 1 - cta) / ncta + 1) : 0;
+    const int nb = (my_tiles + a.SP - 1) / a.SP;             // births
+    const int nsteps = nb > 0 ? nb + a.NG - 1 : 0;
     const int dcol0 = a.TA * kACols;
+    const int dstride = kNC * a.SP;  // accumulator columns of one cohort
 
     // ---- setup ----
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             bar_init(raw + S.bm_raw + 8u * i, 1);
             bar_init(raw + S.bm_full + 8u * i, 1);
-            bar_init(raw + S.bm_empty + 8u * i, 16);
+            bar_init(raw + S.bm_empty + 8u * i, kEpiWarps);
         }
         for (int i = 0; i < a.ND; ++i) {
             bar_init(raw + S.d_full + 8u * i, 1);
-            bar_init(raw + S.d_empty + 8u * i, 4);
+            bar_init(raw + S.d_empty + 8u * i, kEpiWarps);
         }
-        for (int i = 0; i < a.TA; ++i) {
-            bar_init(raw + S.a_full + 8u * i, 4);
-            for (int q = 0; q < 4; ++q) bar_init(raw + S.a_empty + 8u * (i * 4 + q), 1);
+        for (int i = 0; i < a.NG; ++i) {
+            bar_init(raw + S.a_full + 8u * i, kLoaders);
+            bar_init(raw + S.a_empty + 8u * i, kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -306,9 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
 
     if (warp == 0) {
         // ================= bitmap producer =================
+        long long pt[4] = {0, 0, 0, 0};
+        const long long tstart = clock64();
         const uint32_t wbytes = (uint32_t)a.W * 4u;
         const int wM = (int)(a.M >> 5), sh = (int)(a.M & 31u);
-        auto issue = [&](int64_t s) {
+        auto issue = [&](int s) {
             const int ring = (int)(s & 1);
             const int l0 = (int)(s % a.NG) * kLG;
             const int cnt = min(a.L, l0 + kLG) - l0;
@@ -322,62 +341,80 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             }
         };
         // bits [M, M + 32 ext_words) := bits [0, 32 ext_words) of every lattice
-        auto extend = [&](int64_t s) {
+        auto extend = [&](int s) {
             const int ring = (int)(s & 1);
             const int l0 = (int)(s % a.NG) * kLG;
             const int cnt = min(a.L, l0 + kLG) - l0;
-            bar_wait(raw + S.bm_raw + 8u * ring, (uint32_t)((s >> 1) & 1));
+            ROLL_T(pt[0], bar_wait(raw + S.bm_raw + 8u * ring, (uint32_t)((s >> 1) & 1)));
+            const long long te0 = clock64();
             uint32_t* base = reinterpret_cast<uint32_t*>(smem_raw + (ring0 - raw) +
                                                          (uint32_t)ring * ring_bytes);
-            const int per = a.ext_words + 1;
-            for (int e = lane; e < cnt * per; e += 32) {
-                uint32_t* bm = base + (size_t)(e / per) * (a.S2 / 4);
-                const int w = e % per;
-                uint32_t v;
-                if (sh == 0) {
-                    v = w < a.ext_words ? bm[w] : 0u;
-                } else {
-                    const uint32_t lo = w == 0 ? (bm[wM] & ((1u << sh) - 1u)) : (bm[w - 1] >> (32 - sh));
-                    const uint32_t hi = w < a.ext_words ? (bm[w] << sh) : 0u;
-                    v = lo | hi;
+            for (int i = 0; i < cnt; ++i) {
+                uint32_t* bm = base + (size_t)i * (a.S2 / 4);
+                for (int w = lane; w <= a.ext_words; w += 32) {
+                    uint32_t v;
+                    if (sh == 0) {
+                        v = w < a.ext_words ? bm[w] : 0u;
+                    } else {
+                        const uint32_t lo =
+                            w == 0 ? (bm[wM] & ((1u << sh) - 1u)) : (bm[w - 1] >> (32 - sh));
+                        const uint32_t hi = w < a.ext_words ? (bm[w] << sh) : 0u;
+                        v = lo | hi;
+                    }
+                    bm[wM + w] = v;
                 }
-                bm[wM + w] = v;
             }
             __syncwarp();
             if (lane == 0) bar_arrive(raw + S.bm_full + 8u * ring);
+            pt[1] += clock64() - te0;
         };
         if (nsteps > 0) issue(0);
         if (nsteps > 1) issue(1);
         if (nsteps > 0) extend(0);
-        for (int64_t s = 0; s < nsteps; ++s) {
+        for (int s = 0; s < nsteps; ++s) {
             if (s + 1 < nsteps) extend(s + 1);
             if (s + 2 < nsteps) {
-                bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1), (uint32_t)((s >> 1) & 1));
+                ROLL_T(pt[2], bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1),
+                                       (uint32_t)((s >> 1) & 1)));
                 issue(s + 2);
             }
+        }
+        if (PROF && cta == 0 && lane == 0) {
+            a.prof[0] = pt[0];
+            a.prof[1] = pt[1];
+            a.prof[2] = pt[2];
+            a.prof[3] = clock64() - tstart;
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         const bool leader = elect_one();
         const uint32_t idesc = (2u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
-        int buf = 0;
-        int64_t round = 0;
-        for (int64_t s = 0; s < nsteps; ++s) {
-            const uint64_t bdesc =
-                umma_desc(raw + S.bop + (uint32_t)(s % a.NG) * 512u, 256u, 128u);
+        int buf = 0, g = 0, cold = 1 % a.NG;
+        uint32_t round = 0;
+        bool first_round = true;
+        long long pt[4] = {0, 0, 0, 0};
+        const long long tstart = clock64();
+        for (int s = 0; s < nsteps; ++s) {
+            const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)g * 512u, 256u, 128u);
             ROLL_FOR_ITEMS(s, {
-                if (round >= 1)
-                    bar_wait(raw + S.d_empty + 8u * buf, (uint32_t)((round - 1) & 1));
+                if (!first_round) ROLL_T(pt[0], bar_wait(raw + S.d_empty + 8u * buf, round ^ 1u));
                 if (age == 0)
-                    bar_wait(raw + S.a_full + 8u * slot, (uint32_t)((b / a.NG) & 1));
+                    ROLL_T(pt[1], bar_wait(raw + S.a_full + 8u * c, (uint32_t)((b / a.NG) & 1)));
                 tc_fence_after();
                 if (leader) {
-                    umma_i8_ts(tmem + (uint32_t)(dcol0 + kNC * buf),
-                               tmem + (uint32_t)(slot * kACols), bdesc, idesc);
+                    for (int k = 0; k < ntile; ++k)
+                        umma_i8_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
+                                   tmem + (uint32_t)((c * a.SP + k) * kACols), bdesc, idesc);
                     umma_commit(raw + S.d_full + 8u * buf);
                 }
                 __syncwarp();
             })
+            if (++g == a.NG) g = 0;
+        }
+        if (PROF && cta == 0 && lane == 0) {
+            a.prof[8] = pt[0];
+            a.prof[9] = pt[1];
+            a.prof[11] = clock64() - tstart;
         }
     } else if (warp < kEpiWarp0) {
         // ================= row loaders =================
@@ -385,22 +422,22 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         const int hsel = (warp - 2) >> 2;    // tiles k = hsel (mod 2) of every birth
         uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + S.stage) + (warp - 2) * 32 * RS;
         const int4* gbase = reinterpret_cast<const int4*>(a.elems);
-        // item = (birth b, tile k); rows [t*128 + q*32, +32) of tile t = cta + (b*SP + k)*ncta
-        auto item_rows = [&](int64_t b, int k) -> int64_t {
-            return ((cta + (b * a.SP + k) * ncta) * kTile + q * 32);
+        // unit = (birth b, tile k); rows [t*128 + q*32, +32) of tile t = cta + (b*SP + k)*ncta
+        auto unit_rows = [&](int b, int k) -> int64_t {
+            return ((cta + (int64_t)(b * a.SP + k) * ncta) * kTile + q * 32);
         };
-        auto valid_item = [&](int64_t b, int k) -> bool {
+        auto valid_unit = [&](int b, int k) -> bool {
             return b < nb && (b * a.SP + k) < my_tiles;
         };
-        auto advance = [&](int64_t& b, int& k) {
+        auto advance = [&](int& b, int& k) {
             k += 2;
             if (k >= a.SP) {
                 k = hsel;
                 ++b;
             }
         };
-        auto load = [&](int4 (&rawv)[H], int64_t b, int k) {
-            const int64_t r0 = item_rows(b, k);
+        auto load = [&](int4 (&rawv)[H], int b, int k) {
+            const int64_t r0 = unit_rows(b, k);
 #pragma unroll
             for (int i = 0; i < H; ++i) {
                 const int ch = lane + 32 * i;
@@ -408,36 +445,37 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                 rawv[i] = row < a.n ? __ldg(gbase + r0 * H + ch) : make_int4(0, 0, 0, 0);
             }
         };
-        auto prefetch = [&](int64_t b, int k) {
-            const char* p = reinterpret_cast<const char*>(a.elems) + item_rows(b, k) * (8 * D);
-            if (lane * 128 < 32 * 8 * D && item_rows(b, k) + 32 <= a.n) prefetch_l2(p + lane * 128);
+        auto prefetch = [&](int b, int k) {
+            const char* p = reinterpret_cast<const char*>(a.elems) + unit_rows(b, k) * (8 * D);
+            if (lane * 128 < 32 * 8 * D && unit_rows(b, k) + 32 <= a.n) prefetch_l2(p + lane * 128);
         };
-        int64_t b = 0;
+        int b = 0;
         int k = hsel;
-        if (k >= a.SP) b = nb;  // SP == 1: the second loader of each quadrant idles
+        int arrived = 0;  // births this warp has signalled
+        int waited = -1;  // last birth whose slots this warp knows to be free
+        long long pt[4] = {0, 0, 0, 0};
+        const long long tstart = clock64();
         int4 cur[H], nxt[H];
-        if (valid_item(b, k)) load(cur, b, k);
+        if (valid_unit(b, k)) load(cur, b, k);
         {
-            int64_t pb = b;
+            int pb = b;
             int pk = k;
-            for (int i = 0; i < 3; ++i) {
+            for (int i = 0; i < 4; ++i) {
                 advance(pb, pk);
-                if (valid_item(pb, pk)) prefetch(pb, pk);
+                if (valid_unit(pb, pk)) prefetch(pb, pk);
             }
         }
-        while (valid_item(b, k)) {
-            int64_t b2 = b;
+        while (valid_unit(b, k)) {
+            int b2 = b;
             int k2 = k;
             advance(b2, k2);
-            const bool more = valid_item(b2, k2);
+            const bool more = valid_unit(b2, k2);
             if (more) load(nxt, b2, k2);
             {
-                int64_t pb = b2;
+                int pb = b2;
                 int pk = k2;
-                advance(pb, pk);
-                advance(pb, pk);
-                advance(pb, pk);
-                if (valid_item(pb, pk)) prefetch(pb, pk);
+                for (int i = 0; i < 4; ++i) advance(pb, pk);
+                if (valid_unit(pb, pk)) prefetch(pb, pk);
             }
             // pack: one 32-bit word per coordinate pair
 #pragma unroll
@@ -469,15 +507,21 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             // K = 2D: the constant 1; K = 2D + 1: the flag
             if (H < 8) r[H] = 1u | (bad ? 0x100u : 0u);
             __syncwarp();
-            const int slot = (int)(b % a.NG) * a.SP + k;
-            const int64_t beta = b / a.NG;
-            if (beta >= 1)
-                bar_wait(raw + S.a_empty + 8u * (slot * 4 + q), (uint32_t)((beta - 1) & 1));
+            const int c = b % a.NG;
+            const int beta = b / a.NG;
+            if (beta >= 1 && waited < b) {
+                ROLL_T(pt[0], bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1)));
+                waited = b;
+            }
             tc_fence_after();
-            tmem_st8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(slot * kACols), r);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) bar_arrive(raw + S.a_full + 8u * slot);
+            ROLL_T(pt[1], tmem_st8(tmem + ((uint32_t)(q * 32) << 16) +
+                                       (uint32_t)((c * a.SP + k) * kACols), r));
+            if (b2 != b || !more) {  // last unit of this birth for this warp
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
+                arrived = b + 1;
+            }
             b = b2;
             k = k2;
             if (more) {
@@ -485,61 +529,92 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                 for (int i = 0; i < H; ++i) cur[i] = nxt[i];
             }
         }
+        // births in which this warp had no tile (the last, partial one)
+        for (; arrived < nb; ++arrived) {
+            const uint32_t c = (uint32_t)(arrived % a.NG);
+            const int beta = arrived / a.NG;
+            // not before the cohort's previous occupants have retired: an early
+            // arrival would be counted towards THEIR birth
+            if (beta >= 1) bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1));
+            if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
+        }
+        if (PROF && cta == 0 && lane == 0 && warp == 2) {
+            a.prof[16] = pt[0];
+            a.prof[17] = pt[1];
+            a.prof[19] = clock64() - tstart;
+        }
     } else {
         // ================= epilogue =================
         const int ew = warp - kEpiWarp0;
         const int grp = ew >> 2;
         const int q = warp & 3;
-        const uint32_t M = a.M, negM = a.negM, magic = a.magic;
-        uint8_t* hs = smem_raw + S.hits;
-        int buf = 0;
-        int64_t round = 0;
-        for (int64_t s = 0; s < nsteps; ++s) {
-            const int ring = (int)(s & 1);
-            const int l0 = (int)(s % a.NG) * kLG;
-            const int lcg = min(a.L, l0 + kLG) - l0;
+        const uint32_t negM = a.negM, magic = a.magic;
+        uint8_t* hs = smem_raw + S.hits + q * 32 + lane;
+        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)dcol0;
+        int buf = 0, g = 0, cold = 1 % a.NG;
+        uint32_t round = 0;
+        bool first_round = true;
+        (void)first_round;
+        long long pt[4] = {0, 0, 0, 0};
+        const long long tstart = clock64();
+        for (int s = 0; s < nsteps; ++s) {
+            const int ring = s & 1;
+            const int lcg = min(a.L, g * kLG + kLG) - g * kLG;
+            // pair i's bit ends at position 32 - kLG + i of the accumulator
+            const uint32_t lmask = ((1u << lcg) - 1u) << (32 - kLG);
             uint32_t lb[kLG];
 #pragma unroll
-            for (int i = 0; i < kLG; ++i)
-                lb[i] = ring0 + (uint32_t)ring * ring_bytes + (uint32_t)i * a.S2;
-            bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1));
+            for (int i = 0; i < kLG; ++i) {
+                uint32_t t = ring0 + (uint32_t)ring * ring_bytes + (uint32_t)i * a.S2;
+                asm volatile("" : "+r"(t));  // keep the five slot bases in registers
+                lb[i] = t;
+            }
+            ROLL_T(pt[0], bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1)));
             ROLL_FOR_ITEMS(s, {
-                if (((c + k) & 3) == grp) {
-                    bar_wait(raw + S.d_full + 8u * buf, (uint32_t)(round & 1));
-                    tc_fence_after();
+                ROLL_T(pt[1], bar_wait(raw + S.d_full + 8u * buf, round));
+                tc_fence_after();
+                bool freed = false;
+                for (int kk = grp; kk < ntile; kk += kEpiWarps / 4) {
                     uint32_t v[16];
-                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * buf), v);
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
-                    if (a.dbg && s == 0 && j == 0 && cta == 0) {
+                    ROLL_T(pt[2], tmem_ld16(tlane + (uint32_t)(dstride * buf + kNC * kk), v));
+                    if (kk + kEpiWarps / 4 >= ntile) {  // this warp's last tile of the cohort
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
+                        freed = true;
+                    }
+                    if (a.dbg && s == 0 && kk == 0 && cta == 0) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
                     }
-                    uint32_t bacc = 0;
+                    uint8_t* hp = hs + (c * a.SP + kk) * kTile;
+                    uint32_t hprev = 0;
+                    if (age != 0) hprev = *hp;
+                    // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
+                    uint32_t r[kLG], w[kLG];
 #pragma unroll
                     for (int i = 0; i < kLG; ++i) {
-                        if (i < lcg) {
-                            uint32_t x = (v[3 * i + 1] << 8) + v[3 * i];
-                            x = (v[3 * i + 2] << 16) + x;
-                            const uint32_t qq = __umulhi(x, magic);
-                            uint32_t r;
-                            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(qq), "r"(negM), "r"(x));
-                            uint32_t w;
-                            asm volatile("{\n\t.reg .u32 t;\n\t"
-                                         "shr.u32 t, %1, 3;\n\t"
-                                         "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
-                                         "ld.shared.u32 %0, [t];\n\t}"
-                                         : "=r"(w)
-                                         : "r"(r), "r"(lb[i]));
-                            bacc = __funnelshift_r(bacc, __funnelshift_r(w, w, r), 1);
-                        }
+                        uint32_t x = (v[3 * i + 1] << 8) + v[3 * i];
+                        x = (v[3 * i + 2] << 16) + x;
+                        const uint32_t qq = __umulhi(x, magic);
+                        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(x));
                     }
-                    const int hidx = slot * kTile + q * 32 + lane;
-                    uint32_t h = __popc(bacc);
-                    if (age != 0) h += hs[hidx];
+#pragma unroll
+                    for (int i = 0; i < kLG; ++i) {
+                        asm volatile("{\n\t.reg .u32 t;\n\t"
+                                     "shr.u32 t, %1, 3;\n\t"
+                                     "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
+                                     "ld.shared.u32 %0, [t];\n\t}"
+                                     : "=r"(w[i])
+                                     : "r"(r[i]), "r"(lb[i]));
+                    }
+                    uint32_t bacc = 0;
+#pragma unroll
+                    for (int i = 0; i < kLG; ++i)
+                        bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], r[i]), 1);
+                    const uint32_t h = __popc(bacc & lmask) + hprev;
                     if (age == a.NG - 1) {
-                        const int64_t t = cta + j * ncta;
+                        const int64_t t = cta + (int64_t)(b * a.SP + kk) * ncta;
                         const int64_t row0 = t * kTile + q * 32;
                         const int64_t row = row0 + lane;
                         const bool valid = row < a.n;
@@ -552,16 +627,31 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                             __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
                         if (valid && a.hits64) a.hits64[row] = hits;
                         if (lane == 0 && row0 < a.n) a.detmask[row0 >> 5] = det;
-                        if (lane == 0) bar_arrive(raw + S.a_empty + 8u * (slot * 4 + q));
                     } else {
-                        hs[hidx] = (uint8_t)h;
+                        *hp = (uint8_t)h;
                     }
+                }
+                if (!freed) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
+                }
+                if (age == a.NG - 1) {
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(raw + S.a_empty + 8u * c);
                 }
             })
             __syncwarp();
             if (lane == 0) bar_arrive(raw + S.bm_empty + 8u * ring);
+            if (++g == a.NG) g = 0;
         }
-        (void)M;
+        if (PROF && cta == 0 && lane == 0 && (ew == 0 || ew == 15)) {
+            long long* o = a.prof + (ew == 0 ? 24 : 32);
+            o[0] = pt[0];
+            o[1] = pt[1];
+            o[2] = pt[2];
+            o[3] = clock64() - tstart;
+        }
     }
 
     // ---- teardown ----
@@ -588,7 +678,14 @@ static unsigned long long* recomputed_counter() {
 
 template <int D>
 static int launch_d(Args& a, uint32_t smem, int grid, cudaStream_t st) {
-    auto kern = hash_roll_kernel<D>;
+    if (D == 10 && a.prof) {
+        auto kp = hash_roll_kernel<10, true>;
+        SFFTB_CUDA(smem_opt_in(kp, smem));
+        kp<<<grid, kThreads, smem, st>>>(a);
+        SFFTB_CHECK_LAUNCH();
+        return SFFTB_OK;
+    }
+    auto kern = hash_roll_kernel<D, false>;
     SFFTB_CUDA(smem_opt_in(kern, smem));
     kern<<<grid, kThreads, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
@@ -609,7 +706,7 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     }
     const char* mr = getenv("SFFTB_HASH_ROLL_MINROWS");
     const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 18;
-    if (n < min_rows || n > ((int64_t)1 << 40) || L < 1 || L > 255 || M < 64 ||
+    if (n < min_rows || n > ((int64_t)1 << 36) || L < 1 || L > 255 || M < 64 ||
         M >= ((int64_t)1 << 24))
         return 0;
     if (d != 4 && d != 6 && d != 8 && d != 10 && d != 12 && d != 14) return 0;
@@ -627,11 +724,13 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     uint32_t S2 = 64;
     while ((int64_t)S2 < std::max(need_words, W) * 4) S2 <<= 1;
     const int NG = (int)((L + kLG - 1) / kLG);
-    int SP = (512 - kMinND * kNC) / kACols / NG;
-    if (SP < 1) return 0;
-    SP = std::min(SP, 8);
+    // tiles per cohort: 8 when two accumulator buffers still fit, else 4
+    if (NG > kMaxNG) return 0;
+    int SP = 8;
+    if (512 - NG * SP * kACols < 2 * kNC * SP) SP = 4;
+    if (512 - NG * SP * kACols < 2 * kNC * SP) return 0;
     const int TA = NG * SP;
-    const int ND = std::min(kMaxND, (512 - TA * kACols) / kNC);
+    const int ND = std::min(kMaxND, (512 - TA * kACols) / (kNC * SP));
     const int RS = (int)(d / 2) | 1;
     const Smem S = smem_map(NG, TA, RS);
     const uint32_t smem = S.end + S2 + 2u * kLG * S2;
@@ -674,6 +773,13 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
         SFFTB_CUDA(cudaMemsetAsync(dbg, 0xFF, 128 * 16 * sizeof(int32_t), st));
         a.dbg = dbg;
     }
+    a.prof = nullptr;
+    static long long* prof = nullptr;
+    if (getenv("SFFTB_HASH_ROLL_PROF")) {
+        if (!prof) SFFTB_CUDA(cudaMalloc(&prof, 40 * sizeof(long long)));
+        SFFTB_CUDA(cudaMemsetAsync(prof, 0, 40 * sizeof(long long), st));
+        a.prof = prof;
+    }
     int grid = num_sms();
     if (const char* e = getenv("SFFTB_HASH_ROLL_GRID")) grid = std::max(1, atoi(e));
     grid = (int)std::min<int64_t>(grid, a.ntiles);
@@ -698,6 +804,17 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
             for (int i = 0; i < 16; ++i) fprintf(stderr, " %d", h[r * 16 + i]);
             fprintf(stderr, "\n");
         }
+    }
+    if (a.prof && rc == SFFTB_OK) {
+        long long h[40];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "roll prof (cycles, CTA 0): producer raw_wait %lld extend %lld empty_wait %lld total %lld\n",
+                h[0], h[1], h[2], h[3]);
+        fprintf(stderr, "  mma: d_empty_wait %lld a_full_wait %lld total %lld\n", h[8], h[9], h[11]);
+        fprintf(stderr, "  loader w2: a_empty_wait %lld tmem_st %lld total %lld\n", h[16], h[17], h[19]);
+        fprintf(stderr, "  epi w0: bm_wait %lld d_full_wait %lld tmem_ld %lld total %lld\n", h[24], h[25], h[26], h[27]);
+        fprintf(stderr, "  epi w15: bm_wait %lld d_full_wait %lld tmem_ld %lld total %lld\n", h[32], h[33], h[34], h[35]);
     }
     return rc == SFFTB_OK ? 1 : -rc;
 }
