@@ -47,9 +47,8 @@ constexpr int kTile = 128;
 constexpr int kLG = 5;          // lattices per group (15 of the 16 MMA columns)
 constexpr int kNC = 16;         // MMA N
 constexpr int kACols = 8;       // TMEM columns of one A tile (K = 32 bytes)
-constexpr int kMaxTA = 56;      // resident tiles
-constexpr int kMaxND = 8;       // accumulator buffers (one cohort each)
-constexpr int kMaxNG = 14;
+constexpr int kSP = 4;          // tiles per cohort (one per epilogue warp group)
+constexpr int kMaxNG = 12;      // 8*4*NG A columns + two 64-column accumulator buffers
 constexpr int kLoaders = 8;
 constexpr int kEpiWarp0 = 2 + kLoaders;
 constexpr int kEpiWarps = 16;
@@ -59,7 +58,7 @@ struct Args {
     const int64_t* elems;
     int64_t n;
     const int64_t* zmat;  // (L, d)
-    int L, NG, SP, TA, ND;
+    int d, L, NG;
     uint32_t M, negM, magic;
     const uint32_t* bits;  // (L, W)
     int W;                 // words per lattice in global memory
@@ -177,24 +176,22 @@ __device__ __noinline__ int exact_row_hits(const Args& a, int d, int64_t row) {
 // slots follow at the next S2-aligned address).
 struct Smem {
     uint32_t bm_raw, bm_full, bm_empty, d_full, d_empty, a_full, a_empty, tmem_holder;
-    uint32_t bop, hits, stage, end;
+    uint32_t bop, stage, end;
 };
-__host__ __device__ inline Smem smem_map(int NG, int TA, int RS) {
+__host__ __device__ inline Smem smem_map(int NG) {
     Smem s;
     uint32_t o = 0;
     s.bm_raw = o;   o += 16;
     s.bm_full = o;  o += 16;
     s.bm_empty = o; o += 16;
-    s.d_full = o;   o += 8u * kMaxND;
-    s.d_empty = o;  o += 8u * kMaxND;
+    s.d_full = o;   o += 16;
+    s.d_empty = o;  o += 16;
     s.a_full = o;   o += 8u * kMaxNG;
     s.a_empty = o;  o += 8u * kMaxNG;
     s.tmem_holder = o; o += 16;
     o = (o + 127u) & ~127u;
-    s.bop = o;      o += (uint32_t)NG * 512u;           // B operand: NG x [2][16][16 B]
-    s.hits = o;     o += (uint32_t)TA * kTile;          // u8 running hit counts
-    o = (o + 15u) & ~15u;
-    s.stage = o;    o += (uint32_t)kLoaders * 32u * RS * 4u;  // loader transposition
+    s.bop = o;      o += (uint32_t)NG * 512u;                 // B operand: NG x [2][16][16 B]
+    s.stage = o;    o += (uint32_t)kLoaders * 32u * 7u * 4u;  // loader transposition (RS <= 7)
     s.end = (o + 15u) & ~15u;
     return s;
 }
@@ -210,44 +207,134 @@ __host__ __device__ inline Smem smem_map(int NG, int TA, int RS) {
         }                                        \
     } while (0)
 
-// One step's canonical item order, shared by the MMA issuer and the epilogue:
-// cohorts from the oldest (age NG-1, retiring) to the newborn (age 0).  An
-// item is a whole cohort (SP tiles, one accumulator buffer of 16 SP columns).
-#define ROLL_FOR_ITEMS(s_, ...)                                                       \
-    {                                                                                 \
-        int c = cold; /* cohort of age NG-1 */                                        \
-        for (int age = a.NG - 1; age >= 0; --age) {                                   \
-            const int b = (s_) - age;                                                 \
-            if (b >= 0 && b < nb) {                                                   \
-                const int ntile = min(a.SP, my_tiles - b * a.SP);                     \
-                __VA_ARGS__                                                           \
-                if (++buf == a.ND) {                                                  \
-                    buf = 0;                                                          \
-                    round ^= 1u;                                                      \
-                    first_round = false;                                              \
-                }                                                                     \
-            }                                                                         \
-            if (++c == a.NG) c = 0;                                                   \
-        }                                                                             \
-        if (++cold == a.NG) cold = 0;                                                 \
-    }
+struct Ctx {
+    uint32_t raw, tmem;
+    int lane, warp, nb, NG;
+    int64_t cta, ncta;
+};
 
+// Row loader of one warp: lane quadrant q = warp & 3, tiles k = hsel, hsel + 2
+// of every birth.  Coalesced 16-byte loads (a coordinate pair each), packed
+// to one word per pair, transposed through shared memory to thread-per-row,
+// stored into the cohort's A tiles in tensor memory.
 template <int D, bool PROF>
+__device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const Ctx& x,
+                                           uint8_t* smem_raw) {
+    constexpr int H = D / 2;   // 16-byte chunks (coordinate pairs) per row
+    constexpr int RS = H | 1;  // odd row stride of the transposition buffer
+    const int lane = x.lane, q = x.warp & 3, hsel = (x.warp - 2) >> 2;
+    const uint32_t raw = x.raw;
+    uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + S.stage) + (x.warp - 2) * 32 * RS;
+    const int4* gbase = reinterpret_cast<const int4*>(a.elems);
+    // unit = (birth b, tile k): rows [t*128 + q*32, +32) of tile t = cta + (4b + k) ncta
+    auto unit_rows = [&](int b, int k) -> int64_t {
+        return ((x.cta + (int64_t)(b * kSP + k) * x.ncta) * kTile + q * 32);
+    };
+    auto load = [&](int4 (&rawv)[H], int b, int k) {
+        const int64_t r0 = unit_rows(b, k);
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const int ch = lane + 32 * i;
+            const int64_t row = r0 + ch / H;
+            rawv[i] = row < a.n ? __ldg(gbase + r0 * H + ch) : make_int4(0, 0, 0, 0);
+        }
+    };
+    auto prefetch = [&](int b, int k) {
+        const int64_t r0 = unit_rows(b, k);
+        const char* p = reinterpret_cast<const char*>(a.elems) + r0 * (8 * D);
+        if (lane * 128 < 32 * 8 * D && r0 + 32 <= a.n) prefetch_l2(p + lane * 128);
+    };
+    long long pt[2] = {0, 0};
+    const long long tstart = clock64();
+    int4 cur[H], nxt[H];
+    if (x.nb > 0) load(cur, 0, hsel);
+    for (int u = 1; u <= 4; ++u)
+        if ((u >> 1) < x.nb) prefetch(u >> 1, hsel + 2 * (u & 1));
+    int c = 0, beta = 0;
+    for (int b = 0; b < x.nb; ++b) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const int k = hsel + 2 * kk;
+            // the next unit's rows are requested before this one is packed
+            const int b2 = kk == 0 ? b : b + 1, k2 = kk == 0 ? hsel + 2 : hsel;
+            if (b2 < x.nb) load(nxt, b2, k2);
+            {
+                const int u = 2 * b + kk + 5;
+                if ((u >> 1) < x.nb) prefetch(u >> 1, hsel + 2 * (u & 1));
+            }
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const int ch = lane + 32 * i;
+                const uint64_t u0 =
+                    (uint64_t)(((int64_t)(uint32_t)cur[i].x | ((int64_t)cur[i].y << 32)) + kOffset);
+                const uint64_t u1 =
+                    (uint64_t)(((int64_t)(uint32_t)cur[i].z | ((int64_t)cur[i].w << 32)) + kOffset);
+                const uint32_t l0 = (uint32_t)u0, l1 = (uint32_t)u1;
+                uint32_t w = (l0 & 127u) | (((l0 >> 7) & 127u) << 8) | ((l1 & 127u) << 16) |
+                             (((l1 >> 7) & 127u) << 24);
+                if ((u0 | u1) >> 14) w |= 0x80u;
+                stg[(ch / H) * RS + (ch % H)] = w;
+            }
+            __syncwarp();
+            uint32_t r[8];
+            uint32_t bad = 0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                if (p < H) {
+                    const uint32_t w = stg[lane * RS + p];
+                    bad |= w & 0x80u;
+                    r[p] = w & ~0x80u;
+                } else {
+                    r[p] = 0u;
+                }
+            }
+            // K = 2D: the constant 1; K = 2D + 1: the out-of-range flag
+            if (H < 8) r[H] = 1u | (bad ? 0x100u : 0u);
+            __syncwarp();
+            if (kk == 0 && beta >= 1)  // the cohort's previous occupants have retired
+                ROLL_T(pt[0], bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1)));
+            tc_fence_after();
+            ROLL_T(pt[1], tmem_st8(x.tmem + ((uint32_t)(q * 32) << 16) +
+                                       (uint32_t)((c * kSP + k) * kACols), r));
+            if (kk == 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
+            }
+#pragma unroll
+            for (int i = 0; i < H; ++i) cur[i] = nxt[i];
+        }
+        if (++c == x.NG) {
+            c = 0;
+            ++beta;
+        }
+    }
+    if (PROF && x.cta == 0 && lane == 0 && x.warp == 2) {
+        a.prof[16] = pt[0];
+        a.prof[17] = pt[1];
+        a.prof[19] = clock64() - tstart;
+    }
+}
+
+// NG = lattice groups per pass = cohorts.  Every step runs the same NG items
+// (cohorts 0..NG-1 in index order, four tiles each, accumulator buffer c & 1):
+// cohorts not yet born or past the end of the rows are processed as dummies
+// (their outputs are never written), so the whole schedule is static.
+template <int NG, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    constexpr int H = D / 2;        // 16-byte chunks (coordinate pairs) per row
-    constexpr int RS = H | 1;       // odd row stride of the transposition buffer
     const uint32_t raw = smem_addr(smem_raw);
-    const Smem S = smem_map(a.NG, a.TA, RS);
+    const Smem S = smem_map(NG);
     const uint32_t ring0 = (raw + S.end + a.S2 - 1u) & ~(a.S2 - 1u);
     const uint32_t ring_bytes = (uint32_t)kLG * a.S2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t cta = blockIdx.x, ncta = gridDim.x;
     const int my_tiles = a.ntiles > cta ? (int)((a.ntiles - 1 - cta) / ncta + 1) : 0;
-    const int nb = (my_tiles + a.SP - 1) / a.SP;             // births
-    const int nsteps = nb > 0 ? nb + a.NG - 1 : 0;
-    const int dcol0 = a.TA * kACols;
-    const int dstride = kNC * a.SP;  // accumulator columns of one cohort
+    const int nb = (my_tiles + kSP - 1) / kSP;  // births
+    const int nsteps = nb > 0 ? nb + NG - 1 : 0;
+    constexpr int dcol0 = NG * kSP * kACols;
+    constexpr int dstride = kNC * kSP;  // accumulator columns of one cohort
+    const int D = a.d;
 
     // ---- setup ----
     if (threadIdx.x == 0) {
@@ -255,12 +342,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             bar_init(raw + S.bm_raw + 8u * i, 1);
             bar_init(raw + S.bm_full + 8u * i, 1);
             bar_init(raw + S.bm_empty + 8u * i, kEpiWarps);
-        }
-        for (int i = 0; i < a.ND; ++i) {
             bar_init(raw + S.d_full + 8u * i, 1);
             bar_init(raw + S.d_empty + 8u * i, kEpiWarps);
         }
-        for (int i = 0; i < a.NG; ++i) {
+        for (int i = 0; i < NG; ++i) {
             bar_init(raw + S.a_full + 8u * i, kLoaders);
             bar_init(raw + S.a_empty + 8u * i, kEpiWarps);
         }
@@ -277,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     // for lattice g*kLG + i, column 15 = the out-of-range flag.  K bytes:
     // 4p + e = coordinate 2p + (e >> 1), limb weight (e & 1) ? 128 : 1;
     // 2D = the constant (k = u - kOffset); 2D + 1 = the flag.
-    for (uint32_t e4 = threadIdx.x; e4 < (uint32_t)a.NG * 128u; e4 += blockDim.x) {
+    for (uint32_t e4 = threadIdx.x; e4 < (uint32_t)NG * 128u; e4 += blockDim.x) {
         uint32_t word = 0;
         for (int t = 0; t < 4; ++t) {
             const uint32_t idx = e4 * 4 + t;
@@ -328,8 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         const uint32_t wbytes = (uint32_t)a.W * 4u;
         const int wM = (int)(a.M >> 5), sh = (int)(a.M & 31u);
         auto issue = [&](int s) {
-            const int ring = (int)(s & 1);
-            const int l0 = (int)(s % a.NG) * kLG;
+            const int ring = s & 1;
+            const int l0 = (s % NG) * kLG;
             const int cnt = min(a.L, l0 + kLG) - l0;
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -342,8 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         };
         // bits [M, M + 32 ext_words) := bits [0, 32 ext_words) of every lattice
         auto extend = [&](int s) {
-            const int ring = (int)(s & 1);
-            const int l0 = (int)(s % a.NG) * kLG;
+            const int ring = s & 1;
+            const int l0 = (s % NG) * kLG;
             const int cnt = min(a.L, l0 + kLG) - l0;
             ROLL_T(pt[0], bar_wait(raw + S.bm_raw + 8u * ring, (uint32_t)((s >> 1) & 1)));
             const long long te0 = clock64();
@@ -389,27 +474,37 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         // ================= MMA issuer =================
         const bool leader = elect_one();
         const uint32_t idesc = (2u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
-        int buf = 0, g = 0, cold = 1 % a.NG;
-        uint32_t round = 0;
-        bool first_round = true;
+        uint32_t epar[2] = {1u, 1u};  // parity of the d_empty phase before the next use
+        bool used[2] = {false, false};
+        int sm = 0, beta = 0;
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
         for (int s = 0; s < nsteps; ++s) {
-            const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)g * 512u, 256u, 128u);
-            ROLL_FOR_ITEMS(s, {
-                if (!first_round) ROLL_T(pt[0], bar_wait(raw + S.d_empty + 8u * buf, round ^ 1u));
-                if (age == 0)
-                    ROLL_T(pt[1], bar_wait(raw + S.a_full + 8u * c, (uint32_t)((b / a.NG) & 1)));
+            const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)sm * 512u, 256u, 128u);
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int buf = c & 1;
+                if (used[buf]) ROLL_T(pt[0], bar_wait(raw + S.d_empty + 8u * buf, epar[buf]));
+                used[buf] = true;
+                epar[buf] ^= 1u;
+                if (c == sm && s < nb)  // newborn cohort: its rows are in tensor memory
+                    ROLL_T(pt[1], bar_wait(raw + S.a_full + 8u * c, (uint32_t)(beta & 1)));
                 tc_fence_after();
                 if (leader) {
-                    for (int k = 0; k < ntile; ++k)
+#pragma unroll
+                    for (int k = 0; k < kSP; ++k)
                         umma_i8_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
-                                   tmem + (uint32_t)((c * a.SP + k) * kACols), bdesc, idesc);
+                                   tmem + (uint32_t)((c * kSP + k) * kACols), bdesc, idesc);
                     umma_commit(raw + S.d_full + 8u * buf);
                 }
                 __syncwarp();
-            })
-            if (++g == a.NG) g = 0;
+            }
+            if (++sm == NG) {
+                sm = 0;
+                ++beta;
+            }
         }
         if (PROF && cta == 0 && lane == 0) {
             a.prof[8] = pt[0];
@@ -418,148 +513,42 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         }
     } else if (warp < kEpiWarp0) {
         // ================= row loaders =================
-        const int q = warp & 3;              // TMEM lane quadrant of this warp
-        const int hsel = (warp - 2) >> 2;    // tiles k = hsel (mod 2) of every birth
-        uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + S.stage) + (warp - 2) * 32 * RS;
-        const int4* gbase = reinterpret_cast<const int4*>(a.elems);
-        // unit = (birth b, tile k); rows [t*128 + q*32, +32) of tile t = cta + (b*SP + k)*ncta
-        auto unit_rows = [&](int b, int k) -> int64_t {
-            return ((cta + (int64_t)(b * a.SP + k) * ncta) * kTile + q * 32);
-        };
-        auto valid_unit = [&](int b, int k) -> bool {
-            return b < nb && (b * a.SP + k) < my_tiles;
-        };
-        auto advance = [&](int& b, int& k) {
-            k += 2;
-            if (k >= a.SP) {
-                k = hsel;
-                ++b;
-            }
-        };
-        auto load = [&](int4 (&rawv)[H], int b, int k) {
-            const int64_t r0 = unit_rows(b, k);
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-                const int ch = lane + 32 * i;
-                const int64_t row = r0 + ch / H;
-                rawv[i] = row < a.n ? __ldg(gbase + r0 * H + ch) : make_int4(0, 0, 0, 0);
-            }
-        };
-        auto prefetch = [&](int b, int k) {
-            const char* p = reinterpret_cast<const char*>(a.elems) + unit_rows(b, k) * (8 * D);
-            if (lane * 128 < 32 * 8 * D && unit_rows(b, k) + 32 <= a.n) prefetch_l2(p + lane * 128);
-        };
-        int b = 0;
-        int k = hsel;
-        int arrived = 0;  // births this warp has signalled
-        int waited = -1;  // last birth whose slots this warp knows to be free
-        long long pt[4] = {0, 0, 0, 0};
-        const long long tstart = clock64();
-        int4 cur[H], nxt[H];
-        if (valid_unit(b, k)) load(cur, b, k);
-        {
-            int pb = b;
-            int pk = k;
-            for (int i = 0; i < 4; ++i) {
-                advance(pb, pk);
-                if (valid_unit(pb, pk)) prefetch(pb, pk);
-            }
-        }
-        while (valid_unit(b, k)) {
-            int b2 = b;
-            int k2 = k;
-            advance(b2, k2);
-            const bool more = valid_unit(b2, k2);
-            if (more) load(nxt, b2, k2);
-            {
-                int pb = b2;
-                int pk = k2;
-                for (int i = 0; i < 4; ++i) advance(pb, pk);
-                if (valid_unit(pb, pk)) prefetch(pb, pk);
-            }
-            // pack: one 32-bit word per coordinate pair
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-                const int ch = lane + 32 * i;
-                const uint64_t u0 =
-                    (uint64_t)(((int64_t)(uint32_t)cur[i].x | ((int64_t)cur[i].y << 32)) + kOffset);
-                const uint64_t u1 =
-                    (uint64_t)(((int64_t)(uint32_t)cur[i].z | ((int64_t)cur[i].w << 32)) + kOffset);
-                const uint32_t l0 = (uint32_t)u0, l1 = (uint32_t)u1;
-                uint32_t w = (l0 & 127u) | (((l0 >> 7) & 127u) << 8) | ((l1 & 127u) << 16) |
-                             (((l1 >> 7) & 127u) << 24);
-                if ((u0 | u1) >> 14) w |= 0x80u;
-                stg[(ch / H) * RS + (ch % H)] = w;
-            }
-            __syncwarp();
-            uint32_t r[8];
-            uint32_t bad = 0;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                if (p < H) {
-                    const uint32_t w = stg[lane * RS + p];
-                    bad |= w & 0x80u;
-                    r[p] = w & ~0x80u;
-                } else {
-                    r[p] = 0u;
-                }
-            }
-            // K = 2D: the constant 1; K = 2D + 1: the flag
-            if (H < 8) r[H] = 1u | (bad ? 0x100u : 0u);
-            __syncwarp();
-            const int c = b % a.NG;
-            const int beta = b / a.NG;
-            if (beta >= 1 && waited < b) {
-                ROLL_T(pt[0], bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1)));
-                waited = b;
-            }
-            tc_fence_after();
-            ROLL_T(pt[1], tmem_st8(tmem + ((uint32_t)(q * 32) << 16) +
-                                       (uint32_t)((c * a.SP + k) * kACols), r));
-            if (b2 != b || !more) {  // last unit of this birth for this warp
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
-                arrived = b + 1;
-            }
-            b = b2;
-            k = k2;
-            if (more) {
-#pragma unroll
-                for (int i = 0; i < H; ++i) cur[i] = nxt[i];
-            }
-        }
-        // births in which this warp had no tile (the last, partial one)
-        for (; arrived < nb; ++arrived) {
-            const uint32_t c = (uint32_t)(arrived % a.NG);
-            const int beta = arrived / a.NG;
-            // not before the cohort's previous occupants have retired: an early
-            // arrival would be counted towards THEIR birth
-            if (beta >= 1) bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1));
-            if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
-        }
-        if (PROF && cta == 0 && lane == 0 && warp == 2) {
-            a.prof[16] = pt[0];
-            a.prof[17] = pt[1];
-            a.prof[19] = clock64() - tstart;
+        Ctx x;
+        x.raw = raw;
+        x.tmem = tmem;
+        x.lane = lane;
+        x.warp = warp;
+        x.nb = nb;
+        x.NG = NG;
+        x.cta = cta;
+        x.ncta = ncta;
+        switch (D) {
+            case 4: run_loader<4, PROF>(a, S, x, smem_raw); break;
+            case 6: run_loader<6, PROF>(a, S, x, smem_raw); break;
+            case 8: run_loader<8, PROF>(a, S, x, smem_raw); break;
+            case 10: run_loader<10, PROF>(a, S, x, smem_raw); break;
+            case 12: run_loader<12, PROF>(a, S, x, smem_raw); break;
+            default: run_loader<14, PROF>(a, S, x, smem_raw); break;
         }
     } else {
         // ================= epilogue =================
         const int ew = warp - kEpiWarp0;
-        const int grp = ew >> 2;
+        const int grp = ew >> 2;  // the cohort's tile this warp probes
         const int q = warp & 3;
         const uint32_t negM = a.negM, magic = a.magic;
-        uint8_t* hs = smem_raw + S.hits + q * 32 + lane;
-        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)dcol0;
-        int buf = 0, g = 0, cold = 1 % a.NG;
-        uint32_t round = 0;
-        bool first_round = true;
-        (void)first_round;
+        const uint32_t tlane =
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * grp);
+        const bool lane0 = lane == 0;
+        uint32_t h[NG];
+#pragma unroll
+        for (int c = 0; c < NG; ++c) h[c] = 0;
+        uint32_t par[2] = {0u, 0u};
+        int sm = 0;
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
         for (int s = 0; s < nsteps; ++s) {
             const int ring = s & 1;
-            const int lcg = min(a.L, g * kLG + kLG) - g * kLG;
+            const int lcg = min(a.L, sm * kLG + kLG) - sm * kLG;
             // pair i's bit ends at position 32 - kLG + i of the accumulator
             const uint32_t lmask = ((1u << lcg) - 1u) << (32 - kLG);
             uint32_t lb[kLG];
@@ -570,55 +559,52 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                 lb[i] = t;
             }
             ROLL_T(pt[0], bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1)));
-            ROLL_FOR_ITEMS(s, {
-                ROLL_T(pt[1], bar_wait(raw + S.d_full + 8u * buf, round));
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                const int buf = c & 1;
+                ROLL_T(pt[1], bar_wait(raw + S.d_full + 8u * buf, par[buf]));
+                par[buf] ^= 1u;
                 tc_fence_after();
-                bool freed = false;
-                for (int kk = grp; kk < ntile; kk += kEpiWarps / 4) {
-                    uint32_t v[16];
-                    ROLL_T(pt[2], tmem_ld16(tlane + (uint32_t)(dstride * buf + kNC * kk), v));
-                    if (kk + kEpiWarps / 4 >= ntile) {  // this warp's last tile of the cohort
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
-                        freed = true;
-                    }
-                    if (a.dbg && s == 0 && kk == 0 && cta == 0) {
+                uint32_t v[16];
+                ROLL_T(pt[2], tmem_ld16(tlane + (uint32_t)(dstride * buf), v));
+                tc_fence_before();
+                __syncwarp();
+                if (lane0) bar_arrive(raw + S.d_empty + 8u * buf);
+                if (PROF && a.dbg && s == 0 && c == 0 && grp == 0 && cta == 0) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
-                    }
-                    uint8_t* hp = hs + (c * a.SP + kk) * kTile;
-                    uint32_t hprev = 0;
-                    if (age != 0) hprev = *hp;
-                    // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
-                    uint32_t r[kLG], w[kLG];
+                    for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
+                }
+                // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
+                uint32_t r[kLG], w[kLG];
 #pragma unroll
-                    for (int i = 0; i < kLG; ++i) {
-                        uint32_t x = (v[3 * i + 1] << 8) + v[3 * i];
-                        x = (v[3 * i + 2] << 16) + x;
-                        const uint32_t qq = __umulhi(x, magic);
-                        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(x));
-                    }
+                for (int i = 0; i < kLG; ++i) {
+                    uint32_t xx = (v[3 * i + 1] << 8) + v[3 * i];
+                    xx = (v[3 * i + 2] << 16) + xx;
+                    const uint32_t qq = __umulhi(xx, magic);
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
+                }
 #pragma unroll
-                    for (int i = 0; i < kLG; ++i) {
-                        asm volatile("{\n\t.reg .u32 t;\n\t"
-                                     "shr.u32 t, %1, 3;\n\t"
-                                     "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
-                                     "ld.shared.u32 %0, [t];\n\t}"
-                                     : "=r"(w[i])
-                                     : "r"(r[i]), "r"(lb[i]));
-                    }
-                    uint32_t bacc = 0;
+                for (int i = 0; i < kLG; ++i) {
+                    asm volatile("{\n\t.reg .u32 t;\n\t"
+                                 "shr.u32 t, %1, 3;\n\t"
+                                 "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
+                                 "ld.shared.u32 %0, [t];\n\t}"
+                                 : "=r"(w[i])
+                                 : "r"(r[i]), "r"(lb[i]));
+                }
+                uint32_t bacc = 0;
 #pragma unroll
-                    for (int i = 0; i < kLG; ++i)
-                        bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], r[i]), 1);
-                    const uint32_t h = __popc(bacc & lmask) + hprev;
-                    if (age == a.NG - 1) {
-                        const int64_t t = cta + (int64_t)(b * a.SP + kk) * ncta;
+                for (int i = 0; i < kLG; ++i)
+                    bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], r[i]), 1);
+                h[c] += __popc(bacc & lmask);
+                if (sm == (c + NG - 1) % NG) {  // the cohort born at step s - (NG - 1) retires
+                    const int b = s - (NG - 1);
+                    if (b >= 0) {  // b < nb holds: s < nb + NG - 1
+                        const int64_t t = cta + (int64_t)(b * kSP + grp) * ncta;
                         const int64_t row0 = t * kTile + q * 32;
                         const int64_t row = row0 + lane;
                         const bool valid = row < a.n;
-                        int64_t hits = (int64_t)h;
+                        int64_t hits = (int64_t)h[c];
                         if (v[15] != 0u && valid) {
                             hits = exact_row_hits(a, D, row);
                             atomicAdd(a.recomputed, 1ull);
@@ -626,24 +612,16 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                         const unsigned det =
                             __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
                         if (valid && a.hits64) a.hits64[row] = hits;
-                        if (lane == 0 && row0 < a.n) a.detmask[row0 >> 5] = det;
-                    } else {
-                        *hp = (uint8_t)h;
+                        if (lane0 && row0 < a.n) a.detmask[row0 >> 5] = det;
+                        __syncwarp();
+                        if (lane0) bar_arrive(raw + S.a_empty + 8u * c);
                     }
+                    h[c] = 0;
                 }
-                if (!freed) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) bar_arrive(raw + S.d_empty + 8u * buf);
-                }
-                if (age == a.NG - 1) {
-                    __syncwarp();
-                    if (lane == 0) bar_arrive(raw + S.a_empty + 8u * c);
-                }
-            })
+            }
             __syncwarp();
-            if (lane == 0) bar_arrive(raw + S.bm_empty + 8u * ring);
-            if (++g == a.NG) g = 0;
+            if (lane0) bar_arrive(raw + S.bm_empty + 8u * ring);
+            if (++sm == NG) sm = 0;
         }
         if (PROF && cta == 0 && lane == 0 && (ew == 0 || ew == 15)) {
             long long* o = a.prof + (ew == 0 ? 24 : 32);
@@ -676,16 +654,16 @@ static unsigned long long* recomputed_counter() {
     return p;
 }
 
-template <int D>
-static int launch_d(Args& a, uint32_t smem, int grid, cudaStream_t st) {
-    if (D == 10 && a.prof) {
+template <int NG>
+static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
+    if (NG == 10 && a.prof) {
         auto kp = hash_roll_kernel<10, true>;
         SFFTB_CUDA(smem_opt_in(kp, smem));
         kp<<<grid, kThreads, smem, st>>>(a);
         SFFTB_CHECK_LAUNCH();
         return SFFTB_OK;
     }
-    auto kern = hash_roll_kernel<D, false>;
+    auto kern = hash_roll_kernel<NG, false>;
     SFFTB_CUDA(smem_opt_in(kern, smem));
     kern<<<grid, kThreads, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
@@ -724,15 +702,8 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     uint32_t S2 = 64;
     while ((int64_t)S2 < std::max(need_words, W) * 4) S2 <<= 1;
     const int NG = (int)((L + kLG - 1) / kLG);
-    // tiles per cohort: 8 when two accumulator buffers still fit, else 4
     if (NG > kMaxNG) return 0;
-    int SP = 8;
-    if (512 - NG * SP * kACols < 2 * kNC * SP) SP = 4;
-    if (512 - NG * SP * kACols < 2 * kNC * SP) return 0;
-    const int TA = NG * SP;
-    const int ND = std::min(kMaxND, (512 - TA * kACols) / (kNC * SP));
-    const int RS = (int)(d / 2) | 1;
-    const Smem S = smem_map(NG, TA, RS);
+    const Smem S = smem_map(NG);
     const uint32_t smem = S.end + S2 + 2u * kLG * S2;
     static int prop_smem = 0;
     if (prop_smem == 0) {
@@ -749,11 +720,9 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.elems = elems;
     a.n = n;
     a.zmat = zmat;
+    a.d = (int)d;
     a.L = (int)L;
     a.NG = NG;
-    a.SP = SP;
-    a.TA = TA;
-    a.ND = ND;
     a.M = (uint32_t)M;
     a.negM = 0u - (uint32_t)M;
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
@@ -768,7 +737,7 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.recomputed = rec;
     a.dbg = nullptr;
     static int32_t* dbg = nullptr;
-    if (getenv("SFFTB_HASH_ROLL_DUMP")) {
+    if (getenv("SFFTB_HASH_ROLL_DUMP") && getenv("SFFTB_HASH_ROLL_PROF")) {
         if (!dbg) SFFTB_CUDA(cudaMalloc(&dbg, 128 * 16 * sizeof(int32_t)));
         SFFTB_CUDA(cudaMemsetAsync(dbg, 0xFF, 128 * 16 * sizeof(int32_t), st));
         a.dbg = dbg;
@@ -784,16 +753,22 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     if (const char* e = getenv("SFFTB_HASH_ROLL_GRID")) grid = std::max(1, atoi(e));
     grid = (int)std::min<int64_t>(grid, a.ntiles);
     if (getenv("SFFTB_HASH_ROLL_DEBUG"))
-        fprintf(stderr, "hash_roll: d=%d L=%d NG=%d SP=%d TA=%d ND=%d S2=%u ext_words=%d smem=%u grid=%d\n",
-                (int)d, (int)L, NG, SP, TA, ND, S2, (int)ext_words, smem, grid);
+        fprintf(stderr, "hash_roll: d=%d L=%d NG=%d S2=%u ext_words=%d smem=%u grid=%d\n",
+                (int)d, (int)L, NG, S2, (int)ext_words, smem, grid);
     int rc = SFFTB_EINVAL;
-    switch (d) {
-        case 4: rc = launch_d<4>(a, smem, grid, st); break;
-        case 6: rc = launch_d<6>(a, smem, grid, st); break;
-        case 8: rc = launch_d<8>(a, smem, grid, st); break;
-        case 10: rc = launch_d<10>(a, smem, grid, st); break;
-        case 12: rc = launch_d<12>(a, smem, grid, st); break;
-        case 14: rc = launch_d<14>(a, smem, grid, st); break;
+    switch (NG) {
+        case 1: rc = launch_ng<1>(a, smem, grid, st); break;
+        case 2: rc = launch_ng<2>(a, smem, grid, st); break;
+        case 3: rc = launch_ng<3>(a, smem, grid, st); break;
+        case 4: rc = launch_ng<4>(a, smem, grid, st); break;
+        case 5: rc = launch_ng<5>(a, smem, grid, st); break;
+        case 6: rc = launch_ng<6>(a, smem, grid, st); break;
+        case 7: rc = launch_ng<7>(a, smem, grid, st); break;
+        case 8: rc = launch_ng<8>(a, smem, grid, st); break;
+        case 9: rc = launch_ng<9>(a, smem, grid, st); break;
+        case 10: rc = launch_ng<10>(a, smem, grid, st); break;
+        case 11: rc = launch_ng<11>(a, smem, grid, st); break;
+        case 12: rc = launch_ng<12>(a, smem, grid, st); break;
     }
     if (a.dbg && rc == SFFTB_OK) {
         static int32_t h[128 * 16];
