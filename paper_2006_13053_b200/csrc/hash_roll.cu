@@ -69,6 +69,7 @@ struct Args {
     int64_t* hits64;   // may be null
     uint32_t* detmask;
     unsigned long long* recomputed;
+    unsigned int* nbad;  // warps that met a row outside the limb range (this launch)
     int32_t* dbg;  // diagnostics: the 128 x 16 accumulators of tile 0, step 0
     long long* prof;  // diagnostics: cycle counters of CTA 0 (SFFTB_HASH_ROLL_PROF)
 };
@@ -155,7 +156,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 }
 
 // Exact hits of one row from global memory (a coordinate outside the limb range).
-__device__ __noinline__ int exact_row_hits(const Args& a, int d, int64_t row) {
+__device__ int exact_row_hits(const Args& a, int d, int64_t row) {
     int h = 0;
     for (int l = 0; l < a.L; ++l) {
         uint64_t acc = 0;
@@ -172,6 +173,28 @@ __device__ __noinline__ int exact_row_hits(const Args& a, int d, int64_t row) {
     return h;
 }
 
+// Runs after every hash_roll_kernel launch: exits at once unless the main
+// kernel met a row outside the limb range; otherwise finds those rows again
+// (same range test), recomputes their hits exactly and repairs hits64 and the
+// detected bit.
+__global__ void __launch_bounds__(256) roll_fixup_kernel(Args a) {
+    if (*reinterpret_cast<volatile unsigned int*>(a.nbad) == 0u) return;
+    const int d = a.d;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < a.n;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        bool bad = false;
+        for (int j = 0; j < d; ++j)
+            bad |= ((uint64_t)(a.elems[row * d + j] + kOffset) >> 14) != 0;
+        if (!bad) continue;
+        const int64_t hits = exact_row_hits(a, d, row);
+        atomicAdd(a.recomputed, 1ull);
+        if (a.hits64) a.hits64[row] = hits;
+        const uint32_t bit = 1u << (row & 31);
+        if (hits >= a.min_hits) atomicOr(a.detmask + (row >> 5), bit);
+        else atomicAnd(a.detmask + (row >> 5), ~bit);
+    }
+}
+
 // Shared-memory map: byte offsets from the dynamic base (the two bitmap ring
 // slots follow at the next S2-aligned address).
 struct Smem {
@@ -184,8 +207,8 @@ __host__ __device__ inline Smem smem_map(int NG) {
     s.bm_raw = o;   o += 16;
     s.bm_full = o;  o += 16;
     s.bm_empty = o; o += 16;
-    s.d_full = o;   o += 16;
-    s.d_empty = o;  o += 16;
+    s.d_full = o;   o += 32;
+    s.d_empty = o;  o += 32;
     s.a_full = o;   o += 8u * kMaxNG;
     s.a_empty = o;  o += 8u * kMaxNG;
     s.tmem_holder = o; o += 16;
@@ -334,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     const int nsteps = nb > 0 ? nb + NG - 1 : 0;
     constexpr int dcol0 = NG * kSP * kACols;
     constexpr int dstride = kNC * kSP;  // accumulator columns of one cohort
+    // accumulator buffers: cohort c uses buffer c % ND (static; when NG is not
+    // a multiple of ND the step boundary reuses one buffer back to back)
+    constexpr int ND = (dcol0 + 3 * dstride <= 512 && NG >= 3) ? 3 : 2;
     const int D = a.d;
 
     // ---- setup ----
@@ -342,6 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             bar_init(raw + S.bm_raw + 8u * i, 1);
             bar_init(raw + S.bm_full + 8u * i, 1);
             bar_init(raw + S.bm_empty + 8u * i, kEpiWarps);
+        }
+        for (int i = 0; i < ND; ++i) {
             bar_init(raw + S.d_full + 8u * i, 1);
             bar_init(raw + S.d_empty + 8u * i, kEpiWarps);
         }
@@ -474,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         // ================= MMA issuer =================
         const bool leader = elect_one();
         const uint32_t idesc = (2u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
-        uint32_t epar[2] = {1u, 1u};  // parity of the d_empty phase before the next use
-        bool used[2] = {false, false};
+        uint32_t epar[3] = {1u, 1u, 1u};  // parity of the d_empty phase before the next use
+        bool used[3] = {false, false, false};
         int sm = 0, beta = 0;
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
@@ -483,9 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)sm * 512u, 256u, 128u);
 #pragma unroll
             for (int c = 0; c < NG; ++c) {
-                constexpr int dummy = 0;
-                (void)dummy;
-                const int buf = c & 1;
+                const int buf = c % ND;
                 if (used[buf]) ROLL_T(pt[0], bar_wait(raw + S.d_empty + 8u * buf, epar[buf]));
                 used[buf] = true;
                 epar[buf] ^= 1u;
@@ -536,13 +562,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         const int grp = ew >> 2;  // the cohort's tile this warp probes
         const int q = warp & 3;
         const uint32_t negM = a.negM, magic = a.magic;
-        const uint32_t tlane =
-            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * grp);
+        uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * grp);
+        asm volatile("" : "+r"(tlane));
         const bool lane0 = lane == 0;
+        uint32_t dfull = raw + S.d_full, dempty = raw + S.d_empty;
+        asm volatile("" : "+r"(dfull), "+r"(dempty));  // not rematerialised per item
         uint32_t h[NG];
 #pragma unroll
         for (int c = 0; c < NG; ++c) h[c] = 0;
-        uint32_t par[2] = {0u, 0u};
+        uint32_t par[3] = {0u, 0u, 0u};
         int sm = 0;
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
@@ -561,15 +589,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             ROLL_T(pt[0], bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1)));
 #pragma unroll
             for (int c = 0; c < NG; ++c) {
-                const int buf = c & 1;
-                ROLL_T(pt[1], bar_wait(raw + S.d_full + 8u * buf, par[buf]));
+                const int buf = c % ND;
+                ROLL_T(pt[1], bar_wait(dfull + 8u * buf, par[buf]));
                 par[buf] ^= 1u;
                 tc_fence_after();
                 uint32_t v[16];
                 ROLL_T(pt[2], tmem_ld16(tlane + (uint32_t)(dstride * buf), v));
                 tc_fence_before();
                 __syncwarp();
-                if (lane0) bar_arrive(raw + S.d_empty + 8u * buf);
+                if (lane0) bar_arrive(dempty + 8u * buf);
                 if (PROF && a.dbg && s == 0 && c == 0 && grp == 0 && cta == 0) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
@@ -604,11 +632,11 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                         const int64_t row0 = t * kTile + q * 32;
                         const int64_t row = row0 + lane;
                         const bool valid = row < a.n;
-                        int64_t hits = (int64_t)h[c];
-                        if (v[15] != 0u && valid) {
-                            hits = exact_row_hits(a, D, row);
-                            atomicAdd(a.recomputed, 1ull);
-                        }
+                        const int64_t hits = (int64_t)h[c];
+                        // rows outside the limb range: counted here, redone
+                        // exactly by roll_fixup_kernel
+                        if (__any_sync(0xffffffffu, v[15] != 0u && valid) && lane0)
+                            atomicAdd(a.nbad, 1u);
                         const unsigned det =
                             __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
                         if (valid && a.hits64) a.hits64[row] = hits;
@@ -646,8 +674,8 @@ static unsigned long long* recomputed_counter() {
     static unsigned long long* p = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
-        if (cudaMalloc(&p, sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(p, 0, sizeof(unsigned long long));
+        if (cudaMalloc(&p, 2 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(p, 0, 2 * sizeof(unsigned long long));
         else
             p = nullptr;
     });
@@ -735,6 +763,8 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.hits64 = hits64;
     a.detmask = detmask;
     a.recomputed = rec;
+    a.nbad = reinterpret_cast<unsigned int*>(rec + 1);
+    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, sizeof(unsigned int), st));
     a.dbg = nullptr;
     static int32_t* dbg = nullptr;
     if (getenv("SFFTB_HASH_ROLL_DUMP") && getenv("SFFTB_HASH_ROLL_PROF")) {
@@ -769,6 +799,11 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
         case 10: rc = launch_ng<10>(a, smem, grid, st); break;
         case 11: rc = launch_ng<11>(a, smem, grid, st); break;
         case 12: rc = launch_ng<12>(a, smem, grid, st); break;
+    }
+    if (rc == SFFTB_OK) {
+        roll_fixup_kernel<<<4 * num_sms(), 256, 0, st>>>(a);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) rc = SFFTB_ECUDA;
     }
     if (a.dbg && rc == SFFTB_OK) {
         static int32_t h[128 * 16];
