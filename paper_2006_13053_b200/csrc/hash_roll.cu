@@ -19,7 +19,7 @@
 //  * the epilogue reduces x with ONE multiply-high (q = umulhi(x, 2^32/M) is
 //    floor(x/M) or one less, so x - qM < M + ext with ext = ceil(M x_max /
 //    2^32)) and probes a bitmap whose first ext bits are repeated after bit
-//    M, built in shared memory after the bulk copy lands;
+//    M (roll_extend_kernel writes these once per call);
 //  * bitmaps arrive by 1-D bulk copies, one group (5 lattices) per step,
 //    double buffered; a step applies its group to every resident tile.  Tiles
 //    are organised in NG cohorts (NG = groups per pass): at step s the cohort
@@ -62,6 +62,8 @@ struct Args {
     uint32_t M, negM, magic;
     const uint32_t* bits;  // (L, W)
     int W;                 // words per lattice in global memory
+    const uint32_t* xbits; // (L, Wx) wrap-extended bitmaps (roll_extend_kernel)
+    int Wx;
     int ext_words;         // words rewritten/appended from word M >> 5 on
     uint32_t S2;           // shared-memory stride per lattice bitmap (power of two)
     int64_t ntiles;
@@ -147,6 +149,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// asynchronous variant: the registers hold the data only after tmem_wait_ld16,
+// whose in/out operands keep every use of them behind the wait
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                   "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                   "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+                 :
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
@@ -193,6 +214,35 @@ __global__ void __launch_bounds__(256) roll_fixup_kernel(Args a) {
         if (hits >= a.min_hits) atomicOr(a.detmask + (row >> 5), bit);
         else atomicAnd(a.detmask + (row >> 5), ~bit);
     }
+}
+
+// Wrap-extended bitmaps: words [0, Wx) per lattice, bits [M, M + 32 ext_words)
+// repeating bits [0, 32 ext_words).  One thread per output word.
+__global__ void __launch_bounds__(256) roll_extend_kernel(const uint32_t* __restrict__ bits,
+                                                          int L, int W, int Wx, uint32_t M,
+                                                          int ext_words,
+                                                          uint32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L * Wx) return;
+    const int l = i / Wx, w = i % Wx;
+    const uint32_t* bm = bits + (int64_t)l * W;
+    const int wM = (int)(M >> 5), sh = (int)(M & 31u);
+    uint32_t v = 0;
+    if (w < wM) {
+        v = bm[w];
+    } else {
+        const int e = w - wM;  // word e of the repeated part
+        if (e <= ext_words) {
+            if (sh == 0) {
+                v = e < ext_words ? bm[e] : 0u;
+            } else {
+                const uint32_t lo = e == 0 ? (bm[wM] & ((1u << sh) - 1u)) : (bm[e - 1] >> (32 - sh));
+                const uint32_t hi = e < ext_words ? (bm[e] << sh) : 0u;
+                v = lo | hi;
+            }
+        }
+    }
+    out[i] = v;
 }
 
 // Shared-memory map: byte offsets from the dynamic base (the two bitmap ring
@@ -438,59 +488,25 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         // ================= bitmap producer =================
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
-        const uint32_t wbytes = (uint32_t)a.W * 4u;
-        const int wM = (int)(a.M >> 5), sh = (int)(a.M & 31u);
+        const uint32_t wbytes = (uint32_t)a.Wx * 4u;
         auto issue = [&](int s) {
             const int ring = s & 1;
             const int l0 = (s % NG) * kLG;
             const int cnt = min(a.L, l0 + kLG) - l0;
             if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t bar = raw + S.bm_raw + 8u * ring;
+                const uint32_t bar = raw + S.bm_full + 8u * ring;
                 bar_expect_tx(bar, wbytes * (uint32_t)cnt);
                 for (int i = 0; i < cnt; ++i)
                     bulk_g2s_a(ring0 + (uint32_t)ring * ring_bytes + (uint32_t)i * a.S2,
-                               a.bits + (int64_t)(l0 + i) * a.W, wbytes, bar);
+                               a.xbits + (int64_t)(l0 + i) * a.Wx, wbytes, bar);
             }
-        };
-        // bits [M, M + 32 ext_words) := bits [0, 32 ext_words) of every lattice
-        auto extend = [&](int s) {
-            const int ring = s & 1;
-            const int l0 = (s % NG) * kLG;
-            const int cnt = min(a.L, l0 + kLG) - l0;
-            ROLL_T(pt[0], bar_wait(raw + S.bm_raw + 8u * ring, (uint32_t)((s >> 1) & 1)));
-            const long long te0 = clock64();
-            uint32_t* base = reinterpret_cast<uint32_t*>(smem_raw + (ring0 - raw) +
-                                                         (uint32_t)ring * ring_bytes);
-            for (int i = 0; i < cnt; ++i) {
-                uint32_t* bm = base + (size_t)i * (a.S2 / 4);
-                for (int w = lane; w <= a.ext_words; w += 32) {
-                    uint32_t v;
-                    if (sh == 0) {
-                        v = w < a.ext_words ? bm[w] : 0u;
-                    } else {
-                        const uint32_t lo =
-                            w == 0 ? (bm[wM] & ((1u << sh) - 1u)) : (bm[w - 1] >> (32 - sh));
-                        const uint32_t hi = w < a.ext_words ? (bm[w] << sh) : 0u;
-                        v = lo | hi;
-                    }
-                    bm[wM + w] = v;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) bar_arrive(raw + S.bm_full + 8u * ring);
-            pt[1] += clock64() - te0;
         };
         if (nsteps > 0) issue(0);
         if (nsteps > 1) issue(1);
-        if (nsteps > 0) extend(0);
-        for (int s = 0; s < nsteps; ++s) {
-            if (s + 1 < nsteps) extend(s + 1);
-            if (s + 2 < nsteps) {
-                ROLL_T(pt[2], bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1),
-                                       (uint32_t)((s >> 1) & 1)));
-                issue(s + 2);
-            }
+        for (int s = 0; s + 2 < nsteps; ++s) {
+            ROLL_T(pt[2], bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1),
+                                   (uint32_t)((s >> 1) & 1)));
+            issue(s + 2);
         }
         if (PROF && cta == 0 && lane == 0) {
             a.prof[0] = pt[0];
@@ -567,13 +583,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
         const bool lane0 = lane == 0;
         uint32_t dfull = raw + S.d_full, dempty = raw + S.d_empty;
         asm volatile("" : "+r"(dfull), "+r"(dempty));  // not rematerialised per item
-        uint32_t h[NG];
+        // running hit counts of this thread's row in every cohort, one byte each
+        uint32_t hp[(NG + 3) / 4];
 #pragma unroll
-        for (int c = 0; c < NG; ++c) h[c] = 0;
+        for (int i = 0; i < (NG + 3) / 4; ++i) hp[i] = 0;
         uint32_t par[3] = {0u, 0u, 0u};
         int sm = 0;
         long long pt[4] = {0, 0, 0, 0};
         const long long tstart = clock64();
+        uint32_t va[16], vb[16];
         for (int s = 0; s < nsteps; ++s) {
             const int ring = s & 1;
             const int lcg = min(a.L, sm * kLG + kLG) - sm * kLG;
@@ -587,20 +605,27 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                 lb[i] = t;
             }
             ROLL_T(pt[0], bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1)));
+            // accumulators of cohort 0; cohort c + 1 is fetched while c is probed
+            ROLL_T(pt[1], bar_wait(dfull, par[0]));
+            par[0] ^= 1u;
+            tc_fence_after();
+            tmem_ld16_async(tlane, va);
+            tmem_wait_ld16(va);
+            tc_fence_before();
+            __syncwarp();
+            if (lane0) bar_arrive(dempty);
 #pragma unroll
             for (int c = 0; c < NG; ++c) {
-                const int buf = c % ND;
-                ROLL_T(pt[1], bar_wait(dfull + 8u * buf, par[buf]));
-                par[buf] ^= 1u;
-                tc_fence_after();
-                uint32_t v[16];
-                ROLL_T(pt[2], tmem_ld16(tlane + (uint32_t)(dstride * buf), v));
-                tc_fence_before();
-                __syncwarp();
-                if (lane0) bar_arrive(dempty + 8u * buf);
-                if (PROF && a.dbg && s == 0 && c == 0 && grp == 0 && cta == 0) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = (int32_t)v[i];
+                uint32_t(&v)[16] = (c & 1) ? vb : va;
+                uint32_t(&vn)[16] = (c & 1) ? va : vb;
+                constexpr int kDummy = 0;
+                (void)kDummy;
+                const int bn = (c + 1) % ND;
+                if (c + 1 < NG) {
+                    ROLL_T(pt[1], bar_wait(dfull + 8u * bn, par[bn]));
+                    par[bn] ^= 1u;
+                    tc_fence_after();
+                    tmem_ld16_async(tlane + (uint32_t)(dstride * bn), vn);
                 }
                 // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
                 uint32_t r[kLG], w[kLG];
@@ -624,18 +649,27 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
 #pragma unroll
                 for (int i = 0; i < kLG; ++i)
                     bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], r[i]), 1);
-                h[c] += __popc(bacc & lmask);
+                hp[c >> 2] += __popc(bacc & lmask) << (8 * (c & 3));
+                const uint32_t flag = v[15];
+                if (c + 1 < NG) {
+                    tmem_wait_ld16(vn);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane0) bar_arrive(dempty + 8u * bn);
+                }
                 if (sm == (c + NG - 1) % NG) {  // the cohort born at step s - (NG - 1) retires
                     const int b = s - (NG - 1);
+                    const uint32_t hc = (hp[c >> 2] >> (8 * (c & 3))) & 255u;
+                    hp[c >> 2] &= ~(255u << (8 * (c & 3)));
                     if (b >= 0) {  // b < nb holds: s < nb + NG - 1
                         const int64_t t = cta + (int64_t)(b * kSP + grp) * ncta;
                         const int64_t row0 = t * kTile + q * 32;
                         const int64_t row = row0 + lane;
                         const bool valid = row < a.n;
-                        const int64_t hits = (int64_t)h[c];
+                        const int64_t hits = (int64_t)hc;
                         // rows outside the limb range: counted here, redone
                         // exactly by roll_fixup_kernel
-                        if (__any_sync(0xffffffffu, v[15] != 0u && valid) && lane0)
+                        if (__any_sync(0xffffffffu, flag != 0u && valid) && lane0)
                             atomicAdd(a.nbad, 1u);
                         const unsigned det =
                             __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
@@ -644,7 +678,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                         __syncwarp();
                         if (lane0) bar_arrive(raw + S.a_empty + 8u * c);
                     }
-                    h[c] = 0;
                 }
             }
             __syncwarp();
@@ -726,9 +759,9 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     const int64_t ext = (int64_t)(((__int128)M * xmax) >> 32) + 2;
     const int64_t ext_words = (ext + 31) / 32 + 1;
     if (ext_words >= (M >> 5)) return 0;
-    const int64_t need_words = (M >> 5) + ext_words + 2;
+    const int64_t Wx = ((M >> 5) + ext_words + 1 + 3) & ~int64_t(3);
     uint32_t S2 = 64;
-    while ((int64_t)S2 < std::max(need_words, W) * 4) S2 <<= 1;
+    while ((int64_t)S2 < Wx * 4) S2 <<= 1;
     const int NG = (int)((L + kLG - 1) / kLG);
     if (NG > kMaxNG) return 0;
     const Smem S = smem_map(NG);
@@ -756,6 +789,10 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
     a.bits = bits;
     a.W = (int)W;
+    uint32_t* xbits = nullptr;
+    SFFTB_CUDA(cudaMallocAsync(&xbits, (size_t)L * Wx * sizeof(uint32_t), st));
+    a.xbits = xbits;
+    a.Wx = (int)Wx;
     a.ext_words = (int)ext_words;
     a.S2 = S2;
     a.ntiles = (n + kTile - 1) / kTile;
@@ -785,6 +822,9 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     if (getenv("SFFTB_HASH_ROLL_DEBUG"))
         fprintf(stderr, "hash_roll: d=%d L=%d NG=%d S2=%u ext_words=%d smem=%u grid=%d\n",
                 (int)d, (int)L, NG, S2, (int)ext_words, smem, grid);
+    roll_extend_kernel<<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
+        bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
+    count_launch();
     int rc = SFFTB_EINVAL;
     switch (NG) {
         case 1: rc = launch_ng<1>(a, smem, grid, st); break;
@@ -805,6 +845,7 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
         count_launch();
         if (cudaGetLastError() != cudaSuccess) rc = SFFTB_ECUDA;
     }
+    cudaFreeAsync(xbits, st);
     if (a.dbg && rc == SFFTB_OK) {
         static int32_t h[128 * 16];
         cudaStreamSynchronize(st);
