@@ -305,13 +305,26 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
     };
     auto load = [&](int4 (&rawv)[H], int b, int k) {
         const int64_t r0 = unit_rows(b, k);
+        const int4* src = gbase + r0 * H + lane;
+        if (r0 + 32 <= a.n) {  // the whole unit is inside the set
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-            const int ch = lane + 32 * i;
-            const int64_t row = r0 + ch / H;
-            rawv[i] = row < a.n ? __ldg(gbase + r0 * H + ch) : make_int4(0, 0, 0, 0);
+            for (int i = 0; i < H; ++i) rawv[i] = __ldg(src + 32 * i);
+        } else {
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const int64_t row = r0 + (lane + 32 * i) / H;
+                rawv[i] = row < a.n ? __ldg(src + 32 * i) : make_int4(0, 0, 0, 0);
+            }
         }
     };
+    // word (row, pair) of chunk lane + 32 i in the transposition buffer
+    const uint32_t stg_a = smem_addr(stg);
+    uint32_t sdst[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        const int ch = lane + 32 * i;
+        sdst[i] = stg_a + 4u * (uint32_t)((ch / H) * RS + (ch % H));
+    }
     auto prefetch = [&](int b, int k) {
         const int64_t r0 = unit_rows(b, k);
         const char* p = reinterpret_cast<const char*>(a.elems) + r0 * (8 * D);
@@ -337,16 +350,16 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
             }
 #pragma unroll
             for (int i = 0; i < H; ++i) {
-                const int ch = lane + 32 * i;
-                const uint64_t u0 =
-                    (uint64_t)(((int64_t)(uint32_t)cur[i].x | ((int64_t)cur[i].y << 32)) + kOffset);
-                const uint64_t u1 =
-                    (uint64_t)(((int64_t)(uint32_t)cur[i].z | ((int64_t)cur[i].w << 32)) + kOffset);
-                const uint32_t l0 = (uint32_t)u0, l1 = (uint32_t)u1;
-                uint32_t w = (l0 & 127u) | (((l0 >> 7) & 127u) << 8) | ((l1 & 127u) << 16) |
-                             (((l1 >> 7) & 127u) << 24);
-                if ((u0 | u1) >> 14) w |= 0x80u;
-                stg[(ch / H) * RS + (ch % H)] = w;
+                // k in [-2^13, 2^13) <=> high word = sign of the low word and
+                // (low + 2^13) < 2^14
+                const uint32_t l0 = (uint32_t)cur[i].x + (uint32_t)kOffset;
+                const uint32_t l1 = (uint32_t)cur[i].z + (uint32_t)kOffset;
+                const uint32_t o0 = (l0 >> 14) | (uint32_t)(cur[i].y ^ (cur[i].x >> 31));
+                const uint32_t o1 = (l1 >> 14) | (uint32_t)(cur[i].w ^ (cur[i].z >> 31));
+                uint32_t w = (l0 & 127u) | ((l0 << 1) & 0x7F00u) | ((l1 & 127u) << 16) |
+                             ((l1 << 17) & 0x7F000000u);
+                if (o0 | o1) w |= 0x80u;
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst[i]), "r"(w) : "memory");
             }
             __syncwarp();
             uint32_t r[8];
@@ -740,11 +753,13 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
                    uint32_t* detmask, cudaStream_t st) {
     using namespace roll;
     {
+        // on by default; SFFTB_HASH_ROLL=0 keeps the CUDA-core kernel
         const char* e = getenv("SFFTB_HASH_ROLL");
-        if (!e || e[0] != '1') return 0;
+        if (e && e[0] == '0') return 0;
     }
     const char* mr = getenv("SFFTB_HASH_ROLL_MINROWS");
-    const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 18;
+    // measured break-even against hash_rows at the config-4 shape: ~2^21 rows
+    const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 21;
     if (n < min_rows || n > ((int64_t)1 << 36) || L < 1 || L > 255 || M < 64 ||
         M >= ((int64_t)1 << 24))
         return 0;
