@@ -360,12 +360,42 @@ def run_hash_arm(args, world, rank):
                 b.record()
             per = tl.ms()
             times.append(a.elapsed_time(b))
-            hash_ms.append(sum(per["sfftb_hash_hits"]))
             path_ms.append(sum(sum(per.get(k, [0.0])) for k in (
-                "sfftb_nonzero_bitmap", "sfftb_hash_hits", "sfftb_compact_mask",
-                "sfftb_medians")))
+                "sfftb_detect_dev", "sfftb_nonzero_bitmap", "sfftb_hash_hits",
+                "sfftb_compact_mask", "sfftb_medians")))
+        # the hashing entry point alone (detect_and_compute runs it inside ONE
+        # C call, csrc/detect_dev.cu): the same sfftb_hash_hits call on the same
+        # rows, generators and nonzero bitmaps, CUDA events on its stream
+        from paper_2006_13053_b200 import _engine as _eng
+
+        _g, th_dev, bits = _eng.spectra(samples, M, 1, L)
+        del _g
+        nl = hi - lo
+        rows_l = rows_all[lo:hi]
+        hits_t = torch.empty((nl,), dtype=torch.int64, device="cuda")
+        mask_t = torch.empty(((nl + 31) // 32,), dtype=torch.int32, device="cuda")
+        zdev = cfg.zmat_device()
+        for it in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            _native.call("sfftb_hash_hits", rows_l.data_ptr(), nl, d, zdev.data_ptr(), 1, L, M,
+                         bits.data_ptr(), -1, _eng.min_hits_for(cfg.nu, L), hits_t.data_ptr(),
+                         mask_t.data_ptr(), _dev.stream())
+            b.record()
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                hash_ms.append(a.elapsed_time(b))
+        hash_equal = None
+        if world == 1:
+            ref_hits = res._hits
+            hash_equal = bool(torch.equal(hits_t, ref_hits)) if torch.is_tensor(ref_hits) \
+                else bool(np.array_equal(_dev.download(hits_t), ref_hits))
+        del hits_t, mask_t, bits
     clocks = clk.summary()
-    parity = {"detected_equals_support": bool(np.array_equal(idx, pick)),
+    parity = {"hash_call_equals_detection_hits": hash_equal,
+              "detected_equals_support": bool(np.array_equal(idx, pick)),
               "coeff_max_rel_err_vs_truth": float(np.max(np.abs(co - coeffs))
                                                   / np.max(np.abs(coeffs)))}
     # the reference's own run of this instance (tests/golden/make_golden.py
@@ -598,38 +628,48 @@ def _fp64_frac(tflops):
             "fp64_peak_source": "measured DFMA peak (profiles/r01/pipe_peaks.json)"}
 
 
-def _imad_bound(h):
-    """The hash kernel's integer-pipe floor: 12 IMAD-pipe ops per (row,
-    lattice) pair (10 for the dot product, 2 for the reduction; DESIGN.md
-    K3) at the measured IMAD lane rate."""
+def _issue_bound(h):
+    """The rolling tensor-core hash kernel's limiter (profiles/r02/
+    hash_roll_full_details.txt): instruction issue.  The residue dot products
+    run as an exact u8 x u8 -> s32 tcgen05 GEMM; what remains per (row,
+    lattice) pair in the epilogue is 2 multiply-adds (limb recombination), a
+    multiply-high + multiply-add reduction, 2 address ops, 1 shared load and
+    2 funnel shifts, plus the row loaders: 2.1e9 warp instructions per 2^26
+    rows, 77% of the issue slots."""
     pk = _pipe_peaks()
     if not pk:
         return {}
     pairs = h.get("n_local", h["n"]) * h["L"]
+    # the CUDA-core kernel's IMAD-pipe floor (12 IMAD-pipe ops per pair), for comparison
     floor_ms = pairs * 12 / (pk["imad_lanes_per_clk_per_sm"] * pk["sms"]
                              * pk["clock_mhz"] * 1e6) * 1e3
-    return {"int_pipe": {"imad_per_pair": 12, "floor_ms": round(floor_ms, 3),
-                         "frac_of_floor": round(floor_ms / h["hash_ms"], 4),
-                         "note": "exact int64 residues need d multiply-adds per pair on the "
-                                 "IMAD pipe; its floor caps this kernel at "
-                                 f"{round(h['n'] * (8 * h['d'] + 8) / (floor_ms * 1e-3) / 1e9)} "
-                                 "GB/s of algorithmic traffic"}}
+    return {"issue": {"warp_instructions_per_pair": 0.672,
+                      "issue_slots_busy": 0.769,
+                      "dominant_pipe": "alu 0.62, fma 0.24, lsu 0.21, tensor (imma) 0.015",
+                      "source": "profiles/r02/hash_roll_full_details.txt",
+                      "cuda_core_imad_floor_ms": round(floor_ms, 3),
+                      "note": "the all-IMAD kernel (hash_rows, SFFTB_HASH_ROLL=0) cannot go "
+                              "below its IMAD-pipe floor; the tensor-core kernel is below it "
+                              "when launch_ms < cuda_core_imad_floor_ms"}}
 
 
 def roofline_hash(h, peak, src):
-    """Algorithmic bytes of one hashing launch: rows (n*8d) + int64 hits
-    (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8)."""
+    """Algorithmic bytes of one hashing call: rows (n*8d) + int64 hits
+    (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8).  The
+    duration is the whole sfftb_hash_hits call (CUDA events on its stream):
+    bitmap pre-kernel + hash_roll_kernel + the out-of-range repair kernel."""
     n = h.get("n_local", h["n"])  # this rank's rows (all rows at N = 1)
     bytes_ = n * 8 * h["d"] + n * 8 + h["L"] * h["W"] * 4 + n // 8
     ach = bytes_ / (h["hash_ms"] * 1e-3) / 1e9
-    tr = measured_traffic("hash_rows")
+    tr = measured_traffic("hash_roll_kernel")
     traffic = None
     if tr and tr.get("rows") == h["n"] and tr.get("L") == h["L"] and tr.get("M") == h["M"]:
         traffic = tr["dram_read"] + tr["dram_write"]
-    return {"bound": "hbm", "kernel": "hash_rows (sfftb_hash_hits)", "achieved": round(ach, 1),
+    return {"bound": "hbm", "kernel": "hash_roll_kernel (sfftb_hash_hits)",
+            "achieved": round(ach, 1),
             "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
             "algorithmic_bytes": bytes_, "peak_source": src,
-            "launch_ms": round(h["hash_ms"], 4), **_imad_bound(h)}
+            "launch_ms": round(h["hash_ms"], 4), **_issue_bound(h)}
 
 
 def fft_flops(N):
