@@ -804,6 +804,27 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
     a.bits = bits;
     a.W = (int)W;
+    // stream-ordered scratch (reentrant); keep freed blocks in the device's
+    // default pool across synchronisations instead of returning them to the
+    // driver after every call
+    {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64)
+            std::call_once(once[dev], [dev] {
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    unsigned long long thr = 0;
+                    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) ==
+                            cudaSuccess &&
+                        thr < (64ull << 20)) {
+                        thr = 64ull << 20;
+                        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                    }
+                }
+            });
+    }
     uint32_t* xbits = nullptr;
     SFFTB_CUDA(cudaMallocAsync(&xbits, (size_t)L * Wx * sizeof(uint32_t), st));
     a.xbits = xbits;
