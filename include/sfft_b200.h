@@ -161,11 +161,14 @@ int sfftb_nonzero_bitmap(const double *ghat, int64_t G, int64_t L, int64_t M,
  * detmask[g*ceil(n/32) + w] bit b is set when hits of row 32w+b >= min_hits.
  * Replaces _core.pyx:164-197 (the hit half of detect_gather).
  *
- * G == 1 sets of >= 2^16 rows with even d <= 16 run on the tensor cores
- * (csrc/hash_tc.cu): residues as an exact u8 x u8 -> s32 GEMM of the raw row
- * bytes against per-lattice coefficient limbs (tcgen05.mma kind::i8), exact
- * for ANY int64 rows (kbound is not needed there; rows beyond the GEMM range
- * take an exact 64-bit path inside the same kernel).
+ * G == 1 sets of >= 2^21 rows with even d <= 14, L <= 60 and M <= ~1.2e5 run
+ * on the tensor cores (csrc/hash_roll.cu): rows packed into tensor memory as
+ * the A operand of an exact u8 x u8 -> s32 GEMM (tcgen05.mma kind::i8) against
+ * per-lattice coefficient limbs, bitmaps streamed in lattice groups; exact for
+ * ANY int64 rows (rows outside [-2^13, 2^13) are redone by an exact 64-bit
+ * kernel; kbound is not needed).  SFFTB_HASH_ROLL=0 keeps the CUDA-core
+ * kernel; SFFTB_HASH_TC=1 selects the earlier byte-GEMM kernel
+ * (csrc/hash_tc.cu).
  */
 int sfftb_hash_hits(const int64_t *elems, int64_t n, int64_t d,
                     const int64_t *zmat, int64_t G, int64_t L, int64_t M,
