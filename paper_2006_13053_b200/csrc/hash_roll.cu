@@ -91,9 +91,9 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)  // suspend-time hint: sleep, do not spin
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32_t bytes,
@@ -332,64 +332,66 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
     };
     long long pt[2] = {0, 0};
     const long long tstart = clock64();
-    int4 cur[H], nxt[H];
-    if (x.nb > 0) load(cur, 0, hsel);
+    // two register buffers, used alternately (no copies): tile hsel of a birth
+    // is packed from bufA while tile hsel + 2 loads into bufB, and vice versa
+    int4 bufA[H], bufB[H];
+    if (x.nb > 0) load(bufA, 0, hsel);
     for (int u = 1; u <= 4; ++u)
         if ((u >> 1) < x.nb) prefetch(u >> 1, hsel + 2 * (u & 1));
     int c = 0, beta = 0;
-    for (int b = 0; b < x.nb; ++b) {
+    auto pack_store = [&](const int4 (&cur)[H], int k, bool first, bool last) {
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-            const int k = hsel + 2 * kk;
-            // the next unit's rows are requested before this one is packed
-            const int b2 = kk == 0 ? b : b + 1, k2 = kk == 0 ? hsel + 2 : hsel;
-            if (b2 < x.nb) load(nxt, b2, k2);
-            {
-                const int u = 2 * b + kk + 5;
-                if ((u >> 1) < x.nb) prefetch(u >> 1, hsel + 2 * (u & 1));
-            }
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-                // k in [-2^13, 2^13) <=> high word = sign of the low word and
-                // (low + 2^13) < 2^14
-                const uint32_t l0 = (uint32_t)cur[i].x + (uint32_t)kOffset;
-                const uint32_t l1 = (uint32_t)cur[i].z + (uint32_t)kOffset;
-                const uint32_t o0 = (l0 >> 14) | (uint32_t)(cur[i].y ^ (cur[i].x >> 31));
-                const uint32_t o1 = (l1 >> 14) | (uint32_t)(cur[i].w ^ (cur[i].z >> 31));
-                uint32_t w = (l0 & 127u) | ((l0 << 1) & 0x7F00u) | ((l1 & 127u) << 16) |
-                             ((l1 << 17) & 0x7F000000u);
-                if (o0 | o1) w |= 0x80u;
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst[i]), "r"(w) : "memory");
-            }
-            __syncwarp();
-            uint32_t r[8];
-            uint32_t bad = 0;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                if (p < H) {
-                    const uint32_t w = stg[lane * RS + p];
-                    bad |= w & 0x80u;
-                    r[p] = w & ~0x80u;
-                } else {
-                    r[p] = 0u;
-                }
-            }
-            // K = 2D: the constant 1; K = 2D + 1: the out-of-range flag
-            if (H < 8) r[H] = 1u | (bad ? 0x100u : 0u);
-            __syncwarp();
-            if (kk == 0 && beta >= 1)  // the cohort's previous occupants have retired
-                ROLL_T(pt[0], bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1)));
-            tc_fence_after();
-            ROLL_T(pt[1], tmem_st8(x.tmem + ((uint32_t)(q * 32) << 16) +
-                                       (uint32_t)((c * kSP + k) * kACols), r));
-            if (kk == 1) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
-            }
-#pragma unroll
-            for (int i = 0; i < H; ++i) cur[i] = nxt[i];
+        for (int i = 0; i < H; ++i) {
+            // u = k + 2^13 as 64 bits: in range <=> high word 0 and low < 2^14;
+            // a + 256 b for u = a + 128 b is u + (u & ~127)
+            uint32_t l0, h0, l1, h1;
+            asm("add.cc.u32 %0, %2, 8192;\n\taddc.u32 %1, %3, 0;"
+                : "=r"(l0), "=r"(h0)
+                : "r"(cur[i].x), "r"(cur[i].y));
+            asm("add.cc.u32 %0, %2, 8192;\n\taddc.u32 %1, %3, 0;"
+                : "=r"(l1), "=r"(h1)
+                : "r"(cur[i].z), "r"(cur[i].w));
+            const uint32_t p0 = (l0 & 0x3FFFu) + (l0 & 0x3F80u);
+            const uint32_t p1 = (l1 & 0x3FFFu) + (l1 & 0x3F80u);
+            uint32_t w = (p1 << 16) + p0;
+            if ((h0 | h1) | ((l0 | l1) >> 14)) w |= 0x80u;
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst[i]), "r"(w) : "memory");
         }
+        __syncwarp();
+        uint32_t r[8];
+        uint32_t bad = 0;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            if (p < H) {
+                const uint32_t w = stg[lane * RS + p];
+                bad |= w;
+                r[p] = w & ~0x80u;
+            } else {
+                r[p] = 0u;
+            }
+        }
+        // K = 2D: the constant 1; K = 2D + 1: the out-of-range flag
+        if (H < 8) r[H] = 1u + ((bad & 0x80u) << 1);
+        __syncwarp();
+        if (first && beta >= 1)  // the cohort's previous occupants have retired
+            ROLL_T(pt[0], bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1)));
+        tc_fence_after();
+        ROLL_T(pt[1], tmem_st8(x.tmem + ((uint32_t)(q * 32) << 16) +
+                                   (uint32_t)((c * kSP + k) * kACols), r));
+        if (last) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
+        }
+    };
+    for (int b = 0; b < x.nb; ++b) {
+        // the next unit's rows are requested before this one is packed
+        load(bufB, b, hsel + 2);
+        if (b + 3 < x.nb) prefetch(b + 3, hsel);
+        pack_store(bufA, hsel, true, false);
+        if (b + 1 < x.nb) load(bufA, b + 1, hsel);
+        if (b + 3 < x.nb) prefetch(b + 3, hsel + 2);
+        pack_store(bufB, hsel + 2, false, true);
         if (++c == x.NG) {
             c = 0;
             ++beta;
