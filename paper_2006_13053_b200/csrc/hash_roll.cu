@@ -620,7 +620,20 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                 lb[i] = t;
             }
             ROLL_T(pt[0], bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1)));
-            // accumulators of cohort 0; cohort c + 1 is fetched while c is probed
+            // Software pipeline over the step's cohorts: while cohort c is
+            // probed (address, shared load, bit), the residues of cohort c + 1
+            // are computed and the accumulators of cohort c + 2 are in flight.
+            auto residues = [&](const uint32_t (&v)[16], uint32_t (&r)[kLG]) {
+                // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
+#pragma unroll
+                for (int i = 0; i < kLG; ++i) {
+                    uint32_t xx = (v[3 * i + 1] << 8) + v[3 * i];
+                    xx = (v[3 * i + 2] << 16) + xx;
+                    const uint32_t qq = __umulhi(xx, magic);
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
+                }
+            };
+            uint32_t rr[2][kLG], flag[2];
             ROLL_T(pt[1], bar_wait(dfull, par[0]));
             par[0] ^= 1u;
             tc_fence_after();
@@ -629,28 +642,36 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
             tc_fence_before();
             __syncwarp();
             if (lane0) bar_arrive(dempty);
+            if (NG > 1) {
+                ROLL_T(pt[1], bar_wait(dfull + 8u * (1 % ND), par[1 % ND]));
+                par[1 % ND] ^= 1u;
+                tc_fence_after();
+                tmem_ld16_async(tlane + (uint32_t)(dstride * (1 % ND)), vb);
+            }
+            residues(va, rr[0]);
+            flag[0] = va[15];
 #pragma unroll
             for (int c = 0; c < NG; ++c) {
-                uint32_t(&v)[16] = (c & 1) ? vb : va;
-                uint32_t(&vn)[16] = (c & 1) ? va : vb;
-                constexpr int kDummy = 0;
-                (void)kDummy;
-                const int bn = (c + 1) % ND;
+                uint32_t(&vc)[16] = (c & 1) ? vb : va;  // cohort c: consumed, reused for c + 2
+                uint32_t(&vn)[16] = (c & 1) ? va : vb;  // cohort c + 1: in flight
+                const int b1 = (c + 1) % ND, b2 = (c + 2) % ND;
                 if (c + 1 < NG) {
-                    ROLL_T(pt[1], bar_wait(dfull + 8u * bn, par[bn]));
-                    par[bn] ^= 1u;
+                    tmem_wait_ld16(vn);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane0) bar_arrive(dempty + 8u * b1);
+                }
+                if (c + 2 < NG) {
+                    ROLL_T(pt[1], bar_wait(dfull + 8u * b2, par[b2]));
+                    par[b2] ^= 1u;
                     tc_fence_after();
-                    tmem_ld16_async(tlane + (uint32_t)(dstride * bn), vn);
+                    tmem_ld16_async(tlane + (uint32_t)(dstride * b2), vc);
                 }
-                // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
-                uint32_t r[kLG], w[kLG];
-#pragma unroll
-                for (int i = 0; i < kLG; ++i) {
-                    uint32_t xx = (v[3 * i + 1] << 8) + v[3 * i];
-                    xx = (v[3 * i + 2] << 16) + xx;
-                    const uint32_t qq = __umulhi(xx, magic);
-                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
+                if (c + 1 < NG) {
+                    residues(vn, rr[(c + 1) & 1]);
+                    flag[(c + 1) & 1] = vn[15];
                 }
+                uint32_t w[kLG];
 #pragma unroll
                 for (int i = 0; i < kLG; ++i) {
                     asm volatile("{\n\t.reg .u32 t;\n\t"
@@ -658,20 +679,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                                  "lop3.b32 t, t, 0xFFFFFFFC, %2, 0xEA;\n\t"
                                  "ld.shared.u32 %0, [t];\n\t}"
                                  : "=r"(w[i])
-                                 : "r"(r[i]), "r"(lb[i]));
+                                 : "r"(rr[c & 1][i]), "r"(lb[i]));
                 }
                 uint32_t bacc = 0;
 #pragma unroll
                 for (int i = 0; i < kLG; ++i)
-                    bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], r[i]), 1);
+                    bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], rr[c & 1][i]), 1);
                 hp[c >> 2] += __popc(bacc & lmask) << (8 * (c & 3));
-                const uint32_t flag = v[15];
-                if (c + 1 < NG) {
-                    tmem_wait_ld16(vn);
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane0) bar_arrive(dempty + 8u * bn);
-                }
                 if (sm == (c + NG - 1) % NG) {  // the cohort born at step s - (NG - 1) retires
                     const int b = s - (NG - 1);
                     const uint32_t hc = (hp[c >> 2] >> (8 * (c & 3))) & 255u;
@@ -684,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
                         const int64_t hits = (int64_t)hc;
                         // rows outside the limb range: counted here, redone
                         // exactly by roll_fixup_kernel
-                        if (__any_sync(0xffffffffu, flag != 0u && valid) && lane0)
+                        if (__any_sync(0xffffffffu, flag[c & 1] != 0u && valid) && lane0)
                             atomicAdd(a.nbad, 1u);
                         const unsigned det =
                             __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
@@ -722,8 +736,8 @@ static unsigned long long* recomputed_counter() {
     static unsigned long long* p = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
-        if (cudaMalloc(&p, 2 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(p, 0, 2 * sizeof(unsigned long long));
+        if (cudaMalloc(&p, sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(p, 0, sizeof(unsigned long long));
         else
             p = nullptr;
     });
@@ -827,10 +841,15 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
                 }
             });
     }
+    // per-call scratch: the extended bitmaps and, behind them, this call's
+    // out-of-range flag (private to the call: concurrent calls on other
+    // streams must not share it)
     uint32_t* xbits = nullptr;
-    SFFTB_CUDA(cudaMallocAsync(&xbits, (size_t)L * Wx * sizeof(uint32_t), st));
+    SFFTB_CUDA(cudaMallocAsync(&xbits, ((size_t)L * Wx + 4) * sizeof(uint32_t), st));
     a.xbits = xbits;
     a.Wx = (int)Wx;
+    a.nbad = xbits + (size_t)L * Wx;
+    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, sizeof(unsigned int), st));
     a.ext_words = (int)ext_words;
     a.S2 = S2;
     a.ntiles = (n + kTile - 1) / kTile;
@@ -838,8 +857,6 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.hits64 = hits64;
     a.detmask = detmask;
     a.recomputed = rec;
-    a.nbad = reinterpret_cast<unsigned int*>(rec + 1);
-    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, sizeof(unsigned int), st));
     a.dbg = nullptr;
     static int32_t* dbg = nullptr;
     if (getenv("SFFTB_HASH_ROLL_DUMP") && getenv("SFFTB_HASH_ROLL_PROF")) {

@@ -135,3 +135,63 @@ def test_roll_hash_mask_only(cuda):
             else:
                 os.environ[k] = v
     assert np.array_equal(m, _mask_of(want, 25))
+
+
+def test_roll_hash_concurrent_threads(cuda):
+    """Three host threads, each on its own stream, one of them with rows outside
+    the limb range: every call repairs exactly its own rows (the out-of-range
+    flag and the scratch bitmaps are private to a call)."""
+    import threading
+
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    rng = np.random.default_rng(23)
+    d, M, L = 10, 103307, 47
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    bits, words = _bitmaps(rng, L, M, 0.4)
+    cases = []
+    for t in range(3):
+        n = 180_000 + 1000 * t
+        rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+        if t == 1:
+            rows[rng.choice(n, size=500, replace=False), 3] = 1 << 40
+        cases.append((rows, _exact_hits(rows % M, z, M, bits)))
+    env = {"SFFTB_HASH_ROLL": "1", "SFFTB_HASH_ROLL_MINROWS": "1", "SFFTB_HASH_TC": "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    out = [None] * 3
+    zdev, wdev = _dev.upload(z), _dev.upload(words.view(np.int32))
+    torch.cuda.synchronize()
+
+    def work(t):
+        rows, _ = cases[t]
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for _ in range(4):
+                rdev = torch.as_tensor(rows, device="cuda")
+                hits = torch.empty((rows.shape[0],), dtype=torch.int64, device="cuda")
+                mask = torch.empty(((rows.shape[0] + 31) // 32,), dtype=torch.int32, device="cuda")
+                _native.call("sfftb_hash_hits", rdev.data_ptr(), rows.shape[0], d, zdev.data_ptr(),
+                             1, L, M, wdev.data_ptr(), -1, 24, hits.data_ptr(), mask.data_ptr(),
+                             st.cuda_stream)
+            st.synchronize()
+            out[t] = (hits.cpu().numpy(), mask.cpu().numpy().view(np.uint32))
+
+    try:
+        th = [threading.Thread(target=work, args=(t,)) for t in range(3)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for t in range(3):
+        assert out[t] is not None
+        assert np.array_equal(out[t][0], cases[t][1])
+        assert np.array_equal(out[t][1], _mask_of(cases[t][1], 24))
