@@ -183,6 +183,11 @@ int64_t sfftb_hash_tc_recomputed(int reset);
  * with a coordinate outside [-2^13, 2^13) that took its exact 64-bit path. */
 int64_t sfftb_hash_roll_recomputed(int reset);
 
+/* Calls served by the fp16 rolling tensor-core kernel (csrc/hash_rollf.cu:
+ * single group, n >= 2^21, kbound = sum_j max|k_j| < 2048, even d <= 12,
+ * L <= 48) since the last reset; for tests and the bench's kernel label. */
+int64_t sfftb_hash_rollf_calls(int reset);
+
 /*
  * Ascending indices of set bits per group: idx[g*n + k], counts[g].
  * ws: sfftb_compact_workspace_bytes(G, n).

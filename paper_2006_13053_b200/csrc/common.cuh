@@ -215,6 +215,10 @@ int hash_hits_tc(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat
 int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat, int64_t L,
                    int64_t M, const uint32_t* bits, int64_t min_hits, int64_t* hits64,
                    uint32_t* detmask, cudaStream_t st);
+// fp16 variant for small coordinates (csrc/hash_rollf.cu; kbound = sum_j max|k_j| < 2048)
+int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat, int64_t L,
+                    int64_t M, const uint32_t* bits, int64_t kbound, int64_t min_hits,
+                    int64_t* hits64, uint32_t* detmask, cudaStream_t st);
 
 // zero-test thresholds (hash.cu) launched inside the fused transform chain
 int zero_thresholds_launch(const double* sumsq, int64_t G, int64_t L, int64_t M, double* theta,

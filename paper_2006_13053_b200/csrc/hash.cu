@@ -1484,6 +1484,10 @@ extern "C" int sfftb_hash_hits(const int64_t* elems, int64_t n, int64_t d, const
     cudaStream_t st = (cudaStream_t)stream;
     // tensor-core path (csrc/hash_tc.cu): exact for any int64 rows, no bound
     if (G == 1) {
+        const int rf = hash_hits_rollf(elems, n, d, zmat, L, M, bits, kbound, min_hits, hits64,
+                                       detmask, st);
+        if (rf < 0) return -rf;
+        if (rf == 1) return SFFTB_OK;
         const int rr = hash_hits_roll(elems, n, d, zmat, L, M, bits, min_hits, hits64, detmask, st);
         if (rr < 0) return -rr;
         if (rr == 1) return SFFTB_OK;

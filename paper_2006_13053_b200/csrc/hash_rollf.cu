@@ -1,0 +1,744 @@
+// K3 on the tensor cores, third design: the rolling kernel of hash_roll.cu with
+// an exact FP16 x FP16 -> FP32 GEMM for candidate sets whose coordinates are
+// small (kbound = sum_j max|k_j| known and < 2048, the case of every box and
+// hyperbolic cross of the reference's workloads).  Same semantics as
+// hash_rows (hash.cu) / _core.pyx:185-197 (residue, |ghat| > theta probe,
+// hits >= nu*L); same rolling schedule, warp roles and wrap-extended bitmaps
+// as hash_roll.cu.  What changes:
+//  * the A operand is the row itself, k_j as signed fp16 (exact for |k_j| <
+//    2048), K = 16 = d coordinates + three constant slots (2048, 2048, 1);
+//  * the 17-bit coefficients z_j mod M are split in TWO limbs c = c0 + 2^s c1
+//    (both exact in fp16), so a lattice takes two accumulator columns instead
+//    of three and a 16-column tile serves 8 lattices instead of 5: 6 lattice
+//    groups cover L <= 48 where the byte kernel needs 10;
+//  * the constant slots seed every accumulator with 1.5 * 2^23 (+ kbound * M
+//    split over the two limbs, so x' = k.z + kbound M >= 0): the FP32 result
+//    lies in [2^23, 2^24), where its bit pattern is 0x4B000000 + integer.  The
+//    second limb's seed carries one more constant chosen so that
+//        x' = bits1 * 2^s + bits0   (mod 2^32)
+//    exactly: ONE integer multiply-add combines the limbs straight from the raw
+//    accumulator bits (the byte kernel needs two).  Every partial sum is an
+//    integer below 2^24, so the FP32 accumulation is exact in any order;
+//  * two cohorts are born per step (12 cohorts of 4 tiles for 6 groups: 6144
+//    rows resident in 384 TMEM columns + two 64-column accumulator buffers);
+//  * bitmaps stream in HALF groups (4 lattices, 16 KB slots) through a ring of
+//    three buffers; a probe address is ((r >> 3) & 0x3FFC) | buffer base with
+//    the slot as the load's immediate offset, which also bounds the address
+//    for any accumulator content.
+// Per (row, lattice) the epilogue issues IMAD (limbs), IMAD.HI + IMAD
+// (reduction), SHF + LOP3 (address), LDS, 2 funnel shifts.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <cuda_fp16.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+#include "roll_ptx.cuh"
+
+namespace sfftb {
+
+namespace rollf {
+
+using namespace rollptx;
+
+constexpr int kThreads = 832;
+constexpr int kTile = 128;
+constexpr int kLG = 8;          // lattices per group (two accumulator columns each)
+constexpr int kNC = 16;         // MMA N
+constexpr int kACols = 8;       // TMEM columns of one A tile (K = 16 halves)
+constexpr int kSP = 4;          // tiles per cohort (one per epilogue warp group)
+constexpr int kBPS = 2;         // cohorts born per step
+constexpr int kMaxNG = 6;
+constexpr int kLoaders = 8;
+constexpr int kEpiWarp0 = 2 + kLoaders;
+constexpr int kEpiWarps = 16;
+constexpr uint32_t kSlot = 13824;           // bytes per lattice bitmap slot (M + ext <= 110592 bits)
+constexpr uint32_t kBuf = kLG * kSlot;      // one ring buffer: a group of 8 bitmaps
+constexpr uint32_t kBufStride = 0x1C000u;   // buffer 1 starts here (low 14 bits zero: OR-able)
+constexpr int kRing = 2;
+constexpr int32_t kCoordLim = 2048;         // |k_j| < kCoordLim (fp16-exact)
+constexpr uint32_t kSeedBits = 0x4B400000u; // float bits of 1.5 * 2^23
+
+struct Args {
+    const int64_t* elems;
+    int64_t n;
+    const int64_t* zmat;  // (L, d)
+    int d, L, NG;
+    uint32_t M, negM, magic;
+    int s;                 // limb split: c = c0 + 2^s c1
+    uint32_t pow2s;
+    // B-operand constants of the seed slots (A = 2048, 2048, 1), per limb
+    uint32_t seed0[3], seed1[3];
+    const uint32_t* bits;  // (L, W)
+    int W;
+    const uint32_t* xbits; // (L, Wx) wrap-extended bitmaps
+    int Wx;
+    int64_t ntiles;
+    int64_t min_hits;
+    int64_t* hits64;   // may be null
+    uint32_t* detmask;
+    unsigned long long* recomputed;
+    unsigned int* nbad;  // warps that met a coordinate outside (-2048, 2048)
+    uint32_t* dbg;       // diagnostics: raw accumulators of tile 0, step 0
+};
+
+__device__ int exact_row_hits(const Args& a, int d, int64_t row) {
+    int h = 0;
+    for (int l = 0; l < a.L; ++l) {
+        uint64_t acc = 0;
+        for (int j = 0; j < d; ++j) {
+            int64_t e = a.elems[row * d + j] % (int64_t)a.M;
+            if (e < 0) e += a.M;
+            int64_t z = a.zmat[(int64_t)l * d + j] % (int64_t)a.M;
+            if (z < 0) z += a.M;
+            acc = (acc + (uint64_t)e * (uint64_t)z) % a.M;
+        }
+        const uint32_t r = (uint32_t)acc;
+        h += (a.bits[(int64_t)l * a.W + (r >> 5)] >> (r & 31)) & 1u;
+    }
+    return h;
+}
+
+// Runs after every launch: exits at once unless a loader met a coordinate
+// outside the fp16 range; otherwise redoes those rows exactly.
+__global__ void __launch_bounds__(256) rollf_fixup_kernel(Args a) {
+    if (*reinterpret_cast<volatile unsigned int*>(a.nbad) == 0u) return;
+    const int d = a.d;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < a.n;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        bool bad = false;
+        for (int j = 0; j < d; ++j)
+            bad |= ((uint64_t)(a.elems[row * d + j] + kCoordLim) >> 12) != 0;
+        if (!bad) continue;
+        const int64_t hits = exact_row_hits(a, d, row);
+        atomicAdd(a.recomputed, 1ull);
+        if (a.hits64) a.hits64[row] = hits;
+        const uint32_t bit = 1u << (row & 31);
+        if (hits >= a.min_hits) atomicOr(a.detmask + (row >> 5), bit);
+        else atomicAnd(a.detmask + (row >> 5), ~bit);
+    }
+}
+
+// Shared-memory map: byte offsets from the dynamic base.
+//   [0, 110592)        bitmap buffer 0 (8 slots of 13824 B)
+//   [110592, 114688)   barriers, TMEM address, B operands (the gap up to kBufStride)
+//   [114688, 225280)   bitmap buffer 1
+//   [225280, 232448)   loader transposition buffers
+// = the 227 KB a CTA can have.  A probe offset is masked to 16 KB, so a
+// residue computed from a garbage accumulator (a row outside the fp16 range)
+// can read up to 2.5 KB past its 13.5 KB slot: from the last slot of a buffer
+// that lands in the tables behind it, never outside the CTA's window.
+struct Smem {
+    uint32_t bm_full, bm_empty, d_full, d_empty, a_full, a_empty, tmem_holder;
+    uint32_t bop, stage, end;
+};
+__host__ __device__ inline Smem smem_map(int NG) {
+    Smem s;
+    uint32_t o = kBuf;
+    s.bm_full = o;  o += 8u * kRing;
+    s.bm_empty = o; o += 8u * kRing;
+    s.d_full = o;   o += 32;
+    s.d_empty = o;  o += 32;
+    s.a_full = o;   o += 8u * kMaxNG * kBPS;
+    s.a_empty = o;  o += 8u * kMaxNG * kBPS;
+    s.tmem_holder = o; o += 16;
+    o = (o + 127u) & ~127u;
+    s.bop = o;      o += (uint32_t)kMaxNG * 512u;  // B operand: NG x [2][16][16 B]
+    (void)NG;
+    s.stage = kBufStride + kBuf;                   // loader transposition (RS <= 7)
+    s.end = s.stage + (uint32_t)kLoaders * 32u * 7u * 4u;
+    return s;
+}
+static_assert(kBuf + 512u + kMaxNG * 512u <= kBufStride, "tables fit the gap between the buffers");
+static_assert(kBuf % 16u == 0 && (kBufStride & 0x3FFFu) == 0, "buffer alignment");
+static_assert((kLG - 1) * kSlot + 16384u <= kBufStride, "probe overrun of buffer 0 stays in the gap");
+static_assert((kLG - 1) * kSlot + 16384u <= kBuf + kLoaders * 32u * 7u * 4u,
+              "probe overrun of buffer 1 stays in the loader buffers");
+
+struct Ctx {
+    uint32_t raw, tmem;
+    int lane, warp, nb, NG;
+    int64_t cta, ncta;
+};
+
+__device__ __forceinline__ uint32_t half_bits(float v) {
+    return (uint32_t)__half_as_ushort(__float2half_rn(v));
+}
+
+// Bitmap word of residue r in slot I of the ring buffer at byte offset boff
+// (0 or kBufStride) of the window: the mask keeps the offset below 16 KB for
+// any r (see Smem).  Plain C++ so that the window base stays in a uniform
+// register and the slot is the load's immediate: SHF + LOP3 + LDS [R + UR + imm].
+template <int I>
+__device__ __forceinline__ uint32_t probe(uint32_t r, uint32_t boff, const uint8_t* win) {
+    return *reinterpret_cast<const uint32_t*>(win + I * kSlot + (((r >> 3) & 0x3FFCu) | boff));
+}
+
+// Row loader of one warp: lane quadrant q = warp & 3, tiles k = hsel, hsel + 2
+// of both cohorts of every birth.  Coalesced 16-byte loads (a coordinate pair
+// each), converted to an fp16 pair, transposed through shared memory to
+// thread-per-row, stored into the cohort's A tiles in tensor memory.
+template <int D>
+__device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const Ctx& x,
+                                           uint8_t* smem_raw) {
+    constexpr int H = D / 2;   // 16-byte chunks (coordinate pairs) per row
+    constexpr int RS = H | 1;  // odd row stride of the transposition buffer
+    static_assert(H + 2 <= 8, "d + 3 constant slots must fit K = 16");
+    const int lane = x.lane, q = x.warp & 3, hsel = (x.warp - 2) >> 2;
+    const uint32_t raw = x.raw;
+    uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + S.stage) + (x.warp - 2) * 32 * RS;
+    const int4* gbase = reinterpret_cast<const int4*>(a.elems);
+    // unit u of birth b: cohort j = u >> 1, tile k = hsel + 2 (u & 1); rows
+    // [t*128 + q*32, +32) of tile t = cta + ((b kBPS + j) kSP + k) ncta
+    auto unit_rows = [&](int b, int u) -> int64_t {
+        const int j = u >> 1, k = hsel + 2 * (u & 1);
+        return ((x.cta + (int64_t)((b * kBPS + j) * kSP + k) * x.ncta) * kTile + q * 32);
+    };
+    auto load = [&](int4 (&rawv)[H], int b, int u) {
+        const int64_t r0 = unit_rows(b, u);
+        const int4* src = gbase + r0 * H + lane;
+        if (r0 + 32 <= a.n) {  // the whole unit is inside the set
+#pragma unroll
+            for (int i = 0; i < H; ++i) rawv[i] = __ldg(src + 32 * i);
+        } else {
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const int64_t row = r0 + (lane + 32 * i) / H;
+                rawv[i] = row < a.n ? __ldg(src + 32 * i) : make_int4(0, 0, 0, 0);
+            }
+        }
+    };
+    const uint32_t stg_a = smem_addr(stg);
+    uint32_t sdst[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        const int ch = lane + 32 * i;
+        sdst[i] = stg_a + 4u * (uint32_t)((ch / H) * RS + (ch % H));
+    }
+    auto prefetch = [&](int b, int u) {
+        const int64_t r0 = unit_rows(b, u);
+        const char* p = reinterpret_cast<const char*>(a.elems) + r0 * (8 * D);
+        if (lane * 128 < 32 * 8 * D && r0 + 32 <= a.n) prefetch_l2(p + lane * 128);
+    };
+    int c0 = 0, beta = 0;  // first cohort of the current birth slot, its generation
+    auto pack_store = [&](const int4 (&cur)[H], int u) {
+        uint32_t bad = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            // in range <=> k + 2048 as 64 bits < 4096
+            uint32_t l0, h0, l1, h1;
+            asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
+                : "=r"(l0), "=r"(h0)
+                : "r"(cur[i].x), "r"(cur[i].y));
+            asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
+                : "=r"(l1), "=r"(h1)
+                : "r"(cur[i].z), "r"(cur[i].w));
+            bad |= (h0 | h1) | ((l0 | l1) >> 12);
+            const __half2 hh = __floats2half2_rn((float)cur[i].x, (float)cur[i].z);
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(&hh);
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst[i]), "r"(w) : "memory");
+        }
+        if (__any_sync(0xffffffffu, bad != 0u)) {  // also orders the stores (warp-convergent)
+            if (lane == 0) atomicAdd(a.nbad, 1u);
+        }
+        __syncwarp();
+        uint32_t r[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) r[p] = p < H ? stg[lane * RS + p] : 0u;
+        r[H] = 0x68006800u;      // K = D, D + 1: the constants 2048, 2048
+        r[H + 1] = 0x00003C00u;  // K = D + 2: the constant 1
+        __syncwarp();
+        const int c = c0 + (u >> 1);
+        if (!(u & 1) && beta >= 1)  // the cohort's previous occupants have retired
+            bar_wait(raw + S.a_empty + 8u * c, (uint32_t)((beta - 1) & 1));
+        tc_fence_after();
+        const int k = hsel + 2 * (u & 1);
+        tmem_st8(x.tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((c * kSP + k) * kACols), r);
+        if (u & 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(raw + S.a_full + 8u * c);
+        }
+    };
+    // two register buffers used alternately: unit u packs from one while unit
+    // u + 1 loads into the other
+    int4 bufA[H], bufB[H];
+    if (x.nb > 0) load(bufA, 0, 0);
+    for (int v = 1; v <= 8; ++v)
+        if ((v >> 2) < x.nb) prefetch(v >> 2, v & 3);
+    for (int b = 0; b < x.nb; ++b) {
+        load(bufB, b, 1);
+        if (b + 2 < x.nb) prefetch(b + 2, 1);
+        pack_store(bufA, 0);
+        load(bufA, b, 2);
+        if (b + 2 < x.nb) prefetch(b + 2, 2);
+        pack_store(bufB, 1);
+        load(bufB, b, 3);
+        if (b + 2 < x.nb) prefetch(b + 2, 3);
+        pack_store(bufA, 2);
+        if (b + 1 < x.nb) load(bufA, b + 1, 0);
+        if (b + 3 < x.nb) prefetch(b + 3, 0);
+        pack_store(bufB, 3);
+        c0 += kBPS;
+        if (c0 == x.NG * kBPS) {
+            c0 = 0;
+            ++beta;
+        }
+    }
+}
+
+// NG = lattice groups per pass; NCH = kBPS * NG cohorts.  Every step runs the
+// same NCH items (cohorts in index order, four tiles each, accumulator buffer
+// c % ND): cohorts not yet born or past the end of the rows are processed as
+// dummies (their outputs are never written), so the schedule is static.
+template <int NG>
+__global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    constexpr int NCH = NG * kBPS;
+    const uint32_t raw = smem_addr(smem_raw);
+    const Smem S = smem_map(NG);
+    const uint32_t ring0 = raw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t cta = blockIdx.x, ncta = gridDim.x;
+    const int my_tiles = a.ntiles > cta ? (int)((a.ntiles - 1 - cta) / ncta + 1) : 0;
+    const int nb = (my_tiles + kSP * kBPS - 1) / (kSP * kBPS);  // births (kBPS cohorts each)
+    const int nsteps = nb > 0 ? nb + NG - 1 : 0;
+    constexpr int dcol0 = NCH * kSP * kACols;
+    constexpr int dstride = kNC * kSP;  // accumulator columns of one cohort
+    constexpr int ND = (dcol0 + 3 * dstride <= 512) ? 3 : 2;
+    static_assert(dcol0 + ND * dstride <= 512, "tensor memory");
+    const int D = a.d;
+
+    // ---- setup ----
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kRing; ++i) {
+            bar_init(raw + S.bm_full + 8u * i, 1);
+            bar_init(raw + S.bm_empty + 8u * i, kEpiWarps);
+        }
+        for (int i = 0; i < ND; ++i) {
+            bar_init(raw + S.d_full + 8u * i, 1);
+            bar_init(raw + S.d_empty + 8u * i, kEpiWarps);
+        }
+        for (int i = 0; i < NCH; ++i) {
+            bar_init(raw + S.a_full + 8u * i, kLoaders);
+            bar_init(raw + S.a_empty + 8u * i, kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         raw + S.tmem_holder)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // B operand of group g: [2 K-chunks][16 columns][8 halves]; column 2i +
+    // limb for lattice g*kLG + i.  K index kb: < D the coordinate, D and D + 1
+    // the 2048 slots, D + 2 the unit slot.
+    for (uint32_t e = threadIdx.x; e < (uint32_t)NG * 256u; e += blockDim.x) {
+        const int g = (int)(e / 256u);
+        const uint32_t in = e % 256u;
+        const int col = (int)((in / 8u) % 16u);
+        const int kb = (int)(in / 128u) * 8 + (int)(in % 8u);
+        const int i = col >> 1, limb = col & 1;
+        const int l = g * kLG + i;
+        float v = 0.f;
+        if (l < a.L) {
+            if (kb < D) {
+                int64_t z = a.zmat[(int64_t)l * D + kb] % (int64_t)a.M;
+                if (z < 0) z += a.M;
+                const uint32_t c = (uint32_t)z;
+                v = (float)(limb ? (c >> a.s) : (c & (a.pow2s - 1u)));
+            } else if (kb < D + 3) {
+                v = (float)(limb ? a.seed1[kb - D] : a.seed0[kb - D]);
+            }
+        }
+        reinterpret_cast<uint16_t*>(smem_raw + S.bop)[e] = (uint16_t)half_bits(v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + S.tmem_holder);
+
+    if (warp == 0) {
+        // ================= bitmap producer =================
+        const uint32_t wbytes = (uint32_t)a.Wx * 4u;
+        auto issue = [&](int s) {
+            const int ring = s & 1;
+            const int l0 = (s % NG) * kLG;
+            const int cnt = min(a.L, l0 + kLG) - l0;
+            if (lane == 0) {
+                const uint32_t bar = raw + S.bm_full + 8u * ring;
+                bar_expect_tx(bar, wbytes * (uint32_t)cnt);
+                for (int i = 0; i < cnt; ++i)
+                    bulk_g2s_a(ring0 + (uint32_t)ring * kBufStride + (uint32_t)i * kSlot,
+                               a.xbits + (int64_t)(l0 + i) * a.Wx, wbytes, bar);
+            }
+        };
+        if (nsteps > 0) issue(0);
+        if (nsteps > 1) issue(1);
+        for (int s = 0; s + 2 < nsteps; ++s) {
+            bar_wait(raw + S.bm_empty + 8u * (uint32_t)(s & 1), (uint32_t)((s >> 1) & 1));
+            issue(s + 2);
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        const bool leader = elect_one();
+        // kind::f16: D = f32 (1 << 4), A = B = f16 (0), K-major, N >> 3, M >> 4
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
+        uint32_t epar[3] = {1u, 1u, 1u};
+        bool used[3] = {false, false, false};
+        int sm = 0, beta = 0;
+        for (int s = 0; s < nsteps; ++s) {
+            const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)sm * 512u, 256u, 128u);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const int buf = c % ND;
+                if (used[buf]) bar_wait(raw + S.d_empty + 8u * buf, epar[buf]);
+                used[buf] = true;
+                epar[buf] ^= 1u;
+                if ((c / kBPS) == sm && s < nb)  // newborn cohort: its rows are in tensor memory
+                    bar_wait(raw + S.a_full + 8u * c, (uint32_t)(beta & 1));
+                tc_fence_after();
+                if (leader) {
+#pragma unroll
+                    for (int k = 0; k < kSP; ++k)
+                        umma_f16_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
+                                    tmem + (uint32_t)((c * kSP + k) * kACols), bdesc, idesc);
+                    umma_commit(raw + S.d_full + 8u * buf);
+                }
+                __syncwarp();
+            }
+            if (++sm == NG) {
+                sm = 0;
+                ++beta;
+            }
+        }
+    } else if (warp < kEpiWarp0) {
+        // ================= row loaders =================
+        Ctx x;
+        x.raw = raw;
+        x.tmem = tmem;
+        x.lane = lane;
+        x.warp = warp;
+        x.nb = nb;
+        x.NG = NG;
+        x.cta = cta;
+        x.ncta = ncta;
+        switch (D) {
+            case 4: run_loader<4>(a, S, x, smem_raw); break;
+            case 6: run_loader<6>(a, S, x, smem_raw); break;
+            case 8: run_loader<8>(a, S, x, smem_raw); break;
+            case 10: run_loader<10>(a, S, x, smem_raw); break;
+            default: run_loader<12>(a, S, x, smem_raw); break;
+        }
+    } else {
+        // ================= epilogue =================
+        const int ew = warp - kEpiWarp0;
+        const int grp = ew >> 2;  // the cohort's tile this warp probes
+        const int q = warp & 3;
+        const uint32_t negM = a.negM, magic = a.magic, pow2s = a.pow2s;
+        uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dcol0 + kNC * grp);
+        asm volatile("" : "+r"(tlane));
+        const bool lane0 = lane == 0;
+        uint32_t dfull = raw + S.d_full, dempty = raw + S.d_empty;
+        asm volatile("" : "+r"(dfull), "+r"(dempty));  // not rematerialised per item
+        // running hit counts of this thread's row in every cohort, one byte each
+        uint32_t hp[(NCH + 3) / 4];
+#pragma unroll
+        for (int i = 0; i < (NCH + 3) / 4; ++i) hp[i] = 0;
+        uint32_t par[3] = {0u, 0u, 0u};
+        int sm = 0;
+        uint32_t va[16], vb[16];
+        for (int s = 0; s < nsteps; ++s) {
+            const int lcg = max(0, min(a.L, sm * kLG + kLG) - sm * kLG);
+            // pair i's bit ends at position 32 - kLG + i of the accumulator
+            const uint32_t lmask = ((1u << lcg) - 1u) << (32 - kLG);
+            const int ring = s & 1;
+            uint32_t boff = (uint32_t)ring * kBufStride;
+            asm volatile("" : "+r"(boff));  // one register per step, not rematerialised per probe
+            bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1));
+            // Software pipeline over the step's cohorts: while cohort c is
+            // probed, the residues of cohort c + 1 are computed and the
+            // accumulators of cohort c + 2 are in flight.
+            auto residues = [&](const uint32_t (&v)[16], uint32_t (&r)[kLG]) {
+#pragma unroll
+                for (int i = 0; i < kLG; ++i) {
+                    uint32_t xx;
+                    asm("mad.lo.u32 %0, %1, %2, %3;"
+                        : "=r"(xx)
+                        : "r"(v[2 * i + 1]), "r"(pow2s), "r"(v[2 * i]));
+                    const uint32_t qq = __umulhi(xx, magic);
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
+                }
+            };
+            uint32_t rr[2][kLG];
+            bar_wait(dfull, par[0]);
+            par[0] ^= 1u;
+            tc_fence_after();
+            tmem_ld16_async(tlane, va);
+            tmem_wait_ld16(va);
+            tc_fence_before();
+            __syncwarp();
+            if (lane0) bar_arrive(dempty);
+            if (a.dbg && s == 0 && cta == 0 && grp == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = va[i];
+            }
+            if (NCH > 1) {
+                bar_wait(dfull + 8u * (1 % ND), par[1 % ND]);
+                par[1 % ND] ^= 1u;
+                tc_fence_after();
+                tmem_ld16_async(tlane + (uint32_t)(dstride * (1 % ND)), vb);
+            }
+            residues(va, rr[0]);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                uint32_t(&vc)[16] = (c & 1) ? vb : va;  // cohort c: consumed, reused for c + 2
+                uint32_t(&vn)[16] = (c & 1) ? va : vb;  // cohort c + 1: in flight
+                const int b1 = (c + 1) % ND, b2 = (c + 2) % ND;
+                if (c + 1 < NCH) {
+                    tmem_wait_ld16(vn);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane0) bar_arrive(dempty + 8u * b1);
+                }
+                if (c + 2 < NCH) {
+                    bar_wait(dfull + 8u * b2, par[b2]);
+                    par[b2] ^= 1u;
+                    tc_fence_after();
+                    tmem_ld16_async(tlane + (uint32_t)(dstride * b2), vc);
+                }
+                if (c + 1 < NCH) residues(vn, rr[(c + 1) & 1]);
+                uint32_t w[kLG];
+                const uint32_t(&rc)[kLG] = rr[c & 1];
+                w[0] = probe<0>(rc[0], boff, smem_raw);
+                w[1] = probe<1>(rc[1], boff, smem_raw);
+                w[2] = probe<2>(rc[2], boff, smem_raw);
+                w[3] = probe<3>(rc[3], boff, smem_raw);
+                w[4] = probe<4>(rc[4], boff, smem_raw);
+                w[5] = probe<5>(rc[5], boff, smem_raw);
+                w[6] = probe<6>(rc[6], boff, smem_raw);
+                w[7] = probe<7>(rc[7], boff, smem_raw);
+                uint32_t bacc = 0;
+#pragma unroll
+                for (int i = 0; i < kLG; ++i)
+                    bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], rr[c & 1][i]), 1);
+                hp[c >> 2] += __popc(bacc & lmask) << (8 * (c & 3));
+                if (sm == ((c / kBPS) + NG - 1) % NG) {  // born at step s - (NG - 1): retires
+                    const int b = s - (NG - 1);
+                    const uint32_t hc = (hp[c >> 2] >> (8 * (c & 3))) & 255u;
+                    hp[c >> 2] &= ~(255u << (8 * (c & 3)));
+                    if (b >= 0) {  // b < nb holds: s < nb + NG - 1
+                        const int64_t t =
+                            cta + (int64_t)((b * kBPS + (c % kBPS)) * kSP + grp) * ncta;
+                        const int64_t row0 = t * kTile + q * 32;
+                        const int64_t row = row0 + lane;
+                        const bool valid = row < a.n;
+                        const int64_t hits = (int64_t)hc;
+                        const unsigned det =
+                            __ballot_sync(0xffffffffu, valid && hits >= a.min_hits);
+                        if (valid && a.hits64) a.hits64[row] = hits;
+                        if (lane0 && row0 < a.n) a.detmask[row0 >> 5] = det;
+                        __syncwarp();
+                        if (lane0) bar_arrive(raw + S.a_empty + 8u * c);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane0) bar_arrive(raw + S.bm_empty + 8u * ring);
+            if (++sm == NG) sm = 0;
+        }
+    }
+
+    // ---- teardown ----
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
+static std::atomic<long long> g_calls{0};
+
+template <int NG>
+static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
+    auto kern = hash_rollf_kernel<NG>;
+    SFFTB_CUDA(smem_opt_in(kern, smem));
+    kern<<<grid, kThreads, smem, st>>>(a);
+    SFFTB_CHECK_LAUNCH();
+    return SFFTB_OK;
+}
+
+}  // namespace rollf
+
+namespace roll {
+unsigned long long* recomputed_counter();
+}
+
+// Returns 1 when the fp16 rolling kernel handled the call, 0 when the shape is
+// outside it (the caller takes the other kernels), < 0 = -status.
+int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* zmat, int64_t L,
+                    int64_t M, const uint32_t* bits, int64_t kbound, int64_t min_hits,
+                    int64_t* hits64, uint32_t* detmask, cudaStream_t st) {
+    using namespace rollf;
+    {
+        const char* e = getenv("SFFTB_HASH_ROLL");
+        if (e && e[0] == '0') return 0;
+        e = getenv("SFFTB_HASH_ROLLF");
+        if (e && e[0] == '0') return 0;
+    }
+    const char* mr = getenv("SFFTB_HASH_ROLL_MINROWS");
+    const int64_t min_rows = mr ? atoll(mr) : (int64_t)1 << 21;
+    if (n < min_rows || n > ((int64_t)1 << 36) || L < 1 || L > kLG * kMaxNG || M < 4096 ||
+        M >= ((int64_t)1 << 22))
+        return 0;
+    if (kbound < 0 || kbound >= kCoordLim) return 0;
+    if (d != 4 && d != 6 && d != 8 && d != 10 && d != 12) return 0;
+    if (((uintptr_t)elems & 15) != 0 || ((uintptr_t)bits & 15) != 0) return 0;
+    // x' = k.z + J M with J = kbound: 0 <= x' <= 2 kbound M
+    const int64_t J = std::max<int64_t>(kbound, 1);
+    const __int128 xmax = (__int128)2 * J * M;
+    if (xmax >= ((__int128)1 << 31)) return 0;
+    const int64_t JM = J * M;
+    int bitsM = 0;
+    while (((int64_t)1 << bitsM) < M) ++bitsM;
+    // limb split c = c0 + 2^s c1 with both limbs < 2048 (fp16-exact), and
+    //   bits0 = C0 + e0 + v0,  bits1 = C0 + T1 + v1,  e0 + 2^s e1 = J M,
+    //   T1 = off1 + e1 with 2^s (C0 + off1) + C0 == 0 (mod 2^32),
+    // both accumulators inside [2^23, 2^24): |v| + constants < 2^22.  Not
+    // every s has a small enough off1: take the most balanced one that does.
+    const uint64_t C0 = kSeedBits;
+    const int64_t half = (int64_t)1 << 22;
+    int s = -1;
+    int64_t e0 = 0, T1 = 0;
+    for (int dist = 0; dist <= 11 && s < 0; ++dist) {
+        for (int sign = 0; sign < 2 && s < 0; ++sign) {
+            const int st_ = (bitsM + 1) / 2 + (sign ? -dist : dist);
+            if (st_ < 1 || st_ > 11 || bitsM - st_ > 11 || (sign && dist == 0)) continue;
+            const int64_t c0max = ((int64_t)1 << st_) - 1, c1max = (M - 1) >> st_;
+            const uint64_t mod = (uint64_t)1 << (32 - st_);
+            const uint64_t X = ((((uint64_t)1 << 32) - C0) >> st_) % mod;  // 2^st_ divides C0
+            const uint64_t off1 = (X + mod - (C0 % mod)) % mod;
+            const int64_t e0_ = JM & c0max, e1_ = JM >> st_;
+            const int64_t T1_ = (int64_t)off1 + e1_;
+            if (e0_ + kbound * c0max >= half) continue;
+            if (T1_ + kbound * c1max >= half) continue;
+            s = st_;
+            e0 = e0_;
+            T1 = T1_;
+        }
+    }
+    if (s < 0) return 0;
+    const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
+    const int64_t ext = (int64_t)(((__int128)M * xmax) >> 32) + 2;
+    const int64_t ext_words = (ext + 31) / 32 + 1;
+    if (ext_words >= (M >> 5)) return 0;
+    const int64_t Wx = ((M >> 5) + ext_words + 1 + 3) & ~int64_t(3);
+    if (Wx * 4 > (int64_t)kSlot) return 0;
+    const int NG = (int)((L + kLG - 1) / kLG);
+    const Smem S = smem_map(NG);
+    const uint32_t smem = S.end;
+    static int prop_smem = 0;
+    if (prop_smem == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&prop_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (prop_smem <= 0) prop_smem = 232448;
+    }
+    if (smem > (uint32_t)prop_smem) return 0;
+    unsigned long long* rec = roll::recomputed_counter();
+    if (!rec) return 0;
+
+    Args a;
+    a.elems = elems;
+    a.n = n;
+    a.zmat = zmat;
+    a.d = (int)d;
+    a.L = (int)L;
+    a.NG = NG;
+    a.M = (uint32_t)M;
+    a.negM = 0u - (uint32_t)M;
+    a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
+    a.s = s;
+    a.pow2s = 1u << s;
+    // A slots (2048, 2048, 1): limb 0 gets 2048 * 6144 = 1.5 * 2^23 and e0;
+    // limb 1 gets 1.5 * 2^23 + T1 with T1 = 2048 t1h + t1l
+    a.seed0[0] = 6144u;
+    a.seed0[1] = 0u;
+    a.seed0[2] = (uint32_t)e0;
+    a.seed1[0] = 6144u;
+    a.seed1[1] = (uint32_t)(T1 >> 11);
+    a.seed1[2] = (uint32_t)(T1 & 2047);
+    a.bits = bits;
+    a.W = (int)W;
+    uint32_t* xbits = nullptr;
+    SFFTB_CUDA(cudaMallocAsync(&xbits, ((size_t)L * Wx + 4) * sizeof(uint32_t), st));
+    a.xbits = xbits;
+    a.Wx = (int)Wx;
+    a.nbad = xbits + (size_t)L * Wx;
+    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, sizeof(unsigned int), st));
+    a.ntiles = (n + kTile - 1) / kTile;
+    a.min_hits = min_hits;
+    a.hits64 = hits64;
+    a.detmask = detmask;
+    a.recomputed = rec;
+    a.dbg = nullptr;
+    static uint32_t* dbg = nullptr;
+    if (getenv("SFFTB_HASH_ROLL_DUMP")) {
+        if (!dbg) SFFTB_CUDA(cudaMalloc(&dbg, 128 * 16 * sizeof(uint32_t)));
+        SFFTB_CUDA(cudaMemsetAsync(dbg, 0xFF, 128 * 16 * sizeof(uint32_t), st));
+        a.dbg = dbg;
+    }
+    int grid = num_sms();
+    if (const char* e = getenv("SFFTB_HASH_ROLL_GRID")) grid = std::max(1, atoi(e));
+    grid = (int)std::min<int64_t>(grid, a.ntiles);
+    if (getenv("SFFTB_HASH_ROLL_DEBUG"))
+        fprintf(stderr,
+                "hash_rollf: d=%d L=%d NG=%d s=%d kbound=%lld e0=%lld T1=%lld ext_words=%d "
+                "smem=%u grid=%d\n",
+                (int)d, (int)L, NG, s, (long long)kbound, (long long)e0, (long long)T1,
+                (int)ext_words, smem, grid);
+    rollptx::roll_extend_kernel<0><<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
+        bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
+    count_launch();
+    int rc = SFFTB_EINVAL;
+    switch (NG) {
+        case 1: rc = launch_ng<1>(a, smem, grid, st); break;
+        case 2: rc = launch_ng<2>(a, smem, grid, st); break;
+        case 3: rc = launch_ng<3>(a, smem, grid, st); break;
+        case 4: rc = launch_ng<4>(a, smem, grid, st); break;
+        case 5: rc = launch_ng<5>(a, smem, grid, st); break;
+        case 6: rc = launch_ng<6>(a, smem, grid, st); break;
+    }
+    if (rc == SFFTB_OK) {
+        rollf_fixup_kernel<<<4 * num_sms(), 256, 0, st>>>(a);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) rc = SFFTB_ECUDA;
+    }
+    cudaFreeAsync(xbits, st);
+    if (a.dbg && rc == SFFTB_OK) {
+        static uint32_t h[128 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int r : {0, 1, 33, 127}) {
+            fprintf(stderr, "rollf dbg row %3d:", r);
+            for (int i = 0; i < 16; ++i) fprintf(stderr, " %08x", h[r * 16 + i]);
+            fprintf(stderr, "\n");
+        }
+    }
+    if (rc == SFFTB_OK) rollf::g_calls.fetch_add(1, std::memory_order_relaxed);
+    return rc == SFFTB_OK ? 1 : -rc;
+}
+
+}  // namespace sfftb
+
+extern "C" int64_t sfftb_hash_rollf_calls(int reset) {
+    return reset ? sfftb::rollf::g_calls.exchange(0) : sfftb::rollf::g_calls.load();
+}

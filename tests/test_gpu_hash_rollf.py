@@ -1,0 +1,130 @@
+"""K3 on the tensor cores, fp16 rolling kernel (csrc/hash_rollf.cu) against
+exact integer hashing.
+
+For candidate sets with a known small magnitude bound (kbound = sum_j max|k_j|
+< 2048) the residues are an exact FP16 x FP16 -> FP32 GEMM (tcgen05 kind::f16,
+A operand in tensor memory, two limbs per lattice, accumulators seeded into
+[2^23, 2^24) so their bit patterns combine with one integer multiply-add).
+Hit counts and the detected bitmask must equal the reference's gather
+(_core.pyx:185-197) bit for bit; the expected values are computed in numpy
+int64 and, independently, by the CUDA-core kernel.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_hash_tc import _bitmaps, _exact_hits, _mask_of
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rows, z, M, words, min_hits, kbound, rollf=True, roll=True):
+    import torch
+
+    from paper_2006_13053_b200 import _dev, _native
+
+    n, d = rows.shape
+    L = z.shape[0]
+    hits = _dev.empty((n,), torch.int64)
+    mask = _dev.empty(((n + 31) // 32,), torch.int32)
+    env = {"SFFTB_HASH_ROLL": "1" if roll else "0", "SFFTB_HASH_ROLLF": "1" if rollf else "0",
+           "SFFTB_HASH_ROLL_MINROWS": "1", "SFFTB_HASH_TC": "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        keep = [_dev.upload(rows), _dev.upload(z), _dev.upload(words.view(np.int32))]
+        _native.call("sfftb_hash_hits", _dev.ptr(keep[0]), n, d, _dev.ptr(keep[1]), 1, L, M,
+                     _dev.ptr(keep[2]), int(kbound), min_hits, _dev.ptr(hits), _dev.ptr(mask),
+                     _dev.stream())
+        h, m = _dev.download(hits), _dev.download(mask).view(np.uint32)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return h, m
+
+
+@pytest.mark.parametrize("d,M,L,span,n", [
+    (10, 103307, 47, 32, 300_001),      # config-4 shape: 6 groups of 8 lattices
+    (10, 103307, 47, 32, 2_500_003),    # every CTA rolls through several births
+    (10, 103307, 48, 100, 400_000),     # all 48 lattice slots, kbound 1000
+    (4, 20663, 31, 16, 200_000),        # 4 groups, last one partly filled
+    (12, 65537, 12, 100, 50_000),       # 2 groups, second half group empty
+    (8, 4099, 5, 16, 70_000),           # one group: born and retired in one step
+    (6, 10331, 41, 300, 131_072),       # kbound 1800, exact multiple of the tile
+    (10, 103307, 47, 32, 1000),         # fewer tiles than CTAs
+    (10, 107837, 33, 8, 250_000),       # larger modulus, 5 groups (three accumulator buffers)
+    (10, 103307, 17, 32, 250_000),      # 3 groups
+])
+def test_rollf_hash_bitexact(cuda, d, M, L, span, n):
+    from paper_2006_13053_b200 import _native
+
+    rng = np.random.default_rng(d * 7919 + L + n)
+    rows = rng.integers(-span, span + 1, size=(n, d), dtype=np.int64)
+    rows[0] = span      # the bound is attained, both signs
+    rows[1] = -span
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    z[0] = M - 1        # largest coefficients
+    bits, words = _bitmaps(rng, L, M, 0.45)
+    min_hits = (L + 1) // 2
+    want = _exact_hits(rows, z, M, bits)
+    kbound = int(np.abs(rows).max(axis=0).sum())
+    assert kbound < 2048
+    lib = _native.lib()
+    lib.sfftb_hash_roll_recomputed(1)
+    lib.sfftb_hash_rollf_calls(1)
+    h, m = _run(rows, z, M, words, min_hits, kbound)
+    assert lib.sfftb_hash_rollf_calls(1) == 1   # the fp16 kernel served the call
+    assert lib.sfftb_hash_roll_recomputed(1) == 0
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, min_hits))
+    # the byte-limb rolling kernel and the CUDA-core kernel agree
+    h_b, m_b = _run(rows, z, M, words, min_hits, kbound, rollf=False)
+    assert np.array_equal(h_b, want) and np.array_equal(m_b, m)
+    h_cc, m_cc = _run(rows, z, M, words, min_hits, kbound, rollf=False, roll=False)
+    assert np.array_equal(h_cc, want) and np.array_equal(m_cc, m)
+
+
+def test_rollf_negative_generators_and_sparse_bitmaps(cuda):
+    """Generators given as negative / unreduced int64 and nearly empty or
+    nearly full bitmaps (hits 0 and L)."""
+    rng = np.random.default_rng(11)
+    d, M, L, n = 10, 103307, 47, 200_000
+    rows = rng.integers(-32, 33, size=(n, d), dtype=np.int64)
+    z = rng.integers(-5 * M, 5 * M, size=(L, d), dtype=np.int64)
+    kbound = int(np.abs(rows).max(axis=0).sum())
+    for dens in (0.001, 0.999):
+        bits, words = _bitmaps(rng, L, M, dens)
+        want = _exact_hits(rows, z, M, bits)
+        h, m = _run(rows, z, M, words, 24, kbound)
+        assert np.array_equal(h, want)
+        assert np.array_equal(m, _mask_of(want, 24))
+
+
+def test_rollf_rows_outside_the_half_range_are_redone_exactly(cuda):
+    """A caller's bound that does not hold for a few rows (a coordinate
+    outside (-2048, 2048)): the loaders flag them and the follow-up kernel
+    recomputes exactly those rows."""
+    from paper_2006_13053_b200 import _native
+
+    rng = np.random.default_rng(5)
+    d, M, L, n = 10, 103307, 47, 150_000
+    rows = rng.integers(-32, 33, size=(n, d), dtype=np.int64)
+    bad = rng.choice(n, size=37, replace=False)
+    rows[bad, rng.integers(0, d, size=37)] = rng.integers(2048, 1 << 40, size=37) * \
+        rng.choice([-1, 1], size=37)
+    rows[bad[0], 3] = 2048
+    rows[bad[1], 3] = -2049
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    bits, words = _bitmaps(rng, L, M, 0.3)
+    want = _exact_hits(rows, z, M, bits)
+    lib = _native.lib()
+    lib.sfftb_hash_roll_recomputed(1)
+    h, m = _run(rows, z, M, words, 20, 320)
+    assert lib.sfftb_hash_roll_recomputed(1) == 37
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, 20))

@@ -17,7 +17,8 @@ lg = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 103307
 L = int(sys.argv[4]) if len(sys.argv) > 4 else 47
-n, d, N = 1 << lg, 10, 4096
+N = int(sys.argv[5]) if len(sys.argv) > 5 else 4096  # coordinate span; 32 = config 4's box
+n, d = 1 << lg, 10
 g = torch.Generator(device="cuda")
 g.manual_seed(1)
 rows = torch.randint(-N, N + 1, (n, d), generator=g, device="cuda", dtype=torch.int64)
