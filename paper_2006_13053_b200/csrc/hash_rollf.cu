@@ -105,11 +105,12 @@ __device__ int exact_row_hits(const Args& a, int d, int64_t row) {
 // Runs after every launch: exits at once unless a loader met a coordinate
 // outside the fp16 range; otherwise redoes those rows exactly.
 __global__ void __launch_bounds__(256) rollf_fixup_kernel(Args a) {
-    if (*reinterpret_cast<volatile unsigned int*>(a.nbad) == 0u) return;
+    const unsigned int nbad = *reinterpret_cast<volatile unsigned int*>(a.nbad);
+    if (nbad == 0u) return;
     const int d = a.d;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < a.n;
          row += (int64_t)gridDim.x * blockDim.x) {
-        bool bad = false;
+        bool bad = (nbad & 0x80000000u) != 0u;  // the main kernel did not run
         for (int j = 0; j < d; ++j)
             bad |= ((uint64_t)(a.elems[row * d + j] + kCoordLim) >> 12) != 0;
         if (!bad) continue;
@@ -169,12 +170,24 @@ __device__ __forceinline__ uint32_t half_bits(float v) {
 }
 
 // Bitmap word of residue r in slot I of the ring buffer at byte offset boff
-// (0 or kBufStride) of the window: the mask keeps the offset below 16 KB for
-// any r (see Smem).  Plain C++ so that the window base stays in a uniform
-// register and the slot is the load's immediate: SHF + LOP3 + LDS [R + UR + imm].
+// (0 or kBufStride) of the dynamic window: the mask keeps the offset below
+// 16 KB for any r (see Smem).  SHF + LOP3 + LDS with the window base and the
+// slot as the load's immediate: the dynamic shared memory of a kernel without
+// static shared memory starts at address kWin of the shared window (the
+// compiler itself materialises that constant); the kernel checks it and
+// leaves the whole call to the exact follow-up kernel if it ever differs.
+constexpr uint32_t kWin = 0x400u;
+constexpr unsigned int kAllRows = 0x80000000u;
 template <int I>
-__device__ __forceinline__ uint32_t probe(uint32_t r, uint32_t boff, const uint8_t* win) {
-    return *reinterpret_cast<const uint32_t*>(win + I * kSlot + (((r >> 3) & 0x3FFCu) | boff));
+__device__ __forceinline__ uint32_t probe(uint32_t r, uint32_t boff) {
+    uint32_t w;
+    asm volatile("{\n\t.reg .u32 t;\n\t"
+                 "shr.u32 t, %1, 3;\n\t"
+                 "lop3.b32 t, t, 0x3FFC, %2, 0xEA;\n\t"
+                 "ld.shared.u32 %0, [t+%3];\n\t}"
+                 : "=r"(w)
+                 : "r"(r), "r"(boff), "n"(kWin + I * kSlot));
+    return w;
 }
 
 // Row loader of one warp: lane quadrant q = warp & 3, tiles k = hsel, hsel + 2
@@ -311,6 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     constexpr int ND = (dcol0 + 3 * dstride <= 512) ? 3 : 2;
     static_assert(dcol0 + ND * dstride <= 512, "tensor memory");
     const int D = a.d;
+    if (raw != kWin) {  // see probe(): never on current toolchains; exact path for every row
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(a.nbad, kAllRows);
+        return;
+    }
 
     // ---- setup ----
     if (threadIdx.x == 0) {
@@ -462,9 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
             uint32_t boff = (uint32_t)ring * kBufStride;
             asm volatile("" : "+r"(boff));  // one register per step, not rematerialised per probe
             bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1));
-            // Software pipeline over the step's cohorts: while cohort c is
-            // probed, the residues of cohort c + 1 are computed and the
-            // accumulators of cohort c + 2 are in flight.
+            // Software pipeline over the step's cohorts: while the bits of
+            // cohort c are counted, the bitmap words of cohort c + 1 are on
+            // their way from shared memory and the accumulators of cohort
+            // c + 2 on their way from tensor memory.
             auto residues = [&](const uint32_t (&v)[16], uint32_t (&r)[kLG]) {
 #pragma unroll
                 for (int i = 0; i < kLG; ++i) {
@@ -476,7 +494,17 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
                 }
             };
-            uint32_t rr[2][kLG];
+            auto probes = [&](const uint32_t (&r)[kLG], uint32_t (&w)[kLG]) {
+                w[0] = probe<0>(r[0], boff);
+                w[1] = probe<1>(r[1], boff);
+                w[2] = probe<2>(r[2], boff);
+                w[3] = probe<3>(r[3], boff);
+                w[4] = probe<4>(r[4], boff);
+                w[5] = probe<5>(r[5], boff);
+                w[6] = probe<6>(r[6], boff);
+                w[7] = probe<7>(r[7], boff);
+            };
+            uint32_t rr[2][kLG], ww[2][kLG];
             bar_wait(dfull, par[0]);
             par[0] ^= 1u;
             tc_fence_after();
@@ -496,6 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                 tmem_ld16_async(tlane + (uint32_t)(dstride * (1 % ND)), vb);
             }
             residues(va, rr[0]);
+            probes(rr[0], ww[0]);
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 uint32_t(&vc)[16] = (c & 1) ? vb : va;  // cohort c: consumed, reused for c + 2
@@ -513,21 +542,15 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                     tc_fence_after();
                     tmem_ld16_async(tlane + (uint32_t)(dstride * b2), vc);
                 }
-                if (c + 1 < NCH) residues(vn, rr[(c + 1) & 1]);
-                uint32_t w[kLG];
-                const uint32_t(&rc)[kLG] = rr[c & 1];
-                w[0] = probe<0>(rc[0], boff, smem_raw);
-                w[1] = probe<1>(rc[1], boff, smem_raw);
-                w[2] = probe<2>(rc[2], boff, smem_raw);
-                w[3] = probe<3>(rc[3], boff, smem_raw);
-                w[4] = probe<4>(rc[4], boff, smem_raw);
-                w[5] = probe<5>(rc[5], boff, smem_raw);
-                w[6] = probe<6>(rc[6], boff, smem_raw);
-                w[7] = probe<7>(rc[7], boff, smem_raw);
+                if (c + 1 < NCH) {
+                    residues(vn, rr[(c + 1) & 1]);
+                    probes(rr[(c + 1) & 1], ww[(c + 1) & 1]);
+                }
                 uint32_t bacc = 0;
 #pragma unroll
                 for (int i = 0; i < kLG; ++i)
-                    bacc = __funnelshift_r(bacc, __funnelshift_r(w[i], w[i], rr[c & 1][i]), 1);
+                    bacc = __funnelshift_r(
+                        bacc, __funnelshift_r(ww[c & 1][i], ww[c & 1][i], rr[c & 1][i]), 1);
                 hp[c >> 2] += __popc(bacc & lmask) << (8 * (c & 3));
                 if (sm == ((c / kBPS) + NG - 1) % NG) {  // born at step s - (NG - 1): retires
                     const int b = s - (NG - 1);
