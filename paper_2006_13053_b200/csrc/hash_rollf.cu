@@ -47,7 +47,9 @@ using namespace rollptx;
 constexpr int kThreads = 832;
 constexpr int kTile = 128;
 constexpr int kLG = 8;          // lattices per group (two accumulator columns each)
-constexpr int kNC = 16;         // MMA N
+constexpr int kNC = 16;         // MMA N, fp16 mode: 8 lattices x 2 limbs
+constexpr int kNCW = 24;        // MMA N, byte mode: 8 lattices x 3 limbs
+constexpr int64_t kOffsetW = 8192;  // byte mode: u = k + kOffsetW must lie in [0, 2^14)
 constexpr int kACols = 8;       // TMEM columns of one A tile (K = 16 halves)
 constexpr int kSP = 4;          // tiles per cohort (one per epilogue warp group)
 constexpr int kBPS = 2;         // cohorts born per step
@@ -68,6 +70,7 @@ struct Args {
     const int64_t* zmat;  // (L, d)
     int d, L, NG;
     uint32_t M, negM, magic;
+    int wide;              // byte mode (see hash_rollf_kernel)
     int s;                 // limb split: c = c0 + 2^s c1
     uint32_t pow2s;
     // B-operand constants of the seed slots (A = 2048, 2048, 1), per limb
@@ -112,7 +115,8 @@ __global__ void __launch_bounds__(256) rollf_fixup_kernel(Args a) {
          row += (int64_t)gridDim.x * blockDim.x) {
         bool bad = (nbad & 0x80000000u) != 0u;  // the main kernel did not run
         for (int j = 0; j < d; ++j)
-            bad |= ((uint64_t)(a.elems[row * d + j] + kCoordLim) >> 12) != 0;
+            bad |= a.wide ? ((uint64_t)(a.elems[row * d + j] + kOffsetW) >> 14) != 0
+                          : ((uint64_t)(a.elems[row * d + j] + kCoordLim) >> 12) != 0;
         if (!bad) continue;
         const int64_t hits = exact_row_hits(a, d, row);
         atomicAdd(a.recomputed, 1ull);
@@ -148,12 +152,18 @@ __host__ __device__ inline Smem smem_map(int NG) {
     s.tmem_holder = o; o += 16;
     o = (o + 127u) & ~127u;
     s.bop = o;      o += (uint32_t)kMaxNG * 512u;  // B operand: NG x [2][16][16 B]
-    (void)NG;
+    (void)NG;  // byte mode (768 B per group): groups 0-3 here, 4-5 behind the loader buffers
     s.stage = kBufStride + kBuf;                   // loader transposition (RS <= 7)
     s.end = s.stage + (uint32_t)kLoaders * 32u * 7u * 4u;
     return s;
 }
 static_assert(kBuf + 512u + kMaxNG * 512u <= kBufStride, "tables fit the gap between the buffers");
+static_assert(kBuf + 512u + 4u * 768u <= kBufStride, "byte-mode B operands of groups 0-3 fit the gap");
+// byte mode is limited to d <= 10 (RS = 5): its loaders use 5120 B, groups 4-5 follow
+__host__ __device__ inline uint32_t bop_wide(const Smem& S, int g) {
+    return g < 4 ? S.bop + (uint32_t)g * 768u
+                 : S.stage + (uint32_t)kLoaders * 32u * 5u * 4u + (uint32_t)(g - 4) * 768u;
+}
 static_assert(kBuf % 16u == 0 && (kBufStride & 0x3FFFu) == 0, "buffer alignment");
 static_assert((kLG - 1) * kSlot + 16384u <= kBufStride, "probe overrun of buffer 0 stays in the gap");
 static_assert((kLG - 1) * kSlot + 16384u <= kBuf + kLoaders * 32u * 7u * 4u,
@@ -194,7 +204,7 @@ __device__ __forceinline__ uint32_t probe(uint32_t r, uint32_t boff) {
 // of both cohorts of every birth.  Coalesced 16-byte loads (a coordinate pair
 // each), converted to an fp16 pair, transposed through shared memory to
 // thread-per-row, stored into the cohort's A tiles in tensor memory.
-template <int D>
+template <int D, bool WIDE>
 __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const Ctx& x,
                                            uint8_t* smem_raw) {
     constexpr int H = D / 2;   // 16-byte chunks (coordinate pairs) per row
@@ -241,17 +251,32 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
         uint32_t bad = 0;
 #pragma unroll
         for (int i = 0; i < H; ++i) {
-            // in range <=> k + 2048 as 64 bits < 4096
-            uint32_t l0, h0, l1, h1;
-            asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
-                : "=r"(l0), "=r"(h0)
-                : "r"(cur[i].x), "r"(cur[i].y));
-            asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
-                : "=r"(l1), "=r"(h1)
-                : "r"(cur[i].z), "r"(cur[i].w));
-            bad |= (h0 | h1) | ((l0 | l1) >> 12);
-            const __half2 hh = __floats2half2_rn((float)cur[i].x, (float)cur[i].z);
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(&hh);
+            uint32_t l0, h0, l1, h1, w;
+            if (WIDE) {
+                // u = k + 2^13 as 64 bits: in range <=> high word 0 and low < 2^14;
+                // a + 256 b for u = a + 128 b is u + (u & ~127): bytes a0 b0 a1 b1
+                asm("add.cc.u32 %0, %2, 8192;\n\taddc.u32 %1, %3, 0;"
+                    : "=r"(l0), "=r"(h0)
+                    : "r"(cur[i].x), "r"(cur[i].y));
+                asm("add.cc.u32 %0, %2, 8192;\n\taddc.u32 %1, %3, 0;"
+                    : "=r"(l1), "=r"(h1)
+                    : "r"(cur[i].z), "r"(cur[i].w));
+                bad |= (h0 | h1) | ((l0 | l1) >> 14);
+                const uint32_t p0 = (l0 & 0x3FFFu) + (l0 & 0x3F80u);
+                const uint32_t p1 = (l1 & 0x3FFFu) + (l1 & 0x3F80u);
+                w = (p1 << 16) + p0;
+            } else {
+                // in range <=> k + 2048 as 64 bits < 4096
+                asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
+                    : "=r"(l0), "=r"(h0)
+                    : "r"(cur[i].x), "r"(cur[i].y));
+                asm("add.cc.u32 %0, %2, 2048;\n\taddc.u32 %1, %3, 0;"
+                    : "=r"(l1), "=r"(h1)
+                    : "r"(cur[i].z), "r"(cur[i].w));
+                bad |= (h0 | h1) | ((l0 | l1) >> 12);
+                const __half2 hh = __floats2half2_rn((float)cur[i].x, (float)cur[i].z);
+                w = *reinterpret_cast<const uint32_t*>(&hh);
+            }
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst[i]), "r"(w) : "memory");
         }
         if (__any_sync(0xffffffffu, bad != 0u)) {  // also orders the stores (warp-convergent)
@@ -261,8 +286,12 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
         uint32_t r[8];
 #pragma unroll
         for (int p = 0; p < 8; ++p) r[p] = p < H ? stg[lane * RS + p] : 0u;
-        r[H] = 0x68006800u;      // K = D, D + 1: the constants 2048, 2048
-        r[H + 1] = 0x00003C00u;  // K = D + 2: the constant 1
+        if (WIDE) {
+            r[H] = 1u;  // byte K = 2D: the constant 1 (k = u - 2^13)
+        } else {
+            r[H] = 0x68006800u;      // K = D, D + 1: the constants 2048, 2048
+            r[H + 1] = 0x00003C00u;  // K = D + 2: the constant 1
+        }
         __syncwarp();
         const int c = c0 + (u >> 1);
         if (!(u & 1) && beta >= 1)  // the cohort's previous occupants have retired
@@ -307,7 +336,15 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
 // same NCH items (cohorts in index order, four tiles each, accumulator buffer
 // c % ND): cohorts not yet born or past the end of the rows are processed as
 // dummies (their outputs are never written), so the schedule is static.
-template <int NG>
+//
+// WIDE = byte mode for coordinates in [-2^13, 2^13) (any kbound), the limb
+// scheme of hash_roll.cu on this kernel's schedule: u = k + 2^13 = a + 128 b
+// packed as bytes, tcgen05 kind::i8 with THREE base-256 limbs per lattice
+// (N = 24 for the same 8 lattices per group), x = v0 + 256 v1 + 65536 v2.
+// The 24-column accumulators leave room for two HALF-cohort buffers (tiles
+// 0-1 and 2-3: 2 x 48 columns behind the 384 A columns); epilogue warp groups
+// 0-1 and 2-3 each wait on their own buffer, loaded one cohort ahead.
+template <int NG, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     constexpr int NCH = NG * kBPS;
@@ -320,8 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     const int nb = (my_tiles + kSP * kBPS - 1) / (kSP * kBPS);  // births (kBPS cohorts each)
     const int nsteps = nb > 0 ? nb + NG - 1 : 0;
     constexpr int dcol0 = NCH * kSP * kACols;
-    constexpr int dstride = kNC * kSP;  // accumulator columns of one cohort
-    constexpr int ND = (dcol0 + 3 * dstride <= 512) ? 3 : 2;
+    // fp16 mode: ND buffers of one cohort's accumulators (4 tiles x 16 columns);
+    // byte mode: 2 buffers of half a cohort's (2 tiles x 24 columns)
+    constexpr int dstride = WIDE ? kNCW * 2 : kNC * kSP;
+    constexpr int ND = WIDE ? 2 : ((dcol0 + 3 * dstride <= 512) ? 3 : 2);
     static_assert(dcol0 + ND * dstride <= 512, "tensor memory");
     const int D = a.d;
     if (raw != kWin) {  // see probe(): never on current toolchains; exact path for every row
@@ -337,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
         }
         for (int i = 0; i < ND; ++i) {
             bar_init(raw + S.d_full + 8u * i, 1);
-            bar_init(raw + S.d_empty + 8u * i, kEpiWarps);
+            bar_init(raw + S.d_empty + 8u * i, WIDE ? kEpiWarps / 2 : kEpiWarps);
         }
         for (int i = 0; i < NCH; ++i) {
             bar_init(raw + S.a_full + 8u * i, kLoaders);
@@ -352,28 +391,62 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    // B operand of group g: [2 K-chunks][16 columns][8 halves]; column 2i +
-    // limb for lattice g*kLG + i.  K index kb: < D the coordinate, D and D + 1
-    // the 2048 slots, D + 2 the unit slot.
-    for (uint32_t e = threadIdx.x; e < (uint32_t)NG * 256u; e += blockDim.x) {
-        const int g = (int)(e / 256u);
-        const uint32_t in = e % 256u;
-        const int col = (int)((in / 8u) % 16u);
-        const int kb = (int)(in / 128u) * 8 + (int)(in % 8u);
-        const int i = col >> 1, limb = col & 1;
-        const int l = g * kLG + i;
-        float v = 0.f;
-        if (l < a.L) {
-            if (kb < D) {
-                int64_t z = a.zmat[(int64_t)l * D + kb] % (int64_t)a.M;
-                if (z < 0) z += a.M;
-                const uint32_t c = (uint32_t)z;
-                v = (float)(limb ? (c >> a.s) : (c & (a.pow2s - 1u)));
-            } else if (kb < D + 3) {
-                v = (float)(limb ? a.seed1[kb - D] : a.seed0[kb - D]);
+    if (WIDE) {
+        // B operand of group g: [2 K-chunks][24 columns][16 B]; column 3i + limb for
+        // lattice g*kLG + i.  K bytes: 4p + e = coordinate 2p + (e >> 1), limb
+        // weight (e & 1) ? 128 : 1; 2D = the constant (k = u - 2^13).
+        for (uint32_t e = threadIdx.x; e < (uint32_t)NG * 768u; e += blockDim.x) {
+            const int g = (int)(e / 768u);
+            const uint32_t in = e % 768u;
+            const int col = (int)((in / 16u) % 24u);
+            const int kb = (int)(in / 384u) * 16 + (int)(in % 16u);
+            const int i = col / 3, limb = col % 3;
+            const int l = g * kLG + i;
+            uint32_t v = 0;
+            if (l < a.L) {
+                uint64_t c = 0;
+                if (kb < 2 * D) {
+                    int64_t z = a.zmat[(int64_t)l * D + (kb >> 1)] % (int64_t)a.M;
+                    if (z < 0) z += a.M;
+                    c = ((uint64_t)z * ((kb & 1) ? 128u : 1u)) % a.M;
+                } else if (kb == 2 * D) {
+                    uint64_t zs = 0;
+                    for (int j = 0; j < D; ++j) {
+                        int64_t z = a.zmat[(int64_t)l * D + j] % (int64_t)a.M;
+                        if (z < 0) z += a.M;
+                        zs += (uint64_t)z;
+                    }
+                    const uint64_t t2 = ((zs % a.M) * (uint64_t)(kOffsetW % (int64_t)a.M)) % a.M;
+                    c = (a.M - t2) % a.M;
+                }
+                v = (uint32_t)(c >> (8 * limb)) & 255u;
             }
+            smem_raw[bop_wide(S, g) + in] = (uint8_t)v;
         }
-        reinterpret_cast<uint16_t*>(smem_raw + S.bop)[e] = (uint16_t)half_bits(v);
+    } else {
+        // B operand of group g: [2 K-chunks][16 columns][8 halves]; column 2i +
+        // limb for lattice g*kLG + i.  K index kb: < D the coordinate, D and D + 1
+        // the 2048 slots, D + 2 the unit slot.
+        for (uint32_t e = threadIdx.x; e < (uint32_t)NG * 256u; e += blockDim.x) {
+            const int g = (int)(e / 256u);
+            const uint32_t in = e % 256u;
+            const int col = (int)((in / 8u) % 16u);
+            const int kb = (int)(in / 128u) * 8 + (int)(in % 8u);
+            const int i = col >> 1, limb = col & 1;
+            const int l = g * kLG + i;
+            float v = 0.f;
+            if (l < a.L) {
+                if (kb < D) {
+                    int64_t z = a.zmat[(int64_t)l * D + kb] % (int64_t)a.M;
+                    if (z < 0) z += a.M;
+                    const uint32_t c = (uint32_t)z;
+                    v = (float)(limb ? (c >> a.s) : (c & (a.pow2s - 1u)));
+                } else if (kb < D + 3) {
+                    v = (float)(limb ? a.seed1[kb - D] : a.seed0[kb - D]);
+                }
+            }
+            reinterpret_cast<uint16_t*>(smem_raw + S.bop)[e] = (uint16_t)half_bits(v);
+        }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
@@ -405,30 +478,56 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     } else if (warp == 1) {
         // ================= MMA issuer =================
         const bool leader = elect_one();
-        // kind::f16: D = f32 (1 << 4), A = B = f16 (0), K-major, N >> 3, M >> 4
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
+        // kind::f16: D = f32 (1 << 4), A = B = f16 (0); kind::i8: D = s32 (2 << 4),
+        // A = B = u8 (0); K-major, N >> 3, M >> 4
+        constexpr int NCOL = WIDE ? kNCW : kNC;
+        const uint32_t idesc = ((WIDE ? 2u : 1u) << 4) | ((uint32_t)(NCOL >> 3) << 17) |
+                               ((uint32_t)(kTile >> 4) << 24);
         uint32_t epar[3] = {1u, 1u, 1u};
         bool used[3] = {false, false, false};
         int sm = 0, beta = 0;
         for (int s = 0; s < nsteps; ++s) {
-            const uint64_t bdesc = umma_desc(raw + S.bop + (uint32_t)sm * 512u, 256u, 128u);
+            const uint64_t bdesc =
+                WIDE ? umma_desc(raw + bop_wide(S, sm), 384u, 128u)
+                     : umma_desc(raw + S.bop + (uint32_t)sm * 512u, 256u, 128u);
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                const int buf = c % ND;
-                if (used[buf]) bar_wait(raw + S.d_empty + 8u * buf, epar[buf]);
-                used[buf] = true;
-                epar[buf] ^= 1u;
-                if ((c / kBPS) == sm && s < nb)  // newborn cohort: its rows are in tensor memory
-                    bar_wait(raw + S.a_full + 8u * c, (uint32_t)(beta & 1));
-                tc_fence_after();
-                if (leader) {
+                if (WIDE) {
 #pragma unroll
-                    for (int k = 0; k < kSP; ++k)
-                        umma_f16_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
-                                    tmem + (uint32_t)((c * kSP + k) * kACols), bdesc, idesc);
-                    umma_commit(raw + S.d_full + 8u * buf);
+                    for (int h = 0; h < 2; ++h) {  // tiles 2h, 2h + 1 into half buffer h
+                        if (used[h]) bar_wait(raw + S.d_empty + 8u * h, epar[h]);
+                        used[h] = true;
+                        epar[h] ^= 1u;
+                        if (h == 0 && (c / kBPS) == sm && s < nb)
+                            bar_wait(raw + S.a_full + 8u * c, (uint32_t)(beta & 1));
+                        tc_fence_after();
+                        if (leader) {
+#pragma unroll
+                            for (int k = 0; k < 2; ++k)
+                                umma_i8_ts(tmem + (uint32_t)(dcol0 + dstride * h + kNCW * k),
+                                           tmem + (uint32_t)((c * kSP + 2 * h + k) * kACols),
+                                           bdesc, idesc);
+                            umma_commit(raw + S.d_full + 8u * h);
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    const int buf = c % ND;
+                    if (used[buf]) bar_wait(raw + S.d_empty + 8u * buf, epar[buf]);
+                    used[buf] = true;
+                    epar[buf] ^= 1u;
+                    if ((c / kBPS) == sm && s < nb)  // newborn cohort: its rows are in tensor memory
+                        bar_wait(raw + S.a_full + 8u * c, (uint32_t)(beta & 1));
+                    tc_fence_after();
+                    if (leader) {
+#pragma unroll
+                        for (int k = 0; k < kSP; ++k)
+                            umma_f16_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
+                                        tmem + (uint32_t)((c * kSP + k) * kACols), bdesc, idesc);
+                        umma_commit(raw + S.d_full + 8u * buf);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             if (++sm == NG) {
                 sm = 0;
@@ -446,12 +545,21 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
         x.NG = NG;
         x.cta = cta;
         x.ncta = ncta;
-        switch (D) {
-            case 4: run_loader<4>(a, S, x, smem_raw); break;
-            case 6: run_loader<6>(a, S, x, smem_raw); break;
-            case 8: run_loader<8>(a, S, x, smem_raw); break;
-            case 10: run_loader<10>(a, S, x, smem_raw); break;
-            default: run_loader<12>(a, S, x, smem_raw); break;
+        if (WIDE) {
+            switch (D) {
+                case 4: run_loader<4, true>(a, S, x, smem_raw); break;
+                case 6: run_loader<6, true>(a, S, x, smem_raw); break;
+                case 8: run_loader<8, true>(a, S, x, smem_raw); break;
+                default: run_loader<10, true>(a, S, x, smem_raw); break;
+            }
+        } else {
+            switch (D) {
+                case 4: run_loader<4, false>(a, S, x, smem_raw); break;
+                case 6: run_loader<6, false>(a, S, x, smem_raw); break;
+                case 8: run_loader<8, false>(a, S, x, smem_raw); break;
+                case 10: run_loader<10, false>(a, S, x, smem_raw); break;
+                default: run_loader<12, false>(a, S, x, smem_raw); break;
+            }
         }
     } else {
         // ================= epilogue =================
@@ -470,7 +578,13 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
         for (int i = 0; i < (NCH + 3) / 4; ++i) hp[i] = 0;
         uint32_t par[3] = {0u, 0u, 0u};
         int sm = 0;
-        uint32_t va[16], vb[16];
+        // byte mode: this warp's half buffer (tiles 0-1 / 2-3) and its tile's columns
+        const int hb = grp >> 1;
+        uint32_t tlw = tmem + ((uint32_t)(q * 32) << 16) +
+                       (uint32_t)(dcol0 + dstride * hb + kNCW * (grp & 1));
+        uint32_t dfullw = raw + S.d_full + 8u * hb, demptyw = raw + S.d_empty + 8u * hb;
+        asm volatile("" : "+r"(tlw), "+r"(dfullw), "+r"(demptyw));
+        uint32_t parw = 0u;
         for (int s = 0; s < nsteps; ++s) {
             const int lcg = max(0, min(a.L, sm * kLG + kLG) - sm * kLG);
             // pair i's bit ends at position 32 - kLG + i of the accumulator
@@ -479,20 +593,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
             uint32_t boff = (uint32_t)ring * kBufStride;
             asm volatile("" : "+r"(boff));  // one register per step, not rematerialised per probe
             bar_wait(raw + S.bm_full + 8u * ring, (uint32_t)((s >> 1) & 1));
-            // Software pipeline over the step's cohorts: while the bits of
-            // cohort c are counted, the bitmap words of cohort c + 1 are on
-            // their way from shared memory and the accumulators of cohort
-            // c + 2 on their way from tensor memory.
-            auto residues = [&](const uint32_t (&v)[16], uint32_t (&r)[kLG]) {
-#pragma unroll
-                for (int i = 0; i < kLG; ++i) {
-                    uint32_t xx;
-                    asm("mad.lo.u32 %0, %1, %2, %3;"
-                        : "=r"(xx)
-                        : "r"(v[2 * i + 1]), "r"(pow2s), "r"(v[2 * i]));
-                    const uint32_t qq = __umulhi(xx, magic);
-                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[i]) : "r"(qq), "r"(negM), "r"(xx));
-                }
+            // residues in [0, M + ext): x - umulhi(x, 2^32/M) M
+            auto reduce = [&](uint32_t xx) -> uint32_t {
+                const uint32_t qq = __umulhi(xx, magic);
+                uint32_t r;
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(qq), "r"(negM), "r"(xx));
+                return r;
             };
             auto probes = [&](const uint32_t (&r)[kLG], uint32_t (&w)[kLG]) {
                 w[0] = probe<0>(r[0], boff);
@@ -504,53 +610,14 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                 w[6] = probe<6>(r[6], boff);
                 w[7] = probe<7>(r[7], boff);
             };
-            uint32_t rr[2][kLG], ww[2][kLG];
-            bar_wait(dfull, par[0]);
-            par[0] ^= 1u;
-            tc_fence_after();
-            tmem_ld16_async(tlane, va);
-            tmem_wait_ld16(va);
-            tc_fence_before();
-            __syncwarp();
-            if (lane0) bar_arrive(dempty);
-            if (a.dbg && s == 0 && cta == 0 && grp == 0) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = va[i];
-            }
-            if (NCH > 1) {
-                bar_wait(dfull + 8u * (1 % ND), par[1 % ND]);
-                par[1 % ND] ^= 1u;
-                tc_fence_after();
-                tmem_ld16_async(tlane + (uint32_t)(dstride * (1 % ND)), vb);
-            }
-            residues(va, rr[0]);
-            probes(rr[0], ww[0]);
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                uint32_t(&vc)[16] = (c & 1) ? vb : va;  // cohort c: consumed, reused for c + 2
-                uint32_t(&vn)[16] = (c & 1) ? va : vb;  // cohort c + 1: in flight
-                const int b1 = (c + 1) % ND, b2 = (c + 2) % ND;
-                if (c + 1 < NCH) {
-                    tmem_wait_ld16(vn);
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane0) bar_arrive(dempty + 8u * b1);
-                }
-                if (c + 2 < NCH) {
-                    bar_wait(dfull + 8u * b2, par[b2]);
-                    par[b2] ^= 1u;
-                    tc_fence_after();
-                    tmem_ld16_async(tlane + (uint32_t)(dstride * b2), vc);
-                }
-                if (c + 1 < NCH) {
-                    residues(vn, rr[(c + 1) & 1]);
-                    probes(rr[(c + 1) & 1], ww[(c + 1) & 1]);
-                }
+            // the bits of cohort c (words wc, residues rc) into its hit counter;
+            // a cohort that has now seen every group retires
+            auto count_retire = [&](const int c, const uint32_t (&rc)[kLG],
+                                    const uint32_t (&wc)[kLG]) {
                 uint32_t bacc = 0;
 #pragma unroll
                 for (int i = 0; i < kLG; ++i)
-                    bacc = __funnelshift_r(
-                        bacc, __funnelshift_r(ww[c & 1][i], ww[c & 1][i], rr[c & 1][i]), 1);
+                    bacc = __funnelshift_r(bacc, __funnelshift_r(wc[i], wc[i], rc[i]), 1);
                 hp[c >> 2] += __popc(bacc & lmask) << (8 * (c & 3));
                 if (sm == ((c / kBPS) + NG - 1) % NG) {  // born at step s - (NG - 1): retires
                     const int b = s - (NG - 1);
@@ -571,9 +638,116 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                         if (lane0) bar_arrive(raw + S.a_empty + 8u * c);
                     }
                 }
+            };
+            uint32_t rr[2][kLG], ww[2][kLG];
+            if (WIDE) {
+                // Software pipeline: while the bits of cohort c are counted, the
+                // accumulators of cohort c + 1 come from tensor memory; its
+                // bitmap words are requested before cohort c + 1 is counted.
+                uint32_t v[24];
+                auto residues = [&](uint32_t (&r)[kLG]) {
+#pragma unroll
+                    for (int i = 0; i < kLG; ++i) {
+                        uint32_t xx = (v[3 * i + 1] << 8) + v[3 * i];
+                        xx = (v[3 * i + 2] << 16) + xx;
+                        r[i] = reduce(xx);
+                    }
+                };
+                bar_wait(dfullw, parw);
+                parw ^= 1u;
+                tc_fence_after();
+                tmem_ld24_async(tlw, v);
+                tmem_wait_ld24(v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane0) bar_arrive(demptyw);
+                if (a.dbg && s == 0 && cta == 0 && grp == 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = v[i];
+                }
+                residues(rr[0]);
+                probes(rr[0], ww[0]);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    if (c + 1 < NCH) {
+                        bar_wait(dfullw, parw);
+                        parw ^= 1u;
+                        tc_fence_after();
+                        tmem_ld24_async(tlw, v);
+                    }
+                    if (c + 1 < NCH) {
+                        tmem_wait_ld24(v);
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane0) bar_arrive(demptyw);
+                        residues(rr[(c + 1) & 1]);
+                        probes(rr[(c + 1) & 1], ww[(c + 1) & 1]);
+                    }
+                    // after the release: the MMA of cohort c + 2 runs behind this
+                    count_retire(c, rr[c & 1], ww[c & 1]);
+                }
+            } else {
+                // Software pipeline over the step's cohorts: while the bits of
+                // cohort c are counted, the bitmap words of cohort c + 1 are on
+                // their way from shared memory and the accumulators of cohort
+                // c + 2 on their way from tensor memory.
+                uint32_t va[16], vb[16];
+                auto residues = [&](const uint32_t (&v)[16], uint32_t (&r)[kLG]) {
+#pragma unroll
+                    for (int i = 0; i < kLG; ++i) {
+                        uint32_t xx;
+                        asm("mad.lo.u32 %0, %1, %2, %3;"
+                            : "=r"(xx)
+                            : "r"(v[2 * i + 1]), "r"(pow2s), "r"(v[2 * i]));
+                        r[i] = reduce(xx);
+                    }
+                };
+                bar_wait(dfull, par[0]);
+                par[0] ^= 1u;
+                tc_fence_after();
+                tmem_ld16_async(tlane, va);
+                tmem_wait_ld16(va);
+                tc_fence_before();
+                __syncwarp();
+                if (lane0) bar_arrive(dempty);
+                if (a.dbg && s == 0 && cta == 0 && grp == 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) a.dbg[(q * 32 + lane) * 16 + i] = va[i];
+                }
+                if (NCH > 1) {
+                    bar_wait(dfull + 8u * (1 % ND), par[1 % ND]);
+                    par[1 % ND] ^= 1u;
+                    tc_fence_after();
+                    tmem_ld16_async(tlane + (uint32_t)(dstride * (1 % ND)), vb);
+                }
+                residues(va, rr[0]);
+                probes(rr[0], ww[0]);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    uint32_t(&vc)[16] = (c & 1) ? vb : va;  // cohort c: consumed, reused for c + 2
+                    uint32_t(&vn)[16] = (c & 1) ? va : vb;  // cohort c + 1: in flight
+                    const int b1 = (c + 1) % ND, b2 = (c + 2) % ND;
+                    if (c + 1 < NCH) {
+                        tmem_wait_ld16(vn);
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane0) bar_arrive(dempty + 8u * b1);
+                    }
+                    if (c + 2 < NCH) {
+                        bar_wait(dfull + 8u * b2, par[b2]);
+                        par[b2] ^= 1u;
+                        tc_fence_after();
+                        tmem_ld16_async(tlane + (uint32_t)(dstride * b2), vc);
+                    }
+                    if (c + 1 < NCH) {
+                        residues(vn, rr[(c + 1) & 1]);
+                        probes(rr[(c + 1) & 1], ww[(c + 1) & 1]);
+                    }
+                    count_retire(c, rr[c & 1], ww[c & 1]);
+                }
             }
             __syncwarp();
-            if (lane0) bar_arrive(raw + S.bm_empty + 8u * ring);
+            if (lane0) bar_arrive(raw + S.bm_empty + 8u * ring);  // (the probes are volatile asm: done)
             if (++sm == NG) sm = 0;
         }
     }
@@ -590,9 +764,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
 
 static std::atomic<long long> g_calls{0};
 
-template <int NG>
+template <int NG, bool WIDE>
 static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
-    auto kern = hash_rollf_kernel<NG>;
+    auto kern = hash_rollf_kernel<NG, WIDE>;
     SFFTB_CUDA(smem_opt_in(kern, smem));
     kern<<<grid, kThreads, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
@@ -622,14 +796,13 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     if (n < min_rows || n > ((int64_t)1 << 36) || L < 1 || L > kLG * kMaxNG || M < 4096 ||
         M >= ((int64_t)1 << 22))
         return 0;
-    if (kbound < 0 || kbound >= kCoordLim) return 0;
     if (d != 4 && d != 6 && d != 8 && d != 10 && d != 12) return 0;
     if (((uintptr_t)elems & 15) != 0 || ((uintptr_t)bits & 15) != 0) return 0;
-    // x' = k.z + J M with J = kbound: 0 <= x' <= 2 kbound M
+    // fp16 mode: x' = k.z + J M with J = kbound: 0 <= x' <= 2 kbound M
     const int64_t J = std::max<int64_t>(kbound, 1);
-    const __int128 xmax = (__int128)2 * J * M;
-    if (xmax >= ((__int128)1 << 31)) return 0;
-    const int64_t JM = J * M;
+    __int128 xmax = (__int128)2 * J * M;
+    const bool f16_ok = kbound >= 0 && kbound < kCoordLim && xmax < ((__int128)1 << 31);
+    const int64_t JM = f16_ok ? J * M : 0;
     int bitsM = 0;
     while (((int64_t)1 << bitsM) < M) ++bitsM;
     // limb split c = c0 + 2^s c1 with both limbs < 2048 (fp16-exact), and
@@ -641,7 +814,7 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     const int64_t half = (int64_t)1 << 22;
     int s = -1;
     int64_t e0 = 0, T1 = 0;
-    for (int dist = 0; dist <= 11 && s < 0; ++dist) {
+    for (int dist = 0; f16_ok && dist <= 11 && s < 0; ++dist) {
         for (int sign = 0; sign < 2 && s < 0; ++sign) {
             const int st_ = (bitsM + 1) / 2 + (sign ? -dist : dist);
             if (st_ < 1 || st_ > 11 || bitsM - st_ > 11 || (sign && dist == 0)) continue;
@@ -658,7 +831,15 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
             T1 = T1_;
         }
     }
-    if (s < 0) return 0;
+    // byte mode (any kbound): x = sum of 2d limb products + the constant < 2^32
+    const bool wide = s < 0;
+    if (wide) {
+        const char* e = getenv("SFFTB_HASH_ROLLW");
+        if (e && e[0] == '0') return 0;
+        if (d > 10) return 0;  // its B operands use the tail of the loader buffers (RS = 5)
+        xmax = ((__int128)(2 * d) * 127 + 1) * (M - 1);
+        if (xmax >= ((__int128)1 << 32)) return 0;
+    }
     const int64_t W = ((M + 31) / 32 + 3) & ~int64_t(3);
     const int64_t ext = (int64_t)(((__int128)M * xmax) >> 32) + 2;
     const int64_t ext_words = (ext + 31) / 32 + 1;
@@ -689,8 +870,9 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     a.M = (uint32_t)M;
     a.negM = 0u - (uint32_t)M;
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
-    a.s = s;
-    a.pow2s = 1u << s;
+    a.wide = wide ? 1 : 0;
+    a.s = wide ? 0 : s;
+    a.pow2s = wide ? 1u : 1u << s;
     // A slots (2048, 2048, 1): limb 0 gets 2048 * 6144 = 1.5 * 2^23 and e0;
     // limb 1 gets 1.5 * 2^23 + T1 with T1 = 2048 t1h + t1l
     a.seed0[0] = 6144u;
@@ -724,21 +906,32 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     grid = (int)std::min<int64_t>(grid, a.ntiles);
     if (getenv("SFFTB_HASH_ROLL_DEBUG"))
         fprintf(stderr,
-                "hash_rollf: d=%d L=%d NG=%d s=%d kbound=%lld e0=%lld T1=%lld ext_words=%d "
+                "hash_rollf: d=%d L=%d NG=%d wide=%d s=%d kbound=%lld e0=%lld T1=%lld ext_words=%d "
                 "smem=%u grid=%d\n",
-                (int)d, (int)L, NG, s, (long long)kbound, (long long)e0, (long long)T1,
+                (int)d, (int)L, NG, (int)wide, s, (long long)kbound, (long long)e0, (long long)T1,
                 (int)ext_words, smem, grid);
     rollptx::roll_extend_kernel<0><<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
         bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
     count_launch();
     int rc = SFFTB_EINVAL;
-    switch (NG) {
-        case 1: rc = launch_ng<1>(a, smem, grid, st); break;
-        case 2: rc = launch_ng<2>(a, smem, grid, st); break;
-        case 3: rc = launch_ng<3>(a, smem, grid, st); break;
-        case 4: rc = launch_ng<4>(a, smem, grid, st); break;
-        case 5: rc = launch_ng<5>(a, smem, grid, st); break;
-        case 6: rc = launch_ng<6>(a, smem, grid, st); break;
+    if (wide) {
+        switch (NG) {
+            case 1: rc = launch_ng<1, true>(a, smem, grid, st); break;
+            case 2: rc = launch_ng<2, true>(a, smem, grid, st); break;
+            case 3: rc = launch_ng<3, true>(a, smem, grid, st); break;
+            case 4: rc = launch_ng<4, true>(a, smem, grid, st); break;
+            case 5: rc = launch_ng<5, true>(a, smem, grid, st); break;
+            case 6: rc = launch_ng<6, true>(a, smem, grid, st); break;
+        }
+    } else {
+        switch (NG) {
+            case 1: rc = launch_ng<1, false>(a, smem, grid, st); break;
+            case 2: rc = launch_ng<2, false>(a, smem, grid, st); break;
+            case 3: rc = launch_ng<3, false>(a, smem, grid, st); break;
+            case 4: rc = launch_ng<4, false>(a, smem, grid, st); break;
+            case 5: rc = launch_ng<5, false>(a, smem, grid, st); break;
+            case 6: rc = launch_ng<6, false>(a, smem, grid, st); break;
+        }
     }
     if (rc == SFFTB_OK) {
         rollf_fixup_kernel<<<4 * num_sms(), 256, 0, st>>>(a);

@@ -128,3 +128,68 @@ def test_rollf_rows_outside_the_half_range_are_redone_exactly(cuda):
     assert lib.sfftb_hash_roll_recomputed(1) == 37
     assert np.array_equal(h, want)
     assert np.array_equal(m, _mask_of(want, 20))
+
+
+@pytest.mark.parametrize("d,M,L,span,n,kb", [
+    (10, 103307, 47, 4096, 300_001, -1),       # config-4 shape, no bound given
+    (10, 103307, 47, 4096, 2_500_003, 40960),  # several births per CTA
+    (10, 103307, 48, 8191, 400_000, -1),       # all 48 slots, the whole limb range
+    (8, 20663, 31, 3000, 200_000, -1),         # 4 groups
+    (6, 65537, 12, 5000, 50_000, -1),          # 2 groups, second partly filled
+    (4, 4099, 5, 100, 70_000, 50_000),         # one group; bound too large for fp16 mode
+    (10, 103307, 47, 4096, 1000, -1),          # fewer tiles than CTAs
+    (10, 103307, 33, 2048, 250_000, -1),       # 5 groups
+])
+def test_rollf_byte_mode_bitexact(cuda, d, M, L, span, n, kb):
+    """Coordinates beyond the fp16 range (|k| < 2^13, any bound): the same
+    kernel in byte mode (tcgen05 kind::i8, three limbs per lattice, N = 24)."""
+    from paper_2006_13053_b200 import _native
+
+    rng = np.random.default_rng(d * 104729 + L + n)
+    rows = rng.integers(-span, span + 1, size=(n, d), dtype=np.int64)
+    rows[0] = span
+    rows[1] = -span
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    z[0] = M - 1
+    bits, words = _bitmaps(rng, L, M, 0.45)
+    min_hits = (L + 1) // 2
+    want = _exact_hits(rows, z, M, bits)
+    lib = _native.lib()
+    lib.sfftb_hash_roll_recomputed(1)
+    lib.sfftb_hash_rollf_calls(1)
+    h, m = _run(rows, z, M, words, min_hits, kb)
+    assert lib.sfftb_hash_rollf_calls(1) == 1
+    assert lib.sfftb_hash_roll_recomputed(1) == 0
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, min_hits))
+    h_b, m_b = _run(rows, z, M, words, min_hits, kb, rollf=False)
+    assert np.array_equal(h_b, want) and np.array_equal(m_b, m)
+
+
+def test_rollf_byte_mode_rows_outside_limb_range(cuda):
+    """|k| up to 2^62 and the range edges -2^13, 2^13 - 1 in byte mode: flagged
+    by the loaders, redone exactly by the follow-up kernel."""
+    from paper_2006_13053_b200 import _native
+
+    rng = np.random.default_rng(17)
+    d, M, L, n = 10, 103307, 47, 150_000
+    rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+    bad = rng.choice(n, size=41, replace=False)
+    rows[bad, rng.integers(0, d, size=41)] = rng.integers(8192, 1 << 62, size=41) * \
+        rng.choice([-1, 1], size=41)
+    rows[bad[0], 2] = 8192
+    rows[bad[1], 2] = -8193
+    ok = np.setdiff1d(np.arange(n), bad)[:2]
+    rows[ok[0], 5] = -8192
+    rows[ok[1], 5] = 8191
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    bits, words = _bitmaps(rng, L, M, 0.3)
+    want = _exact_hits(rows, z, M, bits)
+    lib = _native.lib()
+    lib.sfftb_hash_roll_recomputed(1)
+    lib.sfftb_hash_rollf_calls(1)
+    h, m = _run(rows, z, M, words, 20, -1)
+    assert lib.sfftb_hash_rollf_calls(1) == 1
+    assert lib.sfftb_hash_roll_recomputed(1) == 41
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, 20))
