@@ -375,18 +375,25 @@ def run_hash_arm(args, world, rank):
         hits_t = torch.empty((nl,), dtype=torch.int64, device="cuda")
         mask_t = torch.empty(((nl + 31) // 32,), dtype=torch.int32, device="cuda")
         zdev = cfg.zmat_device()
+        from paper_2006_13053_b200.detect import _kbound
+
+        kb = int(_kbound(Gs))  # the bound detect_and_compute passes (sum_j max|k_j|)
+        _native.lib().sfftb_hash_rollf_calls(1)
         for it in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record()
             _native.call("sfftb_hash_hits", rows_l.data_ptr(), nl, d, zdev.data_ptr(), 1, L, M,
-                         bits.data_ptr(), -1, _eng.min_hits_for(cfg.nu, L), hits_t.data_ptr(),
+                         bits.data_ptr(), kb, _eng.min_hits_for(cfg.nu, L), hits_t.data_ptr(),
                          mask_t.data_ptr(), _dev.stream())
             b.record()
             torch.cuda.synchronize()
             if it >= args.warmup:
                 hash_ms.append(a.elapsed_time(b))
+        rollf_calls = int(_native.lib().sfftb_hash_rollf_calls(1))
+        hash_kernel = ("hash_rollf_kernel, byte mode" if rollf_calls == args.warmup + args.steps
+                       else "hash_roll_kernel")
         hash_equal = None
         if world == 1:
             ref_hits = res._hits
@@ -476,6 +483,7 @@ def run_hash_arm(args, world, rank):
             "n_det": int(idx.size),
             "ms": max_over_ranks(statistics.mean(times), world),
             "hash_ms": max_over_ranks(statistics.mean(hash_ms), world),
+            "hash_kernel": hash_kernel, "kbound": kb,
             "path_ms": max_over_ranks(statistics.mean(path_ms), world),
             "clocks": clocks, "parity": parity, "gamma_generation_ms": gen_ms,
             "e2e_ms": max_over_ranks(statistics.mean(e2e), world),
@@ -629,13 +637,14 @@ def _fp64_frac(tflops):
 
 
 def _issue_bound(h):
-    """The rolling tensor-core hash kernel's limiter (profiles/r02/
-    hash_roll_full_details.txt): instruction issue.  The residue dot products
-    run as an exact u8 x u8 -> s32 tcgen05 GEMM; what remains per (row,
-    lattice) pair in the epilogue is 2 multiply-adds (limb recombination), a
-    multiply-high + multiply-add reduction, 2 address ops, 1 shared load and
-    2 funnel shifts, plus the row loaders: 2.1e9 warp instructions per 2^26
-    rows, 77% of the issue slots."""
+    """The rolling tensor-core hash kernel's limiters, from its ncu --set full
+    capture (profiles/r02/traffic.json carries the numbers and their source):
+    instruction issue and the shared-memory data pipe.  The residue dot
+    products run as an exact tcgen05 GEMM; what remains per (row, lattice)
+    pair in the epilogue is the limb recombination, a multiply-high +
+    multiply-add reduction, 2 address ops, 1 shared load (3.6 wavefronts on
+    average: 32 random bank addresses) and 2 funnel shifts, plus the row
+    loaders."""
     pk = _pipe_peaks()
     if not pk:
         return {}
@@ -643,29 +652,41 @@ def _issue_bound(h):
     # the CUDA-core kernel's IMAD-pipe floor (12 IMAD-pipe ops per pair), for comparison
     floor_ms = pairs * 12 / (pk["imad_lanes_per_clk_per_sm"] * pk["sms"]
                              * pk["clock_mhz"] * 1e6) * 1e3
-    return {"issue": {"warp_instructions_per_pair": 0.672,
-                      "issue_slots_busy": 0.769,
-                      "dominant_pipe": "alu 0.62, fma 0.24, lsu 0.21, tensor (imma) 0.015",
-                      "source": "profiles/r02/hash_roll_full_details.txt",
-                      "cuda_core_imad_floor_ms": round(floor_ms, 3),
-                      "note": "the all-IMAD kernel (hash_rows, SFFTB_HASH_ROLL=0) cannot go "
-                              "below its IMAD-pipe floor; the tensor-core kernel is below it "
-                              "when launch_ms < cuda_core_imad_floor_ms"}}
+    key = _hash_traffic_key(h)
+    tr = measured_traffic(key) or {}
+    out = {"cuda_core_imad_floor_ms": round(floor_ms, 3),
+           "note": "the all-IMAD kernel (hash_rows, SFFTB_HASH_ROLL=0) cannot go below its "
+                   "IMAD-pipe floor; the tensor-core kernels are below it when launch_ms < "
+                   "cuda_core_imad_floor_ms"}
+    for k in ("warp_instructions", "issue_slots_busy", "lsu_data_pipe_busy", "pipes", "source"):
+        if k in tr:
+            out[k] = tr[k]
+    if "warp_instructions" in tr and tr.get("rows") and tr.get("L"):
+        out["warp_instructions_per_pair"] = round(
+            tr["warp_instructions"] / (tr["rows"] * tr["L"]), 3)
+    return {"issue": out}
+
+
+def _hash_traffic_key(h):
+    return ("hash_rollf_kernel_byte" if h.get("hash_kernel", "").startswith("hash_rollf")
+            else "hash_roll_kernel")
 
 
 def roofline_hash(h, peak, src):
     """Algorithmic bytes of one hashing call: rows (n*8d) + int64 hits
     (n*8) + the L bitmaps (L*W*4) + the detected-row bitmask (n/8).  The
     duration is the whole sfftb_hash_hits call (CUDA events on its stream):
-    bitmap pre-kernel + hash_roll_kernel + the out-of-range repair kernel."""
+    bitmap pre-kernel + the rolling tensor-core kernel + the out-of-range
+    repair kernel."""
     n = h.get("n_local", h["n"])  # this rank's rows (all rows at N = 1)
     bytes_ = n * 8 * h["d"] + n * 8 + h["L"] * h["W"] * 4 + n // 8
     ach = bytes_ / (h["hash_ms"] * 1e-3) / 1e9
-    tr = measured_traffic("hash_roll_kernel")
+    tr = measured_traffic(_hash_traffic_key(h))
     traffic = None
     if tr and tr.get("rows") == h["n"] and tr.get("L") == h["L"] and tr.get("M") == h["M"]:
         traffic = tr["dram_read"] + tr["dram_write"]
-    return {"bound": "hbm", "kernel": "hash_roll_kernel (sfftb_hash_hits)",
+    return {"bound": "hbm", "kernel": h.get("hash_kernel", "hash_roll_kernel") +
+            " (sfftb_hash_hits)",
             "achieved": round(ach, 1),
             "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
             "algorithmic_bytes": bytes_, "peak_source": src,

@@ -256,6 +256,14 @@ static int build_plan(int64_t M, BluesteinPlan** out) {
         set_error(std::string("Bluestein plan upload: ") + cudaGetErrorString(e));
         return e == cudaErrorMemoryAllocation ? SFFTB_ENOMEM : SFFTB_ECUDA;
     }
+    // the uploads are pageable cudaMemcpy on the legacy stream: such a copy can
+    // return before its DMA has finished, and the kernels that read the tables
+    // run on non-blocking streams that do not order after the legacy stream.
+    // One-time cost per (device, M).
+    if ((e = cudaStreamSynchronize(cudaStreamLegacy)) != cudaSuccess) {
+        set_error(std::string("Bluestein plan upload: ") + cudaGetErrorString(e));
+        return SFFTB_ECUDA;
+    }
     *out = p;
     return SFFTB_OK;
 }

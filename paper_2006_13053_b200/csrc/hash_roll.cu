@@ -606,6 +606,29 @@ __global__ void __launch_bounds__(kThreads, 1) hash_roll_kernel(Args a) {
     }
 }
 
+// Keeps freed stream-ordered allocations in the device's default pool across
+// synchronisations (release threshold 64 MB) instead of returning them to the
+// driver after every call: a cudaMallocAsync after a synchronisation otherwise
+// costs ~0.2 ms of host time in front of the kernels.  Once per device.
+void keep_async_pool() {
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64)
+        std::call_once(once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                unsigned long long thr = 0;
+                if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) ==
+                        cudaSuccess &&
+                    thr < (64ull << 20)) {
+                    thr = 64ull << 20;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+            }
+        });
+}
+
 unsigned long long* recomputed_counter() {
     static unsigned long long* p = nullptr;
     static std::once_flag once;
@@ -694,27 +717,9 @@ int hash_hits_roll(const int64_t* elems, int64_t n, int64_t d, const int64_t* zm
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
     a.bits = bits;
     a.W = (int)W;
-    // stream-ordered scratch (reentrant); keep freed blocks in the device's
-    // default pool across synchronisations instead of returning them to the
-    // driver after every call
-    {
-        static std::once_flag once[64];
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev >= 0 && dev < 64)
-            std::call_once(once[dev], [dev] {
-                cudaMemPool_t pool;
-                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                    unsigned long long thr = 0;
-                    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) ==
-                            cudaSuccess &&
-                        thr < (64ull << 20)) {
-                        thr = 64ull << 20;
-                        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-                    }
-                }
-            });
-    }
+    // stream-ordered scratch (reentrant); freed blocks stay in the device's
+    // default pool across synchronisations
+    keep_async_pool();
     // per-call scratch: the extended bitmaps and, behind them, this call's
     // out-of-range flag (private to the call: concurrent calls on other
     // streams must not share it)

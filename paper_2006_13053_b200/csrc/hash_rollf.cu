@@ -777,6 +777,7 @@ static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
 
 namespace roll {
 unsigned long long* recomputed_counter();
+void keep_async_pool();
 }
 
 // Returns 1 when the fp16 rolling kernel handled the call, 0 when the shape is
@@ -883,6 +884,7 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     a.seed1[2] = (uint32_t)(T1 & 2047);
     a.bits = bits;
     a.W = (int)W;
+    roll::keep_async_pool();
     uint32_t* xbits = nullptr;
     SFFTB_CUDA(cudaMallocAsync(&xbits, ((size_t)L * Wx + 4) * sizeof(uint32_t), st));
     a.xbits = xbits;

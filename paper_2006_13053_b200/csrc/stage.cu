@@ -9,6 +9,8 @@
 // between stages.
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "../../include/sfft_b200.h"
 
@@ -100,10 +102,17 @@ int stage_spectra(const sfftb_stage_t* a, void* stream, const Marks& mark, int p
         // one transform chain per group, alternating between this stream and a
         // second one: a group's 5 passes stay in L2 and the two chains fill
         // each other's kernel tails
+        // per-device second stream and events, created once under a lock (the
+        // driver runs one arena per host thread); the events are recorded and
+        // waited on under the same lock so that two threads never interleave
+        // their record/wait pairs
+        static std::mutex split_mu;
         static cudaStream_t st2[64] = {nullptr};
         static cudaEvent_t evs[64][2];
         int dev = 0;
         SFFTB_CUDA(cudaGetDevice(&dev));
+        SFFTB_REQUIRE(dev >= 0 && dev < 64, "stage: device index out of range");
+        std::lock_guard<std::mutex> split_lock(split_mu);
         if (!st2[dev]) {
             SFFTB_CUDA(cudaStreamCreateWithFlags(&st2[dev], cudaStreamNonBlocking));
             SFFTB_CUDA(cudaEventCreateWithFlags(&evs[dev][0], cudaEventDisableTiming));
