@@ -162,13 +162,20 @@ int sfftb_nonzero_bitmap(const double *ghat, int64_t G, int64_t L, int64_t M,
  * Replaces _core.pyx:164-197 (the hit half of detect_gather).
  *
  * G == 1 sets of >= 2^21 rows with even d <= 14, L <= 60 and M <= ~1.2e5 run
- * on the tensor cores (csrc/hash_roll.cu): rows packed into tensor memory as
- * the A operand of an exact u8 x u8 -> s32 GEMM (tcgen05.mma kind::i8) against
- * per-lattice coefficient limbs, bitmaps streamed in lattice groups; exact for
- * ANY int64 rows (rows outside [-2^13, 2^13) are redone by an exact 64-bit
- * kernel; kbound is not needed).  SFFTB_HASH_ROLL=0 keeps the CUDA-core
- * kernel; SFFTB_HASH_TC=1 selects the earlier byte-GEMM kernel
- * (csrc/hash_tc.cu).
+ * on the tensor cores: rows packed into tensor memory as the A operand of an
+ * exact GEMM against per-lattice coefficient limbs, bitmaps streamed in
+ * lattice groups over the resident rows; exact for ANY int64 rows (rows
+ * outside the limb range are redone by an exact 64-bit kernel).
+ *   csrc/hash_rollf.cu (L <= 48, M <= ~1.04e5): 8 lattices per group;
+ *     kbound in [0, 2048), even d <= 12: f16 x f16 -> f32 (tcgen05.mma
+ *     kind::f16, two limbs per lattice, accumulators seeded into [2^23, 2^24)
+ *     and combined from their bit patterns by one integer multiply-add);
+ *     otherwise, even d <= 10: u8 x u8 -> s32 (kind::i8, three limbs, rows
+ *     in [-2^13, 2^13); kbound is not needed).
+ *   csrc/hash_roll.cu: the other shapes (u8 x u8 -> s32, 5 lattices per group).
+ * SFFTB_HASH_ROLL=0 keeps the CUDA-core kernel, SFFTB_HASH_ROLLF=0 /
+ * SFFTB_HASH_ROLLW=0 skip hash_rollf.cu / its byte mode; SFFTB_HASH_TC=1
+ * selects the earlier byte-GEMM kernel (csrc/hash_tc.cu).
  */
 int sfftb_hash_hits(const int64_t *elems, int64_t n, int64_t d,
                     const int64_t *zmat, int64_t G, int64_t L, int64_t M,
