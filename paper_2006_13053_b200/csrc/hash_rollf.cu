@@ -262,8 +262,10 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
                     : "=r"(l1), "=r"(h1)
                     : "r"(cur[i].z), "r"(cur[i].w));
                 bad |= (h0 | h1) | ((l0 | l1) >> 14);
-                const uint32_t p0 = (l0 & 0x3FFFu) + (l0 & 0x3F80u);
-                const uint32_t p1 = (l1 & 0x3FFFu) + (l1 & 0x3F80u);
+                // (no mask on u: a row outside the range is flagged and redone, and
+                // its garbage stays in its own lane of tensor memory)
+                const uint32_t p0 = l0 + (l0 & 0x3F80u);
+                const uint32_t p1 = l1 + (l1 & 0x3F80u);
                 w = (p1 << 16) + p0;
             } else {
                 // in range <=> k + 2048 as 64 bits < 4096
@@ -657,9 +659,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                 parw ^= 1u;
                 tc_fence_after();
                 tmem_ld24_async(tlw, v);
-                tmem_wait_ld24(v);
+                tmem_wait_ld24(v);  // .sync.aligned: every lane's load has completed
                 tc_fence_before();
-                __syncwarp();
                 if (lane0) bar_arrive(demptyw);
                 if (a.dbg && s == 0 && cta == 0 && grp == 0) {
 #pragma unroll
@@ -678,7 +679,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                     if (c + 1 < NCH) {
                         tmem_wait_ld24(v);
                         tc_fence_before();
-                        __syncwarp();
                         if (lane0) bar_arrive(demptyw);
                         residues(rr[(c + 1) & 1]);
                         probes(rr[(c + 1) & 1], ww[(c + 1) & 1]);
@@ -706,9 +706,8 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                 par[0] ^= 1u;
                 tc_fence_after();
                 tmem_ld16_async(tlane, va);
-                tmem_wait_ld16(va);
+                tmem_wait_ld16(va);  // .sync.aligned: every lane's load has completed
                 tc_fence_before();
-                __syncwarp();
                 if (lane0) bar_arrive(dempty);
                 if (a.dbg && s == 0 && cta == 0 && grp == 0) {
 #pragma unroll
@@ -730,7 +729,6 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                     if (c + 1 < NCH) {
                         tmem_wait_ld16(vn);
                         tc_fence_before();
-                        __syncwarp();
                         if (lane0) bar_arrive(dempty + 8u * b1);
                     }
                     if (c + 2 < NCH) {
