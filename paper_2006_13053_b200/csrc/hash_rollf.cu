@@ -124,6 +124,9 @@ __global__ void __launch_bounds__(256) rollf_fixup_kernel(Args a) {
         const uint32_t bit = 1u << (row & 31);
         if (hits >= a.min_hits) atomicOr(a.detmask + (row >> 5), bit);
         else atomicAnd(a.detmask + (row >> 5), ~bit);
+        // the main kernel did not write the mask: clear the bits past the last row
+        if ((nbad & 0x80000000u) && row == a.n - 1 && (a.n & 31))
+            atomicAnd(a.detmask + (row >> 5), (1u << (a.n & 31)) - 1u);
     }
 }
 
@@ -914,7 +917,14 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
         bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
     count_launch();
     int rc = SFFTB_EINVAL;
-    if (wide) {
+    if (getenv("SFFTB_HASH_ROLLF_FORCE_EXACT")) {
+        // tests: take the path of a kernel that declined the call (see probe()):
+        // every row through the exact follow-up kernel
+        const unsigned int all = kAllRows;
+        SFFTB_CUDA(cudaMemcpyAsync(a.nbad, &all, sizeof(all), cudaMemcpyHostToDevice, st));
+        SFFTB_CUDA(cudaStreamSynchronize(st));  // `all` is a stack variable
+        rc = SFFTB_OK;
+    } else if (wide) {
         switch (NG) {
             case 1: rc = launch_ng<1, true>(a, smem, grid, st); break;
             case 2: rc = launch_ng<2, true>(a, smem, grid, st); break;

@@ -193,3 +193,24 @@ def test_rollf_byte_mode_rows_outside_limb_range(cuda):
     assert lib.sfftb_hash_roll_recomputed(1) == 41
     assert np.array_equal(h, want)
     assert np.array_equal(m, _mask_of(want, 20))
+
+
+def test_rollf_declined_call_is_served_exactly(cuda, monkeypatch):
+    """The kernel leaves a call it cannot serve (its shared-memory window is not
+    where the probe immediates assume) to the exact follow-up kernel: forced
+    here, every row must come out of the 64-bit path with the same results."""
+    from paper_2006_13053_b200 import _native
+
+    rng = np.random.default_rng(23)
+    d, M, L, n = 10, 103307, 47, 20_011   # a partly filled last mask word
+    rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    bits, words = _bitmaps(rng, L, M, 0.3)
+    want = _exact_hits(rows, z, M, bits)
+    lib = _native.lib()
+    lib.sfftb_hash_roll_recomputed(1)
+    monkeypatch.setenv("SFFTB_HASH_ROLLF_FORCE_EXACT", "1")
+    h, m = _run(rows, z, M, words, 20, -1)
+    assert lib.sfftb_hash_roll_recomputed(1) == n
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, 20))
