@@ -1,16 +1,18 @@
 // K3 on the tensor cores, third design: the rolling kernel of hash_roll.cu with
-// an exact FP16 x FP16 -> FP32 GEMM for candidate sets whose coordinates are
-// small (kbound = sum_j max|k_j| known and < 2048, the case of every box and
-// hyperbolic cross of the reference's workloads).  Same semantics as
+// 8 lattices per group instead of 5 (6 groups cover L <= 48 where it needs 10:
+// fewer, larger work items per row), in two modes.  Same semantics as
 // hash_rows (hash.cu) / _core.pyx:185-197 (residue, |ghat| > theta probe,
 // hits >= nu*L); same rolling schedule, warp roles and wrap-extended bitmaps
-// as hash_roll.cu.  What changes:
+// as hash_roll.cu.
+//
+// fp16 mode -- candidate sets whose coordinates are small (kbound = sum_j
+// max|k_j| known and < 2048, the case of the boxes and hyperbolic crosses of the
+// reference's workloads): an exact FP16 x FP16 -> FP32 GEMM.
 //  * the A operand is the row itself, k_j as signed fp16 (exact for |k_j| <
 //    2048), K = 16 = d coordinates + three constant slots (2048, 2048, 1);
 //  * the 17-bit coefficients z_j mod M are split in TWO limbs c = c0 + 2^s c1
 //    (both exact in fp16), so a lattice takes two accumulator columns instead
-//    of three and a 16-column tile serves 8 lattices instead of 5: 6 lattice
-//    groups cover L <= 48 where the byte kernel needs 10;
+//    of three and a 16-column tile serves 8 lattices;
 //  * the constant slots seed every accumulator with 1.5 * 2^23 (+ kbound * M
 //    split over the two limbs, so x' = k.z + kbound M >= 0): the FP32 result
 //    lies in [2^23, 2^24), where its bit pattern is 0x4B000000 + integer.  The
@@ -18,15 +20,22 @@
 //        x' = bits1 * 2^s + bits0   (mod 2^32)
 //    exactly: ONE integer multiply-add combines the limbs straight from the raw
 //    accumulator bits (the byte kernel needs two).  Every partial sum is an
-//    integer below 2^24, so the FP32 accumulation is exact in any order;
+//    integer below 2^24, so the FP32 accumulation is exact in any order.
+// Byte mode -- coordinates in [-2^13, 2^13), any kbound: see hash_rollf_kernel.
+//
+// Both modes:
 //  * two cohorts are born per step (12 cohorts of 4 tiles for 6 groups: 6144
-//    rows resident in 384 TMEM columns + two 64-column accumulator buffers);
-//  * bitmaps stream in HALF groups (4 lattices, 16 KB slots) through a ring of
-//    three buffers; a probe address is ((r >> 3) & 0x3FFC) | buffer base with
-//    the slot as the load's immediate offset, which also bounds the address
-//    for any accumulator content.
-// Per (row, lattice) the epilogue issues IMAD (limbs), IMAD.HI + IMAD
-// (reduction), SHF + LOP3 (address), LDS, 2 funnel shifts.
+//    rows resident in 384 TMEM columns, accumulator buffers behind them);
+//  * a group's 8 bitmaps sit in 13 824-byte slots, two buffers (see Smem); a
+//    probe address is ((r >> 3) & 0x3FFC) | buffer offset with the slot and
+//    the window base as the load's immediate, which also bounds the address
+//    for any accumulator content;
+//  * the bitmap words of cohort c + 1 are requested before the bits of cohort
+//    c are counted;
+//  * rows outside the mode's range are flagged by the loaders (one vote per 32
+//    rows) and redone exactly by rollf_fixup_kernel.
+// Per (row, lattice) the epilogue issues IMAD (limbs; two in byte mode),
+// IMAD.HI + IMAD (reduction), SHF + LOP3 (address), LDS, 2 funnel shifts.
 #include <stdio.h>
 #include <stdlib.h>
 
