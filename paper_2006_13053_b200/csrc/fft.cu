@@ -821,9 +821,11 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
     double2* hi_s = lo + 64;
     const int tid = threadIdx.x;
     const int f = tid >> 4, t = tid & 15;
-    // middle passes: 192 (row, column) pairs on threads 0..191 (6 full warps)
-    const bool mid = tid < F * 12;
-    const int f2 = tid / 12, sc = tid % 12;
+    // middle passes: the 12 columns of row f on lanes t < 12 of the row's own
+    // half-warp, so that a row never leaves its warp: every exchange through the
+    // row's slot needs a warp barrier only (no CTA barrier in the tile loop)
+    const bool mid = t < 12;
+    const int f2 = f, sc = t;
     const int N = N1 * N2;
     stage(tw1, a.tw_n1, N1);
     stage(lo, a.tw_lo, 64);
@@ -833,6 +835,7 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
     const double2* hi = hi_s;
     pdl_wait();    // the predecessor's output (constant tables staged above)
     pdl_launch();
+    __syncthreads();  // the staged tables
     double2* slot = smem + f * kR192Slot;
     double2* slot2 = smem + f2 * kR192Slot;
     const int per_b = N2 / F;
@@ -844,7 +847,7 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
         double2 x[12];
 #pragma unroll
         for (int r = 0; r < 12; ++r) x[r] = row[t + 16 * r];
-        __syncthreads();  // previous tile done with the slots
+        __syncwarp();  // previous tile done with the row's slot
         // forward pass 1: radix 12 over r, twiddle w192^{t s} (powers of w^t)
         dft12<false>(x);
         {
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
 #pragma unroll
             for (int sI = 0; sI < 12; ++sI) slot[t * 13 + sI] = sI ? cmul(x[sI], p(sI)) : x[sI];
         }
-        __syncthreads();
+        __syncwarp();
         double2 u[16];
         if (mid) {
             // forward pass 2: radix 16 over t' for column sc of row f2
@@ -865,7 +868,7 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
             // inverse pass A: radix 16 over q
             dft_reg<16, true>(u);  // u[t'] = sum_q X w16^{-t' q}
         }
-        __syncthreads();  // pass-2 loads done before the slots are rewritten
+        __syncwarp();  // pass-2 loads done before the slot is rewritten
         if (mid) {
             // twiddle w192^{-t' s} from the powers of conj(w^s)
             const Pow16 p(conj_if_b(tw1[sc], true), conj_if_b(tw1[2 * sc], true),
@@ -874,7 +877,7 @@ __global__ void __launch_bounds__(256, 2) fs2_rowB192(DftArgs a, int N2_rt) {
             for (int tp = 0; tp < 16; ++tp)
                 slot2[sc * 17 + tp] = tp ? cmul(u[tp], p(tp)) : u[tp];
         }
-        __syncthreads();
+        __syncwarp();
         // inverse pass B: radix 12 over s for t' = t
 #pragma unroll
         for (int sI = 0; sI < 12; ++sI) x[sI] = slot[sI * 17 + t];

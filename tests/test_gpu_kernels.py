@@ -466,8 +466,11 @@ def test_step1_select_matches_reference_lexsort(cuda, K, nv, r, s_local, theta):
     vals = np.sort(rng.choice(np.arange(-K // 2, K // 2 + K), size=nv, replace=False))
     off = (d * nv + 1) // 2 * 2
     res = _dev.empty((off + 2 * nl,), torch.int32)
-    _native.call("sfftb_step1_select", _dev.ptr(_dev.upload(est)), nl, K,
-                 _dev.ptr(_dev.upload(vals)), nv, r, s_local, theta, _dev.ptr(res),
+    # both inputs stay referenced until the call is enqueued (a temporary freed
+    # inside the argument list hands its block to the next upload)
+    est_d, vals_d = _dev.upload(est), _dev.upload(vals)
+    _native.call("sfftb_step1_select", _dev.ptr(est_d), nl, K,
+                 _dev.ptr(vals_d), nv, r, s_local, theta, _dev.ptr(res),
                  res[off:].data_ptr(), _dev.stream())
     arr = _dev.download(res)
     present = arr[:d * nv].reshape(d, nv) != 0
