@@ -341,6 +341,20 @@ static int fs_grid(int64_t ntiles, bool rows = false) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * k));
 }
 
+// fs2_rowB192 keeps every row inside a warp (no CTA barrier in its tile loop),
+// so fewer, longer-lived CTAs pay: their warps drift apart over the tiles and
+// hide each other's load latency, and the 16 KB of tables are staged once per
+// ~3 tiles.  Measured (profiles/r02/ab_rowB192_warp_rows.txt): 6 CTAs per SM
+// 3.94-3.97 ms per reconstruction, 16 per SM 3.98-4.00 ms.
+static int fs_grid_rows192(int64_t ntiles) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        const char* e = getenv("SFFTB_FS_CTAS_ROWS");
+        per_sm = e ? std::max(1, atoi(e)) : 6;
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm));
+}
+
 template <bool C>
 __device__ __forceinline__ double2 conj_if(double2 v) {
     return C ? make_double2(v.x, -v.y) : v;
@@ -1222,7 +1236,7 @@ static int fs2_rows192(const DftArgs& a, int64_t batch, int N2, cudaStream_t st)
     const size_t sm = sizeof(double2) * (16 * kR192Slot + 192 + 64 + hi);
     DftArgs c = a;
     c.ntiles = (int64_t)(N2 / 16) * batch;
-    const int grid = fs_grid(c.ntiles, true);
+    const int grid = fs_grid_rows192(c.ntiles);
     // (a compile-time N2 spills more here and is no faster: runtime N2)
     SFFTB_CUDA(allow_smem(fs2_rowB192<>, sm));
     SFFTB_CUDA(launch_maybe_pdl(c.pdl, fs2_rowB192<>, dim3(grid), dim3(256), sm, st, c, N2));
