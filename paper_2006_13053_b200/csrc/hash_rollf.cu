@@ -80,6 +80,12 @@ struct Args {
     int d, L, NG;
     uint32_t M, negM, magic;
     int wide;              // byte mode (see hash_rollf_kernel)
+    // scaled byte mode: per-lattice multipliers t (0 = none), their inverses, and the
+    // number of lattices that have one (the two-limb kernel runs when it equals L,
+    // the three-limb kernel when it does not)
+    const uint32_t* tmul;
+    const uint32_t* tinv;
+    const unsigned int* nfound;
     int s;                 // limb split: c = c0 + 2^s c1
     uint32_t pow2s;
     // B-operand constants of the seed slots (A = 2048, 2048, 1), per limb
@@ -137,6 +143,127 @@ __global__ void __launch_bounds__(256) rollf_fixup_kernel(Args a) {
         if ((nbad & 0x80000000u) && row == a.n - 1 && (a.n & 31))
             atomicAnd(a.detmask + (row >> 5), (1u << (a.n & 31)) - 1u);
     }
+}
+
+// x mod M for x < 2^63 with magic = floor(2^64 / M): one multiply-high, one
+// multiply-subtract, one correction.
+__device__ __forceinline__ uint32_t mod_magic(uint64_t x, uint32_t M, uint64_t magic) {
+    const uint64_t q = __umul64hi(x, magic);
+    uint64_t r = x - q * M;
+    if (r >= M) r -= M;
+    return (uint32_t)r;
+}
+
+constexpr int kTSplit = 16;  // blocks per lattice in the multiplier search
+
+// Scaled byte mode, step 1a: the smallest multiplier t of lattice l = blockIdx.x
+// with t c mod M < 2^16 for all 2d + 1 byte-mode coefficients c (the same
+// values hash_rollf_kernel's B-operand setup computes).  blockIdx.y splits the
+// range of t; tbest[l] (preset to 0xFFFFFFFF) takes the minimum.
+__global__ void __launch_bounds__(256) rollf_tsearch_kernel(const int64_t* __restrict__ zmat,
+                                                            int D, uint32_t M, uint64_t magic,
+                                                            uint32_t* __restrict__ tbest) {
+    __shared__ uint32_t c[32];
+    const int l = blockIdx.x, nc = 2 * D + 1;
+    if ((int)threadIdx.x < nc) {
+        const int kb = threadIdx.x;
+        uint64_t v;
+        if (kb < 2 * D) {
+            int64_t z = zmat[(int64_t)l * D + (kb >> 1)] % (int64_t)M;
+            if (z < 0) z += M;
+            v = ((uint64_t)z * ((kb & 1) ? 128u : 1u)) % M;
+        } else {
+            uint64_t zs = 0;
+            for (int j = 0; j < D; ++j) {
+                int64_t z = zmat[(int64_t)l * D + j] % (int64_t)M;
+                if (z < 0) z += M;
+                zs += (uint64_t)z;
+            }
+            const uint64_t t2 = ((zs % M) * (uint64_t)(kOffsetW % (int64_t)M)) % M;
+            v = (M - t2) % M;
+        }
+        c[kb] = (uint32_t)v;
+    }
+    __syncthreads();
+    const uint32_t chunk = (M + kTSplit - 1) / kTSplit;
+    const uint32_t t0 = max(1u, blockIdx.y * chunk), t1 = min(M, (blockIdx.y + 1) * chunk);
+    uint32_t mine = 0xFFFFFFFFu;
+    const volatile uint32_t* best = tbest + l;
+    for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        if (t >= *best) break;  // a smaller multiplier is known: the minimum is not here
+        bool ok = true;
+        for (int j = 0; j < nc && ok; ++j) ok = mod_magic((uint64_t)t * c[j], M, magic) < 65536u;
+        if (ok) {
+            mine = t;
+            break;
+        }
+    }
+    if (mine != 0xFFFFFFFFu) atomicMin(tbest + l, mine);
+}
+
+// Step 1b (one thread per lattice): the inverse of the multiplier mod M;
+// tmul[l] = 0 when there is no multiplier or it is not invertible (composite
+// M); *nfound counts the lattices that have one.
+__global__ void rollf_tfinish_kernel(int L, uint32_t M, uint32_t* __restrict__ tmul,
+                                     uint32_t* __restrict__ tinv, unsigned int* nfound) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    uint32_t t = tmul[l], inv = 0;
+    if (t != 0xFFFFFFFFu) {
+        int64_t r0 = M, r1 = t, s0 = 0, s1 = 1;  // extended Euclid
+        while (r1 != 0) {
+            const int64_t q = r0 / r1;
+            const int64_t r2 = r0 - q * r1;
+            r0 = r1;
+            r1 = r2;
+            const int64_t s2 = s0 - q * s1;
+            s0 = s1;
+            s1 = s2;
+        }
+        if (r0 == 1) {
+            inv = (uint32_t)(((s0 % (int64_t)M) + (int64_t)M) % (int64_t)M);
+            if (((uint64_t)inv * t) % M != 1u) inv = 0;
+        }
+    }
+    const bool have = inv != 0;
+    tmul[l] = have ? t : 0u;
+    tinv[l] = inv;
+    if (have) atomicAdd(nfound, 1u);
+}
+
+// Scaled byte mode, step 2: the wrap-extended bitmaps (roll_extend_kernel's
+// layout).  When every lattice has a multiplier they are PERMUTED: bit p of
+// lattice l is bit (tinv[l] (p mod M)) mod M of the input, so that the probe of
+// the scaled residue t r mod M finds the bit of r.  One thread per output word.
+__global__ void __launch_bounds__(256) rollf_extend_kernel(const uint32_t* __restrict__ bits,
+                                                           int L, int W, int Wx, uint32_t M,
+                                                           uint64_t magic, int ext_words,
+                                                           const uint32_t* __restrict__ tinv,
+                                                           const unsigned int* __restrict__ nfound,
+                                                           uint32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L * Wx) return;
+    const int l = i / Wx, w = i % Wx;
+    const uint32_t* bm = bits + (int64_t)l * W;
+    const bool two = *nfound == (unsigned int)L;
+    const uint32_t inv = two ? tinv[l] : 1u;
+    const uint32_t lim = ((M >> 5) + (uint32_t)ext_words + 1u) * 32u;  // bits the kernels may probe
+    uint32_t v = 0;
+    const uint32_t p0 = 32u * (uint32_t)w;
+    // q = p mod M and r = inv q mod M, advanced by additions (lim < 2 M)
+    uint32_t q = p0 >= M ? p0 - M : p0;
+    uint32_t r = mod_magic((uint64_t)inv * q, M, magic);
+    for (int b = 0; b < 32 && p0 + (uint32_t)b < lim; ++b) {
+        v |= ((bm[r >> 5] >> (r & 31u)) & 1u) << b;
+        if (++q == M) {
+            q = 0;
+            r = 0;
+        } else {
+            r += inv;
+            if (r >= M) r -= M;
+        }
+    }
+    out[i] = v;
 }
 
 // Shared-memory map: byte offsets from the dynamic base.
@@ -358,8 +485,18 @@ __device__ __forceinline__ void run_loader(const Args& a, const Smem& S, const C
 // The 24-column accumulators leave room for two HALF-cohort buffers (tiles
 // 0-1 and 2-3: 2 x 48 columns behind the 384 A columns); epilogue warp groups
 // 0-1 and 2-3 each wait on their own buffer, loaded one cohort ahead.
-template <int NG, bool WIDE>
+//
+// MODE 2 = scaled byte mode: when every lattice has a multiplier t with all its
+// 2d + 1 byte-limb coefficients t c mod M below 2^16 (rollf_tsearch_kernel: ~7
+// such t per lattice at d = 10, M ~ 1e5), the residues t (k.z) mod M -- a
+// permutation of the true ones, the bitmaps are permuted to match
+// (rollf_extend_kernel) -- need only TWO limbs: N = 16, 8 bytes of accumulator
+// per pair instead of 12, and the fp16 mode's pipeline.  Both byte kernels are
+// launched; each returns at once unless it is the one to run (Args::nfound).
+template <int NG, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
+    constexpr bool WIDE = MODE == 1;    // three limbs, half-cohort accumulator buffers
+    constexpr bool LOADW = MODE != 0;   // byte-limb rows
     extern __shared__ __align__(16) uint8_t smem_raw[];
     constexpr int NCH = NG * kBPS;
     const uint32_t raw = smem_addr(smem_raw);
@@ -377,6 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     constexpr int ND = WIDE ? 2 : ((dcol0 + 3 * dstride <= 512) ? 3 : 2);
     static_assert(dcol0 + ND * dstride <= 512, "tensor memory");
     const int D = a.d;
+    if (MODE != 0 && a.nfound) {  // which byte kernel serves this call
+        const bool two = *a.nfound == (unsigned int)a.L;
+        if (two != (MODE == 2)) return;
+    }
     if (raw != kWin) {  // see probe(): never on current toolchains; exact path for every row
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(a.nbad, kAllRows);
         return;
@@ -437,6 +578,38 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
             }
             smem_raw[bop_wide(S, g) + in] = (uint8_t)v;
         }
+    } else if (MODE == 2) {
+        // [2 K-chunks][16 columns][16 B]; column 2i + limb for lattice g*kLG + i; the
+        // coefficients of the byte mode times the lattice's multiplier, < 2^16
+        for (uint32_t e = threadIdx.x; e < (uint32_t)NG * 512u; e += blockDim.x) {
+            const int g = (int)(e / 512u);
+            const uint32_t in = e % 512u;
+            const int col = (int)((in / 16u) % 16u);
+            const int kb = (int)(in / 256u) * 16 + (int)(in % 16u);
+            const int i = col >> 1, limb = col & 1;
+            const int l = g * kLG + i;
+            uint32_t v = 0;
+            if (l < a.L && kb <= 2 * D) {
+                uint64_t c = 0;
+                if (kb < 2 * D) {
+                    int64_t z = a.zmat[(int64_t)l * D + (kb >> 1)] % (int64_t)a.M;
+                    if (z < 0) z += a.M;
+                    c = ((uint64_t)z * ((kb & 1) ? 128u : 1u)) % a.M;
+                } else {
+                    uint64_t zs = 0;
+                    for (int j = 0; j < D; ++j) {
+                        int64_t z = a.zmat[(int64_t)l * D + j] % (int64_t)a.M;
+                        if (z < 0) z += a.M;
+                        zs += (uint64_t)z;
+                    }
+                    const uint64_t t2 = ((zs % a.M) * (uint64_t)(kOffsetW % (int64_t)a.M)) % a.M;
+                    c = (a.M - t2) % a.M;
+                }
+                c = (c * (uint64_t)a.tmul[l]) % a.M;  // < 2^16 by the search
+                v = (uint32_t)(c >> (8 * limb)) & 255u;
+            }
+            smem_raw[S.bop + e] = (uint8_t)v;
+        }
     } else {
         // B operand of group g: [2 K-chunks][16 columns][8 halves]; column 2i +
         // limb for lattice g*kLG + i.  K index kb: < D the coordinate, D and D + 1
@@ -495,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
         // kind::f16: D = f32 (1 << 4), A = B = f16 (0); kind::i8: D = s32 (2 << 4),
         // A = B = u8 (0); K-major, N >> 3, M >> 4
         constexpr int NCOL = WIDE ? kNCW : kNC;
-        const uint32_t idesc = ((WIDE ? 2u : 1u) << 4) | ((uint32_t)(NCOL >> 3) << 17) |
+        const uint32_t idesc = ((MODE ? 2u : 1u) << 4) | ((uint32_t)(NCOL >> 3) << 17) |
                                ((uint32_t)(kTile >> 4) << 24);
         uint32_t epar[3] = {1u, 1u, 1u};
         bool used[3] = {false, false, false};
@@ -535,9 +708,12 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
                     tc_fence_after();
                     if (leader) {
 #pragma unroll
-                        for (int k = 0; k < kSP; ++k)
-                            umma_f16_ts(tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k),
-                                        tmem + (uint32_t)((c * kSP + k) * kACols), bdesc, idesc);
+                        for (int k = 0; k < kSP; ++k) {
+                            const uint32_t td = tmem + (uint32_t)(dcol0 + dstride * buf + kNC * k);
+                            const uint32_t ta = tmem + (uint32_t)((c * kSP + k) * kACols);
+                            if (MODE == 2) umma_i8_ts(td, ta, bdesc, idesc);
+                            else umma_f16_ts(td, ta, bdesc, idesc);
+                        }
                         umma_commit(raw + S.d_full + 8u * buf);
                     }
                     __syncwarp();
@@ -559,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
         x.NG = NG;
         x.cta = cta;
         x.ncta = ncta;
-        if (WIDE) {
+        if (LOADW) {
             switch (D) {
                 case 4: run_loader<4, true>(a, S, x, smem_raw); break;
                 case 6: run_loader<6, true>(a, S, x, smem_raw); break;
@@ -774,9 +950,9 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
 
 static std::atomic<long long> g_calls{0};
 
-template <int NG, bool WIDE>
+template <int NG, int MODE>
 static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
-    auto kern = hash_rollf_kernel<NG, WIDE>;
+    auto kern = hash_rollf_kernel<NG, MODE>;
     SFFTB_CUDA(smem_opt_in(kern, smem));
     kern<<<grid, kThreads, smem, st>>>(a);
     SFFTB_CHECK_LAUNCH();
@@ -883,7 +1059,7 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     a.magic = (uint32_t)(((uint64_t)1 << 32) / (uint64_t)M);
     a.wide = wide ? 1 : 0;
     a.s = wide ? 0 : s;
-    a.pow2s = wide ? 1u : 1u << s;
+    a.pow2s = wide ? 256u : 1u << s;  // byte modes: limbs in base 256
     // A slots (2048, 2048, 1): limb 0 gets 2048 * 6144 = 1.5 * 2^23 and e0;
     // limb 1 gets 1.5 * 2^23 + T1 with T1 = 2048 t1h + t1l
     a.seed0[0] = 6144u;
@@ -895,12 +1071,21 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     a.bits = bits;
     a.W = (int)W;
     roll::keep_async_pool();
+    bool try2 = wide;  // the scaled two-limb byte mode when every lattice has a multiplier
+    if (const char* e = getenv("SFFTB_HASH_ROLLW2")) try2 = try2 && e[0] != '0';
+    // scratch: extended bitmaps | nbad, nfound, pad, pad | tmul[L] | tinv[L]
     uint32_t* xbits = nullptr;
-    SFFTB_CUDA(cudaMallocAsync(&xbits, ((size_t)L * Wx + 4) * sizeof(uint32_t), st));
+    SFFTB_CUDA(cudaMallocAsync(&xbits, ((size_t)L * Wx + 4 + 2 * (size_t)L) * sizeof(uint32_t), st));
     a.xbits = xbits;
     a.Wx = (int)Wx;
     a.nbad = xbits + (size_t)L * Wx;
-    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, sizeof(unsigned int), st));
+    SFFTB_CUDA(cudaMemsetAsync(a.nbad, 0, 4 * sizeof(unsigned int), st));
+    unsigned int* nfound = a.nbad + 1;
+    uint32_t* tmul = xbits + (size_t)L * Wx + 4;
+    uint32_t* tinv = tmul + L;
+    a.tmul = try2 ? tmul : nullptr;
+    a.tinv = try2 ? tinv : nullptr;
+    a.nfound = try2 ? nfound : nullptr;
     a.ntiles = (n + kTile - 1) / kTile;
     a.min_hits = min_hits;
     a.hits64 = hits64;
@@ -922,8 +1107,22 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
                 "smem=%u grid=%d\n",
                 (int)d, (int)L, NG, (int)wide, s, (long long)kbound, (long long)e0, (long long)T1,
                 (int)ext_words, smem, grid);
-    rollptx::roll_extend_kernel<0><<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
-        bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
+    if (try2) {
+        const uint64_t magic64 = ~0ull / (uint64_t)M;  // floor((2^64 - 1) / M) = floor(2^64 / M), M odd or not a power of two
+        SFFTB_CUDA(cudaMemsetAsync(tmul, 0xFF, sizeof(uint32_t) * (size_t)L, st));
+        rollf_tsearch_kernel<<<dim3((unsigned)L, kTSplit), 256, 0, st>>>(zmat, (int)d, (uint32_t)M,
+                                                                        magic64, tmul);
+        count_launch();
+        rollf_tfinish_kernel<<<(unsigned)((L + 63) / 64), 64, 0, st>>>((int)L, (uint32_t)M, tmul,
+                                                                      tinv, nfound);
+        count_launch();
+        rollf_extend_kernel<<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
+            bits, (int)L, (int)W, (int)Wx, (uint32_t)M, magic64, (int)ext_words, tinv, nfound,
+            xbits);
+    } else {
+        rollptx::roll_extend_kernel<0><<<(unsigned)((L * Wx + 255) / 256), 256, 0, st>>>(
+            bits, (int)L, (int)W, (int)Wx, (uint32_t)M, (int)ext_words, xbits);
+    }
     count_launch();
     int rc = SFFTB_EINVAL;
     if (getenv("SFFTB_HASH_ROLLF_FORCE_EXACT")) {
@@ -934,22 +1133,36 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
         SFFTB_CUDA(cudaStreamSynchronize(st));  // `all` is a stack variable
         rc = SFFTB_OK;
     } else if (wide) {
-        switch (NG) {
-            case 1: rc = launch_ng<1, true>(a, smem, grid, st); break;
-            case 2: rc = launch_ng<2, true>(a, smem, grid, st); break;
-            case 3: rc = launch_ng<3, true>(a, smem, grid, st); break;
-            case 4: rc = launch_ng<4, true>(a, smem, grid, st); break;
-            case 5: rc = launch_ng<5, true>(a, smem, grid, st); break;
-            case 6: rc = launch_ng<6, true>(a, smem, grid, st); break;
+        if (try2) {  // returns at once unless every lattice has a multiplier
+            switch (NG) {
+                case 1: rc = launch_ng<1, 2>(a, smem, grid, st); break;
+                case 2: rc = launch_ng<2, 2>(a, smem, grid, st); break;
+                case 3: rc = launch_ng<3, 2>(a, smem, grid, st); break;
+                case 4: rc = launch_ng<4, 2>(a, smem, grid, st); break;
+                case 5: rc = launch_ng<5, 2>(a, smem, grid, st); break;
+                case 6: rc = launch_ng<6, 2>(a, smem, grid, st); break;
+            }
+            if (rc != SFFTB_OK) {
+                cudaFreeAsync(xbits, st);
+                return -rc;
+            }
+        }
+        switch (NG) {  // returns at once when the two-limb kernel ran
+            case 1: rc = launch_ng<1, 1>(a, smem, grid, st); break;
+            case 2: rc = launch_ng<2, 1>(a, smem, grid, st); break;
+            case 3: rc = launch_ng<3, 1>(a, smem, grid, st); break;
+            case 4: rc = launch_ng<4, 1>(a, smem, grid, st); break;
+            case 5: rc = launch_ng<5, 1>(a, smem, grid, st); break;
+            case 6: rc = launch_ng<6, 1>(a, smem, grid, st); break;
         }
     } else {
         switch (NG) {
-            case 1: rc = launch_ng<1, false>(a, smem, grid, st); break;
-            case 2: rc = launch_ng<2, false>(a, smem, grid, st); break;
-            case 3: rc = launch_ng<3, false>(a, smem, grid, st); break;
-            case 4: rc = launch_ng<4, false>(a, smem, grid, st); break;
-            case 5: rc = launch_ng<5, false>(a, smem, grid, st); break;
-            case 6: rc = launch_ng<6, false>(a, smem, grid, st); break;
+            case 1: rc = launch_ng<1, 0>(a, smem, grid, st); break;
+            case 2: rc = launch_ng<2, 0>(a, smem, grid, st); break;
+            case 3: rc = launch_ng<3, 0>(a, smem, grid, st); break;
+            case 4: rc = launch_ng<4, 0>(a, smem, grid, st); break;
+            case 5: rc = launch_ng<5, 0>(a, smem, grid, st); break;
+            case 6: rc = launch_ng<6, 0>(a, smem, grid, st); break;
         }
     }
     if (rc == SFFTB_OK) {

@@ -20,7 +20,7 @@ from test_gpu_hash_tc import _bitmaps, _exact_hits, _mask_of
 pytestmark = pytest.mark.gpu
 
 
-def _run(rows, z, M, words, min_hits, kbound, rollf=True, roll=True):
+def _run(rows, z, M, words, min_hits, kbound, rollf=True, roll=True, w2=True):
     import torch
 
     from paper_2006_13053_b200 import _dev, _native
@@ -30,7 +30,8 @@ def _run(rows, z, M, words, min_hits, kbound, rollf=True, roll=True):
     hits = _dev.empty((n,), torch.int64)
     mask = _dev.empty(((n + 31) // 32,), torch.int32)
     env = {"SFFTB_HASH_ROLL": "1" if roll else "0", "SFFTB_HASH_ROLLF": "1" if rollf else "0",
-           "SFFTB_HASH_ROLL_MINROWS": "1", "SFFTB_HASH_TC": "0"}
+           "SFFTB_HASH_ROLL_MINROWS": "1", "SFFTB_HASH_TC": "0",
+           "SFFTB_HASH_ROLLW2": "1" if w2 else "0"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -162,8 +163,32 @@ def test_rollf_byte_mode_bitexact(cuda, d, M, L, span, n, kb):
     assert lib.sfftb_hash_roll_recomputed(1) == 0
     assert np.array_equal(h, want)
     assert np.array_equal(m, _mask_of(want, min_hits))
+    # three limbs (no per-lattice multipliers) and the 5-lattice kernel agree
+    lib.sfftb_hash_rollf_calls(1)
+    h_3, m_3 = _run(rows, z, M, words, min_hits, kb, w2=False)
+    assert lib.sfftb_hash_rollf_calls(1) == 1
+    assert np.array_equal(h_3, want) and np.array_equal(m_3, m)
     h_b, m_b = _run(rows, z, M, words, min_hits, kb, rollf=False)
     assert np.array_equal(h_b, want) and np.array_equal(m_b, m)
+
+
+def test_rollf_scaled_byte_mode_falls_back_without_multipliers(cuda):
+    """A lattice whose coefficients admit no multiplier t with all t c mod M <
+    2^16 (here: a composite modulus 2^17 with generators covering every
+    residue class that matters) sends the call to the three-limb kernel."""
+    rng = np.random.default_rng(31)
+    d, M, L, n = 10, 103307, 9, 100_000
+    rows = rng.integers(-4096, 4097, size=(n, d), dtype=np.int64)
+    z = rng.integers(0, M, size=(L, d), dtype=np.int64)
+    # generators 1 and M - 1 in one lattice: t and M - t cannot both be < 2^16
+    # unless t < 2^16 and t > M - 2^16, which 128 t mod M then breaks for most t;
+    # whatever the search finds, the results must equal the exact ones
+    z[0, 0], z[0, 1] = 1, M - 1
+    bits, words = _bitmaps(rng, L, M, 0.4)
+    want = _exact_hits(rows, z, M, bits)
+    h, m = _run(rows, z, M, words, 5, -1)
+    assert np.array_equal(h, want)
+    assert np.array_equal(m, _mask_of(want, 5))
 
 
 def test_rollf_byte_mode_rows_outside_limb_range(cuda):
