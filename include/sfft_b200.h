@@ -170,8 +170,11 @@ int sfftb_nonzero_bitmap(const double *ghat, int64_t G, int64_t L, int64_t M,
  *     kbound in [0, 2048), even d <= 12: f16 x f16 -> f32 (tcgen05.mma
  *     kind::f16, two limbs per lattice, accumulators seeded into [2^23, 2^24)
  *     and combined from their bit patterns by one integer multiply-add);
- *     otherwise, even d <= 10: u8 x u8 -> s32 (kind::i8, three limbs, rows
- *     in [-2^13, 2^13); kbound is not needed).
+ *     otherwise, even d <= 10: u8 x u8 -> s32 (kind::i8, rows in [-2^13,
+ *     2^13); kbound is not needed) -- two limbs per lattice on residues scaled
+ *     by a per-lattice multiplier against bitmaps permuted to match when every
+ *     lattice has such a multiplier (found on the device per call), three
+ *     limbs otherwise (SFFTB_HASH_ROLLW2=0 forces three).
  *   csrc/hash_roll.cu: the other shapes (u8 x u8 -> s32, 5 lattices per group).
  * SFFTB_HASH_ROLL=0 keeps the CUDA-core kernel, SFFTB_HASH_ROLLF=0 /
  * SFFTB_HASH_ROLLW=0 skip hash_rollf.cu / its byte mode; SFFTB_HASH_TC=1
@@ -194,6 +197,11 @@ int64_t sfftb_hash_roll_recomputed(int reset);
  * single group, n >= 2^21, kbound = sum_j max|k_j| < 2048, even d <= 12,
  * L <= 48) since the last reset; for tests and the bench's kernel label. */
 int64_t sfftb_hash_rollf_calls(int reset);
+
+/* Of those, the calls its scaled two-limb byte kernel served (every lattice had
+ * a multiplier t with all byte-limb coefficients t c mod M < 2^16); synchronous,
+ * for tests and the bench's kernel label. */
+int64_t sfftb_hash_rollf_scaled_runs(int reset);
 
 /*
  * Ascending indices of set bits per group: idx[g*n + k], counts[g].

@@ -54,6 +54,7 @@ _SIGS = {
     "sfftb_hash_tc_recomputed": (_i64, [_int]),
     "sfftb_hash_roll_recomputed": (_i64, [_int]),
     "sfftb_hash_rollf_calls": (_i64, [_int]),
+    "sfftb_hash_rollf_scaled_runs": (_i64, [_int]),
     "sfftb_compact_workspace_bytes": (_i64, [_i64, _i64]),
     "sfftb_compact_mask": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
     "sfftb_medians": (_int, [_p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _p]),

@@ -86,6 +86,7 @@ struct Args {
     const uint32_t* tmul;
     const uint32_t* tinv;
     const unsigned int* nfound;
+    unsigned long long* scaled_runs;  // launches the two-limb kernel served (persistent counter)
     int s;                 // limb split: c = c0 + 2^s c1
     uint32_t pow2s;
     // B-operand constants of the seed slots (A = 2048, 2048, 1), per limb
@@ -517,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
     if (MODE != 0 && a.nfound) {  // which byte kernel serves this call
         const bool two = *a.nfound == (unsigned int)a.L;
         if (two != (MODE == 2)) return;
+        if (MODE == 2 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.scaled_runs, 1ull);
     }
     if (raw != kWin) {  // see probe(): never on current toolchains; exact path for every row
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(a.nbad, kAllRows);
@@ -950,6 +952,18 @@ __global__ void __launch_bounds__(kThreads, 1) hash_rollf_kernel(Args a) {
 
 static std::atomic<long long> g_calls{0};
 
+static unsigned long long* scaled_counter() {
+    static unsigned long long* p = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaMalloc(&p, sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(p, 0, sizeof(unsigned long long));
+        else
+            p = nullptr;
+    });
+    return p;
+}
+
 template <int NG, int MODE>
 static int launch_ng(Args& a, uint32_t smem, int grid, cudaStream_t st) {
     auto kern = hash_rollf_kernel<NG, MODE>;
@@ -1086,6 +1100,8 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
     a.tmul = try2 ? tmul : nullptr;
     a.tinv = try2 ? tinv : nullptr;
     a.nfound = try2 ? nfound : nullptr;
+    a.scaled_runs = scaled_counter();
+    if (!a.scaled_runs) try2 = false, a.tmul = a.tinv = nullptr, a.nfound = nullptr;
     a.ntiles = (n + kTile - 1) / kTile;
     a.min_hits = min_hits;
     a.hits64 = hits64;
@@ -1186,6 +1202,15 @@ int hash_hits_rollf(const int64_t* elems, int64_t n, int64_t d, const int64_t* z
 }
 
 }  // namespace sfftb
+
+extern "C" int64_t sfftb_hash_rollf_scaled_runs(int reset) {
+    unsigned long long* p = sfftb::rollf::scaled_counter();
+    if (!p) return -1;
+    unsigned long long v = 0;
+    if (cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (reset) cudaMemset(p, 0, sizeof(v));
+    return (int64_t)v;
+}
 
 extern "C" int64_t sfftb_hash_rollf_calls(int reset) {
     return reset ? sfftb::rollf::g_calls.exchange(0) : sfftb::rollf::g_calls.load();

@@ -158,8 +158,13 @@ def test_rollf_byte_mode_bitexact(cuda, d, M, L, span, n, kb):
     lib = _native.lib()
     lib.sfftb_hash_roll_recomputed(1)
     lib.sfftb_hash_rollf_calls(1)
+    lib.sfftb_hash_rollf_scaled_runs(1)
     h, m = _run(rows, z, M, words, min_hits, kb)
     assert lib.sfftb_hash_rollf_calls(1) == 1
+    scaled = lib.sfftb_hash_rollf_scaled_runs(1)
+    assert scaled in (0, 1)   # 1: every lattice had a multiplier (the two-limb kernel ran)
+    if M < 65536:
+        assert scaled == 1    # t = 1 serves: every coefficient is below 2^16 already
     assert lib.sfftb_hash_roll_recomputed(1) == 0
     assert np.array_equal(h, want)
     assert np.array_equal(m, _mask_of(want, min_hits))
@@ -167,6 +172,7 @@ def test_rollf_byte_mode_bitexact(cuda, d, M, L, span, n, kb):
     lib.sfftb_hash_rollf_calls(1)
     h_3, m_3 = _run(rows, z, M, words, min_hits, kb, w2=False)
     assert lib.sfftb_hash_rollf_calls(1) == 1
+    assert lib.sfftb_hash_rollf_scaled_runs(1) == 0
     assert np.array_equal(h_3, want) and np.array_equal(m_3, m)
     h_b, m_b = _run(rows, z, M, words, min_hits, kb, rollf=False)
     assert np.array_equal(h_b, want) and np.array_equal(m_b, m)
