@@ -640,6 +640,14 @@ def _fp64_frac(tflops):
             "fp64_peak_source": "measured DFMA peak (profiles/r01/pipe_peaks.json)"}
 
 
+def arm_config(world):
+    """The `config` object of the bench line, shared verbatim by both arms."""
+    return {"workload": WORKLOAD,
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": "flushed (256 MB write) between timed steps",
+            "value_semantics": "seconds per reconstruction (replicas: step time / N)"}
+
+
 def _issue_bound(h):
     """The rolling tensor-core hash kernel's limiters, from its ncu --set full
     capture (profiles/r02/traffic.json carries the numbers and their source):
@@ -828,10 +836,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MB write) between timed steps",
-                   "value_semantics": "seconds per reconstruction (replicas: step time / N)"},
+        "config": arm_config(world),
         "parity": r["parity"],
         "e2e": {"value": round(r["e2e_ms"] / 1e3 / world, 6), "unit": "s",
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
@@ -1031,7 +1036,9 @@ def reference_arm(args, rank, world, workers):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(value * 1e3, 1), "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD},
+           # our arm's config verbatim (the driver compares the two objects); its
+           # parallelism / l2 keys describe the GPU arm's measurement
+           "config": arm_config(world),
            "cpu_baseline": {"value": round(value, 4), "unit": "s", "cores": workers, "kind": kind,
                             "extrapolated": False, "algorithm_matched": True,
                             "sample": (f"per step: the whole metric instance ({samples} samples, "
