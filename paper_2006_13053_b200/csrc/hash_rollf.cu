@@ -21,7 +21,13 @@
 //    exactly: ONE integer multiply-add combines the limbs straight from the raw
 //    accumulator bits (the byte kernel needs two).  Every partial sum is an
 //    integer below 2^24, so the FP32 accumulation is exact in any order.
-// Byte mode -- coordinates in [-2^13, 2^13), any kbound: see hash_rollf_kernel.
+// Byte modes -- coordinates in [-2^13, 2^13), any kbound (see hash_rollf_kernel):
+// byte limbs of the rows against THREE base-256 limbs of the coefficients (kind::i8,
+// N = 24), or -- the default when every lattice has a multiplier t with all its
+// coefficients t c mod M below 2^16 -- TWO limbs on the residues scaled by t against
+// bitmaps permuted to match (N = 16, the fp16 mode's pipeline).  The three-limb
+// kernel is bound by its tensor-memory reads (12 B per pair at 63 of 64 B/clk), the
+// two-limb kernel by the shared-memory data pipe (the random bitmap probes).
 //
 // Both modes:
 //  * two cohorts are born per step (12 cohorts of 4 tiles for 6 groups: 6144
@@ -34,7 +40,7 @@
 //    c are counted;
 //  * rows outside the mode's range are flagged by the loaders (one vote per 32
 //    rows) and redone exactly by rollf_fixup_kernel.
-// Per (row, lattice) the epilogue issues IMAD (limbs; two in byte mode),
+// Per (row, lattice) the epilogue issues IMAD (limbs; two with three limbs),
 // IMAD.HI + IMAD (reduction), SHF + LOP3 (address), LDS, 2 funnel shifts.
 #include <stdio.h>
 #include <stdlib.h>
